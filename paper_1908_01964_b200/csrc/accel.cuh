@@ -1,0 +1,178 @@
+// accel.cuh -- K2: the on-chip Algorithm 2 iteration kernel (sm_100a).
+//
+// Reference: solver_accel.hpp:183-240 (detail::run_accelerated with
+// second_stage = true), i.e. per iteration
+//   gamma = r~_h / (r~_u + r~_h rho~_aa) (+ gamma_fault)            :67-76, :213
+//   r_h   = max((gamma (r~_u + gamma |rho~_ax|^2) + beta)/(alpha+2), eps)  :134-141
+//   lambda= max((1/J) sum_t [gamma |s_ab|^2 + |s_bx - gamma conj(s_ab) rho~_ax|^2 / r~_u], eps) :143-158
+//   rho   = tau + sigma-terms / lambda_new                             :113-129
+//   r_u   = max((gamma rho_aa q + rho_xx - 2 gamma Re(rho~_ax conj rho_ax))/M, eps) :160-176
+//
+// Mapping: one CTA (CL == 1) or one thread-block cluster of CL CTAs per
+// frequency bin. Each thread owns SPT slots of the bin and keeps every
+// per-slot quantity (r_h, r_u, rho~_ax, tau_ax, s_ab*s_bx, s_bx, tau_xx, |s_bx|^2)
+// in REGISTERS for all iterations: HBM is touched once to load (56 B/slot) and
+// once to store (16 B/slot). The only cross-slot dependency -- lambda's sum over
+// frames -- is a fixed-order warp butterfly + block reduction (+ DSMEM exchange
+// across the cluster), so results are deterministic and independent of how
+// many GPUs the bins are sharded over.
+//
+// Per slot-iteration the FP64 work is ~38 DP instructions for 47 canonical
+// flops; the two divisions of the reference share one MUFU reciprocal:
+// inv = 1/(D r~_u) gives gamma = r~_h r~_u inv and 1/r~_u = D inv.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+
+namespace rcscm {
+
+struct AccelArgs {
+  int64_t nb;
+  int64_t J;
+  int iters;
+  double inv_M;
+  double k1;  // 1 / (alpha + 2)
+  double k2;  // beta / (alpha + 2)
+  double eps;
+  double gamma_fault;
+  const double2* sigma_ab;  // [bin]
+  const double* tau_aa;     // [bin]
+  const double2* sigma_bx;  // [bin][t]
+  const double2* tau_ax;    // [bin][t]
+  const double* tau_xx;     // [bin][t]
+  double* r_h;              // [bin][t] in/out
+  double* r_u;              // [bin][t] in/out
+  double* lambda;           // [bin]    in/out
+  double* traj_r_h;         // optional [it][bin][t]
+  double* traj_r_u;
+  double* traj_lambda;      // optional [it][bin]
+};
+
+template <int SPT, int CL>
+__global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
+  namespace cg = cooperative_groups;
+  constexpr int kMaxWarps = 256 / 32;
+  __shared__ double red[2][kMaxWarps];
+  __shared__ double cl_part[2];
+  const int NT = blockDim.x;
+  const int nwarps = NT >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t bin = blockIdx.x / CL;
+  const int rank = (CL > 1) ? static_cast<int>(blockIdx.x % CL) : 0;
+  const int64_t J = P.J;
+  const int64_t Jc = (J + CL - 1) / CL;
+  const int64_t t0 = rank * Jc;
+  const int64_t t_end = min(J, t0 + Jc);
+  const int64_t base = bin * J;
+
+  const double2 sab = P.sigma_ab[bin];
+  const double s2 = cnorm(sab);  // |sigma_ab|^2
+  const double taa = P.tau_aa[bin];
+  double lam = P.lambda[bin];
+  double il = 1.0 / lam;
+  double raa = fma(s2, il, taa);  // rho_aa (solver_accel.hpp:122)
+
+  double rh[SPT], ru[SPT], txx[SPT], dd[SPT];
+  double2 rax[SPT], tax[SPT], cc[SPT], sbx[SPT];
+  bool valid[SPT];
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+    valid[k] = t < t_end;
+    const int64_t s = base + (valid[k] ? t : t0);
+    rh[k] = P.r_h[s];
+    ru[k] = P.r_u[s];
+    sbx[k] = P.sigma_bx[s];
+    tax[k] = P.tau_ax[s];
+    txx[k] = P.tau_xx[s];
+    cc[k] = cmul(sab, sbx[k]);  // sigma_ab * sigma_bx
+    dd[k] = cnorm(sbx[k]);      // |sigma_bx|^2
+    rax[k] = make_double2(fma(cc[k].x, il, tax[k].x), fma(cc[k].y, il, tax[k].y));
+  }
+
+  const double invJ = 1.0 / static_cast<double>(J);
+  for (int it = 0; it < P.iters; ++it) {
+    const int buf = it & 1;
+    double g[SPT], gq[SPT];
+    double acc_g = 0.0, acc_r = 0.0;
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const double D = fma(rh[k], raa, ru[k]);  // r~_u + r~_h rho~_aa
+      const double inv = rcp_pos(D * ru[k]);
+      const double gk = (rh[k] * inv) * ru[k] + P.gamma_fault;
+      const double iru = D * inv;  // 1 / r~_u
+      const double n2 = cnorm(rax[k]);
+      const double q = fma(gk, n2, ru[k]);
+      const double gqk = gk * q;
+      rh[k] = fmax(fma(gqk, P.k1, P.k2), P.eps);
+      // resid = s_bx - gamma conj(s_ab) rho~_ax
+      const double2 e = cmulc(sab, rax[k]);
+      const double rx = fma(-gk, e.x, sbx[k].x);
+      const double ry = fma(-gk, e.y, sbx[k].y);
+      const double rr = fma(rx, rx, ry * ry);
+      if (valid[k]) {
+        acc_g += gk;
+        acc_r = fma(rr, iru, acc_r);
+      }
+      g[k] = gk;
+      gq[k] = gqk;
+    }
+    // lambda: deterministic fixed-order reduction over the bin's frames.
+    double part = fma(s2, acc_g, acc_r);
+    part = warp_sum(part);
+    if (lane == 0) red[buf][warp] = part;
+    __syncthreads();
+    double total = 0.0;
+    for (int w = 0; w < nwarps; ++w) total += red[buf][w];
+    if constexpr (CL > 1) {
+      cg::cluster_group cluster = cg::this_cluster();
+      if (tid == 0) cl_part[buf] = total;
+      cluster.sync();
+      total = 0.0;
+#pragma unroll
+      for (int r = 0; r < CL; ++r) total += *cluster.map_shared_rank(&cl_part[buf], r);
+    }
+    lam = fmax(total * invJ, P.eps);
+    il = 1.0 / lam;
+    raa = fma(s2, il, taa);
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const double2 nax = make_double2(fma(cc[k].x, il, tax[k].x), fma(cc[k].y, il, tax[k].y));
+      const double rxx = fma(dd[k], il, txx[k]);
+      const double re = fma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
+      double val = fma(gq[k], raa, rxx);
+      val = fma(-2.0 * g[k], re, val);
+      ru[k] = fmax(val * P.inv_M, P.eps);
+      rax[k] = nax;
+    }
+    if (P.traj_r_h) {
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        if (valid[k]) {
+          const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+          const int64_t o = static_cast<int64_t>(it) * P.nb * J + base + t;
+          P.traj_r_h[o] = rh[k];
+          P.traj_r_u[o] = ru[k];
+        }
+      }
+      if (rank == 0 && tid == 0) P.traj_lambda[static_cast<int64_t>(it) * P.nb + bin] = lam;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    if (valid[k]) {
+      const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+      P.r_h[base + t] = rh[k];
+      P.r_u[base + t] = ru[k];
+    }
+  }
+  if (rank == 0 && tid == 0) P.lambda[bin] = lam;
+  if constexpr (CL > 1) {
+    // No CTA may leave while a peer can still read its cl_part via DSMEM.
+    cooperative_groups::this_cluster().sync();
+  }
+}
+
+}  // namespace rcscm

@@ -1,0 +1,71 @@
+// common.cuh -- shared device helpers for the rcscm B200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rcscm {
+
+constexpr int kMaxMics = 16;
+
+// Complex helpers on double2 (re, im).
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// conj(a) * b
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
+}
+// acc + a * b
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 acc) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+// acc + conj(a) * b
+__device__ __forceinline__ double2 cfmac(double2 a, double2 b, double2 acc) {
+  return make_double2(fma(a.x, b.x, fma(a.y, b.y, acc.x)), fma(a.x, b.y, fma(-a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double cnorm(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+
+// Reciprocal for strictly positive, normal x: MUFU.RCP64H seed refined by one
+// Newton step plus the cubic term (error ~ e0^3, far below 1 ulp for the
+// ~2^-22 seed). Replaces the IEEE division slow path in the on-chip loop.
+__device__ __forceinline__ double rcp_pos(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, fma(e, e, e), r);
+}
+
+// Device error word: the lowest failing (slot << 8 | code) wins (atomicMin),
+// so the reported failure is the first in the reference's (bin, frame) order.
+enum ErrCode : unsigned {
+  kErrNone = 0,
+  kErrEStepSingular = 1,   // solver_naive.hpp:207-209
+  kErrMStepSingular = 2,   // solver_naive.hpp:366-367
+  kErrNullVector = 3,      // linalg.hpp:82-84 via model.hpp:82-86 (count in bits 4..7)
+  kErrNotPsd = 4,          // linalg.hpp:41-44 via model.hpp:82-86
+  kErrObjectiveNotPd = 5,  // model.hpp:141-143
+  kErrObjectiveNonFinite = 6,  // model.hpp:151-153
+  kErrEigNoConverge = 7,   // linalg.hpp:31-32
+};
+__device__ __forceinline__ void report_error(unsigned long long* err, long long slot, unsigned code) {
+  atomicMin(err, (static_cast<unsigned long long>(slot) << 8) | code);
+}
+
+// Deterministic warp sum (xor butterfly: every lane ends with the same value).
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+}  // namespace rcscm

@@ -1,0 +1,250 @@
+// stream.cuh -- K4 Wiener output kernel, the MAP-objective kernel and the
+// reference-layout <-> device-layout transposes (sm_100a).
+#pragma once
+
+#include "common.cuh"
+
+namespace rcscm {
+
+struct WienerArgs {
+  int64_t nb, J;
+  const double2* X;         // [bin][t][m] (FROM_X or NOISE)
+  const double2* a;         // [bin][M]
+  const double2* b;         // [bin][M]          (FROM_X)
+  const double2* Rpp;       // [bin][M*M]        (FROM_X)
+  const double2* sigma_ab;  // [bin]             (!FROM_X)
+  const double* tau_aa;     // [bin]             (!FROM_X)
+  const double2* sigma_bx;  // [bin][t]          (!FROM_X)
+  const double2* tau_ax;    // [bin][t]          (!FROM_X)
+  const double* r_h;        // [bin][t]
+  const double* r_u;        // [bin][t]
+  const double* lambda;     // [bin]
+  double2* dry;             // [bin][t] (may be null)
+  double2* image;           // [bin][t][m] (may be null)
+  double2* noise;           // [bin][t][m] (NOISE)
+};
+
+// K4: multichannel Wiener filter through the scalar expansion
+// (wiener.hpp:19-43): gamma = r_h / (r_u + r_h rho_aa), s^ = gamma rho_ax,
+// image = a s^; noise = x - image (wiener.hpp:46-53). FROM_X recomputes
+// sigma_bx / tau_ax from x on the fly (the standalone API, wiener.hpp:24-26);
+// otherwise the solve's resident precompute is reused. HBM-bound.
+template <int M, int NT, bool FROM_X, bool NOISE>
+__global__ void __launch_bounds__(NT) k_wiener(WienerArgs P) {
+  __shared__ double2 sa[M];
+  __shared__ double2 sb[M];
+  __shared__ double2 sp[M];
+  __shared__ double sbin[4];  // rho_aa, Re/Im(sigma_ab * inv_lam) ... see below
+  const int64_t bin = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid < M) {
+    sa[tid] = P.a[bin * M + tid];
+    if (FROM_X) {
+      sb[tid] = P.b[bin * M + tid];
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = 0; k < M; ++k) s = cfma(P.Rpp[bin * M * M + tid + k * M], P.a[bin * M + k], s);
+      sp[tid] = s;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double2 sab;
+    double taa;
+    if (FROM_X) {
+      double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);
+      for (int k = 0; k < M; ++k) {
+        ab = cfmac(sa[k], sb[k], ab);
+        aa = cfmac(sa[k], sp[k], aa);
+      }
+      sab = ab;
+      taa = fmax(aa.x, 0.0);
+    } else {
+      sab = P.sigma_ab[bin];
+      taa = P.tau_aa[bin];
+    }
+    const double inv_lam = 1.0 / P.lambda[bin];
+    sbin[0] = taa + cnorm(sab) * inv_lam;
+    sbin[1] = sab.x;
+    sbin[2] = sab.y;
+    sbin[3] = inv_lam;
+  }
+  __syncthreads();
+  const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + tid;
+  if (t >= P.J) return;
+  const int64_t slot = bin * P.J + t;
+  const double raa = sbin[0];
+  const double2 sab = make_double2(sbin[1], sbin[2]);
+  const double inv_lam = sbin[3];
+  double2 x[M];
+  double2 sbx, tax;
+  if (FROM_X || NOISE) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) x[m] = P.X[slot * M + m];
+  }
+  if (FROM_X) {
+    sbx = make_double2(0.0, 0.0);
+    tax = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      sbx = cfmac(sb[m], x[m], sbx);
+      tax = cfmac(sp[m], x[m], tax);
+    }
+  } else {
+    sbx = P.sigma_bx[slot];
+    tax = P.tau_ax[slot];
+  }
+  const double2 c = cmul(sab, sbx);
+  const double2 rax = make_double2(fma(c.x, inv_lam, tax.x), fma(c.y, inv_lam, tax.y));
+  const double rh = P.r_h[slot], ru = P.r_u[slot];
+  const double gamma = rh / fma(rh, raa, ru);
+  const double2 s = cscale(rax, gamma);
+  if (P.dry) P.dry[slot] = s;
+  if (P.image || NOISE) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const double2 img = cmul(sa[m], s);
+      if (P.image) P.image[slot * M + m] = img;
+      if (NOISE) P.noise[slot * M + m] = csub(x[m], img);
+    }
+  }
+}
+
+// K5: MAP objective (model.hpp:129-157), one thread per slot with an in-register
+// complex Cholesky of R_x = r_h a a^H + r_u (R' + lambda b b^H); per-CTA partial
+// sums are written in fixed order and reduced by k_sum_partials.
+struct ObjArgs {
+  int64_t nb, J;
+  double alpha, beta;
+  const double2* X;
+  const double2* a;
+  const double2* b;
+  const double2* Rp;
+  const double* r_h;
+  const double* r_u;
+  const double* lambda;
+  double* partial;  // [gridDim.x][gridDim.y]
+  unsigned long long* err;
+};
+
+template <int M, int NT>
+__global__ void __launch_bounds__(NT) k_objective(ObjArgs P) {
+  __shared__ double2 sa[M];
+  __shared__ double2 sRu[M * M];
+  __shared__ double red[NT / 32];
+  const int64_t bin = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid < M) sa[tid] = P.a[bin * M + tid];
+  const double lam = P.lambda[bin];
+  for (int k = tid; k < M * M; k += NT) {
+    const int r = k % M, c = k / M;
+    sRu[k] = cadd(P.Rp[bin * M * M + k], cmul(cscale(P.b[bin * M + r], lam), cconj(P.b[bin * M + c])));
+  }
+  __syncthreads();
+  const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + tid;
+  double val = 0.0;
+  if (t < P.J) {
+    const int64_t slot = bin * P.J + t;
+    const double rh = P.r_h[slot], ru = P.r_u[slot];
+    double2 L[M * M];
+    bool ok = true;
+    double logdet = M * log(3.14159265358979323846);
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
+      double xk = fma(rh, cnorm(sa[k]), ru * sRu[k + k * M].x);
+#pragma unroll
+      for (int j = 0; j < k; ++j) xk -= cnorm(L[k + j * M]);
+      if (!(xk > 0.0)) ok = false;
+      const double lkk = sqrt(fmax(xk, 1e-300));
+      L[k + k * M] = make_double2(lkk, 0.0);
+      logdet += 2.0 * log(lkk);
+#pragma unroll
+      for (int i = k + 1; i < M; ++i) {
+        const double2 rxi = cadd(cscale(cmul(sa[i], cconj(sa[k])), rh), cscale(sRu[i + k * M], ru));
+        double2 s = rxi;
+#pragma unroll
+        for (int j = 0; j < k; ++j) s = csub(s, cmul(L[i + j * M], cconj(L[k + j * M])));
+        L[i + k * M] = cscale(s, 1.0 / lkk);
+      }
+    }
+    if (!ok) {
+      report_error(P.err, slot, kErrObjectiveNotPd);
+    } else {
+      // quad = x^H R_x^{-1} x = |L^{-1} x|^2
+      double2 y[M];
+      double quad = 0.0;
+#pragma unroll
+      for (int i = 0; i < M; ++i) {
+        double2 s = P.X[slot * M + i];
+#pragma unroll
+        for (int j = 0; j < i; ++j) s = csub(s, cmul(L[i + j * M], y[j]));
+        y[i] = cscale(s, 1.0 / L[i + i * M].x);
+        quad += cnorm(y[i]);
+      }
+      val = -logdet - quad - (P.alpha + 1.0) * log(rh) - P.beta / rh;
+      if (!isfinite(val)) report_error(P.err, slot, kErrObjectiveNonFinite);
+    }
+  }
+  val = warp_sum(val);
+  if ((tid & 31) == 0) red[tid >> 5] = val;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+    P.partial[blockIdx.x * static_cast<int64_t>(gridDim.y) + blockIdx.y] = s;
+  }
+}
+
+// Deterministic single-CTA sum of n partials (fixed strided order + tree).
+__global__ void k_sum_partials(const double* partial, int64_t n, double* out) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s += partial[k];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+    *out = tot;
+  }
+}
+
+// Reference I x J column-major (element (i, t) at i + t*I) -> device [i][t]
+// (element at i*J + t), per utterance block of I bins. 32 x 32 smem tiles.
+template <typename T>
+__global__ void k_ij_to_bt(const T* __restrict__ src, T* __restrict__ dst, int64_t I, int64_t J) {
+  __shared__ T tile[32][33];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, t0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t u = blockIdx.z;
+  const T* s = src + u * I * J;
+  T* d = dst + u * I * J;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, t = t0 + k;
+    if (i < I && t < J) tile[k][threadIdx.x] = s[i + t * I];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t i = i0 + k, t = t0 + threadIdx.x;
+    if (i < I && t < J) d[i * J + t] = tile[threadIdx.x][k];
+  }
+}
+
+template <typename T>
+__global__ void k_bt_to_ij(const T* __restrict__ src, T* __restrict__ dst, int64_t I, int64_t J) {
+  __shared__ T tile[32][33];
+  const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, t0 = static_cast<int64_t>(blockIdx.y) * 32;
+  const int64_t u = blockIdx.z;
+  const T* s = src + u * I * J;
+  T* d = dst + u * I * J;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t i = i0 + k, t = t0 + threadIdx.x;
+    if (i < I && t < J) tile[k][threadIdx.x] = s[i * J + t];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int64_t i = i0 + threadIdx.x, t = t0 + k;
+    if (i < I && t < J) d[i + t * I] = tile[threadIdx.x][k];
+  }
+}
+
+}  // namespace rcscm

@@ -1,0 +1,464 @@
+#!/usr/bin/env python
+"""Benchmark of the rcscm hot path on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1], the single-GPU config the metric is quoted
+on): one utterance, M = 4 mics, I = 1025 bins, J = 640 frames, 100 iterations of
+the accelerated rule (Algorithm 2, solver_accel.hpp:254), complex128. Synthetic
+inputs from the BASELINE recipe (paper_1908_01964_b200/synth.py), seed
+1000 * 1 + rank, generated once on the host.
+
+A step = run_algorithm2 on the device with its inputs resident in HBM:
+restore params0 -> sigma/tau precompute (K1) -> 100 on-chip iterations (K2).
+value  = B * I * J * iters * n_gpus / (max-over-ranks device time per step).
+e2e    = the same metric through the C ABI entry point rcscm_gpu_run_algorithm2
+         with pinned host buffers in the reference layout (H2D of X, inputs and
+         params0, D2H of r_h, r_u, lambda inside the timed region).
+naive  = the naive rule (solver_naive.hpp:412) on the same resident inputs.
+--impl reference runs the oracle port (the reference's CPU algorithm,
+restated in oracle/; the reference itself needs Eigen and cannot be built here).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = 1
+FLOPS_ACCEL = 47.0  # canonical flops per slot-iteration
+FLOPS_NAIVE = {2: 341.0, 4: 1804.0, 8: 11052.0}
+# K1 / K4 algorithmic bytes per slot (complex128): SURVEY 8(d)
+BYTES_PRE = {2: 88.0, 4: 120.0, 8: 184.0}
+BYTES_WIENER = {2: 96.0, 4: 128.0, 8: 192.0}
+NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # HGX B200 spec class
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
+
+
+def ncu_traffic(kernel_key):
+    """dram bytes per launch from the committed ncu summary (profiles/), or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def workload_config():
+    from paper_1908_01964_b200 import synth
+
+    c = synth.CONFIGS[CFG]
+    return c
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_problem(u):
+    from oracle import oracle as O
+
+    O.build()
+    inp = O.build_noise_scm(u.W, u.A, u.X, 0)
+    p0 = O.init_params(inp, u.T, u.V, u.W, u.A, u.X)
+    return O, inp, p0
+
+
+def cpu_baseline(u, c, budget_s=15.0, threads=None):
+    """Oracle port of Algorithm 2 on the host cores over a bounded sample of the
+    workload: all I bins, J frames, as many iterations as fit ~budget_s."""
+    O, inp, p0 = oracle_problem(u)
+    threads = threads or os.cpu_count() or 1
+    I, J = u.X.shape[0], u.X.shape[1]
+    t0 = time.perf_counter()
+    O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=2, threads=threads))
+    per_it = max((time.perf_counter() - t0) / 2, 1e-6)
+    iters = int(max(2, min(c["iters"], budget_s / per_it)))
+    t0 = time.perf_counter()
+    O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=iters, threads=threads))
+    dt = time.perf_counter() - t0
+    # reference-faithful single thread (solver_accel.hpp:183-240 is serial), few iterations
+    it1 = 3
+    r1 = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=it1 + 3))
+    t_single = statistics.median(r1.iter_seconds[3:]) if len(r1.iter_seconds) > 3 else r1.iter_seconds[-1]
+    return {
+        "value": I * J * iters / dt,
+        "unit": "TF-slot updates/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": f"oracle Algorithm 2, all {I} bins x {J} frames, {iters} iterations (incl. sigma/tau precompute), "
+                  f"bins split over {threads} threads; host {cpu_model()}",
+        "single_thread_value": I * J / t_single,
+        "single_thread_sample": "serial restatement of run_algorithm2 (the reference's accel2 is single-threaded), "
+                                "median per-iteration time after 3 warm-ups (metrics.hpp:43-51)",
+    }
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1908_01964_b200 import synth
+
+    c = workload_config()
+    u = synth.make_config(CFG, utterances=1)[0]
+    O, inp, p0 = oracle_problem(u)
+    threads = os.cpu_count() or 1
+    I, J = u.X.shape[0], u.X.shape[1]
+    # size each step as a bounded sample: the full config if it fits ~20 s per step
+    t0 = time.perf_counter()
+    O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=2, threads=threads))
+    per_it = max((time.perf_counter() - t0) / 2, 1e-6)
+    total_budget = 150.0
+    iters = int(max(1, min(c["iters"], total_budget / max(args.steps + args.warmup, 1) / per_it)))
+    for _ in range(args.warmup):
+        O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=iters, threads=threads))
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=iters, threads=threads))
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = I * J * iters * args.steps / tot
+    sample = (f"oracle port of Algorithm 2 (solver_accel.hpp:183-240) on the full config-1 problem "
+              f"({I} bins x {J} frames), {iters} of {c['iters']} iterations per step, bins over {threads} threads; "
+              f"host {cpu_model()}")
+    line = {
+        "impl": "reference",
+        "metric": "TF-slot updates/s (I*J*iters/s), accelerated rule (Algorithm 2)",
+        "value": value,
+        "unit": "TF-slot updates/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE recipe, seed 1001)",
+        "config": {"workload": c["name"], "M": c["M"], "I": c["I"], "J": c["J"], "iters_per_step": iters,
+                   "rule": "accel2"},
+        "cpu_baseline": {"value": value, "unit": "TF-slot updates/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "TF-slot updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (C++/Eigen) cannot be built in this image; oracle/ restates its algorithm",
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_01964_b200 import GpuContext, Hyperparams, synth
+    import paper_1908_01964_b200._capi as C
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    c = workload_config()
+    u = synth.make_config(CFG, utterances=1, seed_base=1000 * CFG + rank)[0]
+    X, W, A, T, V = synth.stack([u])
+    B, I, J, M = X.shape
+    iters = c["iters"]
+    tstream = torch.cuda.Stream(device=dev)
+    ctx = GpuContext(local, stream=tstream.cuda_stream)
+    hyper = Hyperparams()
+    ctx.session_load(X, W, A, T, V, 0)
+    ctx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
+    ctx.session_check()
+    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def flush():
+        with torch.cuda.stream(tstream):
+            l2_flush.fill_(1.0)
+
+    step_stages_a = C.STAGE_RESET | C.STAGE_PRECOMPUTE
+    step_stages_b = C.STAGE_ACCEL
+
+    # warm-up
+    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+        ctx.session_run(step_stages_a, 0, hyper)
+        ctx.session_run(step_stages_b, iters, hyper)
+    torch.cuda.synchronize(dev)
+    ctx.session_check()
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches0 = ctx.launch_count
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clk:
+        for k in range(args.steps):
+            flush()  # L2 flush between steps (outside the events)
+            e0, e1, e2 = ev[k]
+            e0.record(tstream)
+            ctx.session_run(step_stages_a, 0, hyper)
+            e1.record(tstream)
+            ctx.session_run(step_stages_b, iters, hyper)
+            e2.record(tstream)
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    launches = (ctx.launch_count - launches0) / args.steps
+    step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
+    k2_ms = [e1.elapsed_time(e2) for _, e1, e2 in ev]
+    k1_ms = [e0.elapsed_time(e1) for e0, e1, _ in ev]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    ctx.session_check()
+    slot_iters = B * I * J * iters
+    value = slot_iters * world * args.steps / (tot_ms * 1e-3)
+
+    # roofline of K2 (FP64 pipe) against the measured DFMA peak
+    tf = ctypes.c_double()
+    pm = ctypes.c_double()
+    rc = C.load().rcscm_gpu_probe_fp64(ctx.handle, ctypes.byref(tf), ctypes.byref(pm))
+    fp64_peak = tf.value if rc == 0 else NOMINAL_FP64_TFLOPS
+    k2_avg = sum(k2_ms) / len(k2_ms)
+    achieved = FLOPS_ACCEL * slot_iters / (k2_avg * 1e-3) / 1e12
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": ncu_traffic("k_accel"),
+                "kernel": "k_accel (K2, on-chip Algorithm 2 iterations)",
+                "flops_per_slot_iter": FLOPS_ACCEL, "slot_iters_per_launch": slot_iters,
+                "avg_launch_ms": k2_avg,
+                "peak_source": "measured live: DFMA probe (rcscm_gpu_probe_fp64) on this GPU; MEASURED_PEAKS.json "
+                               "has no FP64 figure",
+                "nominal_peak": NOMINAL_FP64_TFLOPS,
+                "frac_of_nominal": achieved / NOMINAL_FP64_TFLOPS}
+
+    # secondary kernels: K1 precompute and K4 wiener (HBM), naive rule (FP64)
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs", 6650.0)
+    S = B * I * J
+
+    def timed(stages, n, reps=5):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx.session_run(stages, n, hyper)
+        flush()
+        e0.record(tstream)
+        for _ in range(reps):
+            ctx.session_run(stages, n, hyper)
+        e1.record(tstream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    pre_ms = timed(C.STAGE_PRECOMPUTE, 0)
+    wie_ms = timed(C.STAGE_WIENER, 0)
+    naive_iters = c["naive_iters"]
+    naive_ms = timed(C.STAGE_RESET | C.STAGE_NAIVE, naive_iters, reps=3)
+    ctx.session_check()
+    stream_kernels = {
+        "k_slots_precompute": {"ms": pre_ms, "bytes_per_slot": BYTES_PRE.get(M), "achieved_gbs":
+                               BYTES_PRE.get(M, 0) * S / (pre_ms * 1e-3) / 1e9, "peak_gbs": hbm,
+                               "frac": BYTES_PRE.get(M, 0) * S / (pre_ms * 1e-3) / 1e9 / hbm,
+                               "note": "inputs smaller than L2 on this config; timed back-to-back after one flush"},
+        "k_wiener": {"ms": wie_ms, "bytes_per_slot": BYTES_WIENER.get(M), "achieved_gbs":
+                     BYTES_WIENER.get(M, 0) * S / (wie_ms * 1e-3) / 1e9, "peak_gbs": hbm,
+                     "frac": BYTES_WIENER.get(M, 0) * S / (wie_ms * 1e-3) / 1e9 / hbm},
+    }
+    naive = {"value": S * naive_iters / (naive_ms * 1e-3), "unit": "TF-slot updates/s", "iters": naive_iters,
+             "ms_per_run": naive_ms,
+             "achieved_tflops_canonical": FLOPS_NAIVE.get(M, 0) * S * naive_iters / (naive_ms * 1e-3) / 1e12,
+             "canonical_flops_per_slot_iter": FLOPS_NAIVE.get(M),
+             "accel_over_naive_per_iteration": (naive_ms / naive_iters) / (k2_avg / iters)}
+
+    # e2e through the C ABI with pinned host buffers (reference layout)
+    e2e = e2e_measure(ctx, u, iters, hyper, args, torch)
+
+    out = None
+    if rank == 0:
+        clocks = clk.summary()
+        cpu = cpu_baseline(u, c) if world == 1 or rank == 0 else None
+        out = {
+            "metric": "TF-slot updates/s (I*J*iters/s), accelerated rule (Algorithm 2)",
+            "value": value,
+            "unit": "TF-slot updates/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (BASELINE recipe: sinc-coherent diffuse noise + NMF-variance target, 0 dB; seed 1001+rank)",
+            "config": {"workload": c["name"], "M": M, "I": I, "J": J, "utterances_per_gpu": B, "iters": iters,
+                       "step": "reset params0 + sigma/tau precompute (K1) + 100 on-chip iterations (K2)",
+                       "l2": "flushed between steps (256 MiB write, outside the timed events)",
+                       "parallelism": f"bins sharded by utterance, {world} GPU(s), no collective in the loop"},
+            "gpu_launches": launches,
+            "breakdown_ms": {"precompute_k1": sum(k1_ms) / len(k1_ms), "accel_k2": k2_avg},
+            "roofline": roofline,
+            "stream_kernels": stream_kernels,
+            "naive": naive,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": clocks,
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    ctx.close()
+
+
+def e2e_measure(ctx, u, iters, hyper, args, torch):
+    """rcscm_gpu_run_algorithm2 with pinned host inputs/outputs (reference layout)."""
+    import paper_1908_01964_b200._capi as C
+    from oracle import oracle as O
+
+    lib = C.load()
+    inp = ctx.build_noise_scm(u.W, u.A, u.X, 0)
+    p0 = ctx.init_params(inp, u.T, u.V, u.W, u.A, u.X)
+    I, J, M = u.X.shape
+
+    def pinned(arr):
+        t = torch.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+        return t
+
+    Xp = pinned(u.X.view(np.float64))
+    ap = pinned(inp.a.view(np.float64))
+    bp = pinned(inp.b.view(np.float64))
+    rpp = pinned(np.ascontiguousarray(inp.R_prime_pinv.transpose(0, 2, 1)).view(np.float64))
+    rh0 = pinned(np.ascontiguousarray(p0.r_h.T))
+    ru0 = pinned(np.ascontiguousarray(p0.r_u.T))
+    l0 = pinned(p0.lam)
+    rh = torch.empty(I * J, dtype=torch.float64).pin_memory()
+    ru = torch.empty(I * J, dtype=torch.float64).pin_memory()
+    lam = torch.empty(I, dtype=torch.float64).pin_memory()
+    dp = lambda t: ctypes.cast(t.data_ptr(), C._dp)
+    ci = C.CInputs(I, J, M, 0, dp(ap), None, dp(rpp), dp(bp))
+    cp = C.CParams(dp(rh0), dp(ru0), dp(l0))
+    co = C.CParams(dp(rh), dp(ru), dp(lam))
+    h = C.CHyper(hyper.alpha, hyper.beta)
+    o = C.COpts(iters, 0, 0, 0.0, 1, 1e-12, 0.0)
+
+    def call():
+        rc = lib.rcscm_gpu_run_algorithm2(ctx.handle, ctypes.byref(ci), ctypes.byref(cp), ctypes.byref(h), dp(Xp),
+                                          ctypes.byref(o), ctypes.byref(co), None)
+        if rc != 0:
+            raise RuntimeError(lib.rcscm_gpu_last_error().decode())
+
+    for _ in range(max(args.warmup, 1)):
+        call()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        call()
+    dt = (time.perf_counter() - t0) / args.steps
+    h2d = (Xp.numel() + ap.numel() + bp.numel() + rpp.numel() + rh0.numel() + ru0.numel() + l0.numel()) * 8
+    d2h = (rh.numel() + ru.numel() + lam.numel()) * 8
+    return {"value": I * J * iters / dt, "unit": "TF-slot updates/s", "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
+            "path": "rcscm_gpu_run_algorithm2 (C ABI, synchronous) with pinned host buffers, host wall clock"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gpu", choices=["gpu", "reference"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

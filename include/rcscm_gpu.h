@@ -178,6 +178,11 @@ int rcscm_gpu_session_check(rcscm_gpu_ctx* ctx);
 /* The stream the context launches on (cudaStream_t as void*). */
 void* rcscm_gpu_stream(rcscm_gpu_ctx* ctx);
 
+/* ---- diagnostics ----------------------------------------------------------
+ * Measured FP64 FMA-pipe throughput of this device (independent DFMA chains on
+ * every SM), the denominator of the accel kernel's roofline fraction. */
+int rcscm_gpu_probe_fp64(rcscm_gpu_ctx* ctx, double* tflops, double* ms);
+
 #ifdef __cplusplus
 }
 #endif

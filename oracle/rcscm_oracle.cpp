@@ -313,14 +313,15 @@ static CMat rank_one_restored_inverse(const CMat& Rpp, const CVec& b, double lam
 }
 
 // Complex Cholesky (Eigen::LLT stand-in, lower triangle read). Returns false
-// when a pivot is not strictly positive, as LLT::info() != Success.
+// when a pivot is <= 0, as LLT::info() != Success (Eigen's own test, so a NaN
+// pivot is not caught here and surfaces later as a non-finite value).
 static bool llt(const CMat& A, CMat* L) {
   const int n = A.rows;
   *L = CMat(n, n);
   for (int k = 0; k < n; ++k) {
     double x = std::real(A(k, k));
     for (int j = 0; j < k; ++j) x -= std::norm((*L)(k, j));
-    if (!(x > 0.0)) return false;
+    if (x <= 0.0) return false;  // Eigen LLT test: a NaN pivot passes on
     const double lkk = std::sqrt(x);
     (*L)(k, k) = lkk;
     for (int i = k + 1; i < n; ++i) {

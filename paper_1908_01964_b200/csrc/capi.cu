@@ -933,4 +933,27 @@ int rcscm_gpu_session_check(rcscm_gpu_ctx* c) {
   });
 }
 
+int rcscm_gpu_probe_fp64(rcscm_gpu_ctx* c, double* tflops, double* ms) {
+  return guarded([&] {
+    if (!c || !tflops) fail(RCSCM_INVALID_INPUT, "probe_fp64: NULL argument");
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    constexpr int NACC = 8, NT = 256;
+    const int blocks = sms * 8, iters = 20000;
+    double* out = c->obj.get<double>(1);
+    k_fp64_probe<NACC><<<blocks, NT, 0, c->stream>>>(1.0, iters / 10, out);  // warm-up
+    c->launched();
+    CK(cudaEventRecord(c->ev0, c->stream));
+    k_fp64_probe<NACC><<<blocks, NT, 0, c->stream>>>(1.0, iters, out);
+    c->launched();
+    CK(cudaEventRecord(c->ev1, c->stream));
+    CK(cudaEventSynchronize(c->ev1));
+    float t = 0.f;
+    CK(cudaEventElapsedTime(&t, c->ev0, c->ev1));
+    const double flops = 2.0 * NACC * static_cast<double>(iters) * blocks * NT;
+    *tflops = flops / (t * 1e-3) / 1e12;
+    if (ms) *ms = t;
+  });
+}
+
 }  // extern "C"

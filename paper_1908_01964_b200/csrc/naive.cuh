@@ -130,7 +130,7 @@ __device__ __forceinline__ bool herm_pd_inverse(const double2 (&R)[M * M], doubl
       double x = R[k + k * M].x;
 #pragma unroll
       for (int j = 0; j < k; ++j) x -= cnorm(L[k + j * M]);
-      if (!(x > 0.0)) return false;
+      if (x <= 0.0) return false;  // Eigen::LLT's pivot test
       const double lkk = sqrt(x);
       dinv[k] = 1.0 / lkk;
       L[k + k * M] = make_double2(lkk, 0.0);

@@ -153,8 +153,8 @@ __global__ void __launch_bounds__(NT) k_objective(ObjArgs P) {
       double xk = fma(rh, cnorm(sa[k]), ru * sRu[k + k * M].x);
 #pragma unroll
       for (int j = 0; j < k; ++j) xk -= cnorm(L[k + j * M]);
-      if (!(xk > 0.0)) ok = false;
-      const double lkk = sqrt(fmax(xk, 1e-300));
+      if (xk <= 0.0) ok = false;  // Eigen::LLT's pivot test (NaN passes to the finiteness check)
+      const double lkk = ok ? sqrt(xk) : 1.0;
       L[k + k * M] = make_double2(lkk, 0.0);
       logdet += 2.0 * log(lkk);
 #pragma unroll
@@ -247,4 +247,25 @@ __global__ void k_bt_to_ij(const T* __restrict__ src, T* __restrict__ dst, int64
   }
 }
 
+}  // namespace rcscm
+
+namespace rcscm {
+// FP64 pipe probe: NACC independent DFMA chains per thread; each iteration
+// issues NACC DFMA (2 flops each). Used by bench.py to measure the FP64 peak
+// that K2's roofline fraction is reported against.
+template <int NACC>
+__global__ void __launch_bounds__(256) k_fp64_probe(double seed, int iters, double* out) {
+  double acc[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) acc[k] = seed + 1e-3 * (threadIdx.x + k);
+  const double m = 0.9999999, a = 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = fma(acc[k], m, a);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) s += acc[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
 }  // namespace rcscm

@@ -1,0 +1,289 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Instances: the reference's own seeded instances (make_verify_instance, the
+generator of proj/tests/ and `rcscm verify`) and the BASELINE synthetic recipe
+(paper_1908_01964_b200.synth) at sizes the oracle finishes in seconds, plus the
+full C1 configuration. Bars (tests/parity.py): <= 1e-9 elementwise relative on
+r_h, r_u, lambda after one iteration (r_u condition-aware on the synthetic
+recipe), trajectories <= 1e-8 over 50 iterations (acceptance.cpp:34-65), and
+<= 1e-6 on the Wiener output after the full iteration count.
+"""
+import numpy as np
+import pytest
+
+from parity import check_params, output_rel_err, ru_condition_scale
+
+pytestmark = pytest.mark.gpu
+
+
+def _hyper():
+    from paper_1908_01964_b200 import Hyperparams
+
+    return Hyperparams()
+
+
+def _opts(**kw):
+    from paper_1908_01964_b200 import SolverOptions
+
+    return SolverOptions(**kw)
+
+
+def _synthetic(O, cfg, I, J):
+    from paper_1908_01964_b200 import synth
+
+    u = synth.make_config(cfg, utterances=1, I=I, J=J)[0]
+    inp = O.build_noise_scm(u.W, u.A, u.X, 0)
+    p0 = O.init_params(inp, u.T, u.V, u.W, u.A, u.X)
+    return u, inp, p0
+
+
+# ---- the reference's own instances -------------------------------------------------
+@pytest.mark.parametrize("I,J,M", [(8, 16, 2), (8, 16, 3), (8, 128, 4), (64, 16, 8), (64, 128, 2), (8, 16, 1)])
+def test_verify_instances_one_iteration(O, gpu, I, J, M):
+    inp, p, X = O.make_verify_instance(I, J, M, 1000 * I + 10 * J + M)
+    for backend, fn in (("accel2", gpu.run_algorithm2), ("naive", gpu.run_naive)):
+        g = fn(inp, p, _hyper(), X, _opts(iters=1)).params
+        o = O.run(backend, inp, p, X, O.SolverOptions(iters=1)).params
+        r = check_params(g, o)
+        assert r["ok"], (backend, r)
+
+
+@pytest.mark.parametrize("I,J,M", [(8, 16, 2), (8, 16, 4), (8, 128, 3), (64, 16, 8)])
+def test_verify_grid_trajectories(O, gpu, I, J, M):
+    """cmd_verify / acceptance criterion 1: naive == accel trajectories <= 1e-8,
+    here GPU-naive vs GPU-accel vs oracle-naive over 50 iterations."""
+    inp, p, X = O.make_verify_instance(I, J, M, 7000 + M)
+    opt = _opts(iters=50, record_trajectory=True)
+    ga = gpu.run_algorithm2(inp, p, _hyper(), X, opt)
+    gn = gpu.run_naive(inp, p, _hyper(), X, opt)
+    on = O.run("naive", inp, p, X, O.SolverOptions(iters=50, record_trajectory=True))
+    assert len(ga.trajectory) == len(gn.trajectory) == 50
+    worst = 0.0
+    for k in range(50):
+        worst = max(worst, O.trajectory_distance(ga.trajectory[k], on.trajectory[k]),
+                    O.trajectory_distance(gn.trajectory[k], on.trajectory[k]),
+                    O.trajectory_distance(ga.trajectory[k], gn.trajectory[k]))
+    assert worst <= 1e-8, worst
+
+
+# ---- BASELINE synthetic recipe ------------------------------------------------------
+SYNTH = [(0, 64, 320), (1, 64, 640), (2, 6, 20000), (3, 32, 320), (4, 12, 4096), (1, 5, 17)]
+
+
+@pytest.mark.parametrize("cfg,I,J", SYNTH)
+def test_synthetic_setup_parity(O, gpu, cfg, I, J):
+    from paper_1908_01964_b200 import synth
+
+    u = synth.make_config(cfg, utterances=1, I=I, J=J)[0]
+    gi = gpu.build_noise_scm(u.W, u.A, u.X, 0)
+    oi = O.build_noise_scm(u.W, u.A, u.X, 0)
+    for f in ("a", "b", "R_prime", "R_prime_pinv"):
+        g, o = getattr(gi, f), getattr(oi, f)
+        assert np.max(np.abs(g - o)) <= 1e-9 * max(1.0, np.max(np.abs(o))), f
+    gp = gpu.init_params(oi, u.T, u.V, u.W, u.A, u.X)
+    op = O.init_params(oi, u.T, u.V, u.W, u.A, u.X)
+    assert check_params(gp, op)["ok"]
+
+
+@pytest.mark.parametrize("cfg,I,J", SYNTH)
+def test_synthetic_one_iteration(O, gpu, cfg, I, J):
+    u, inp, p0 = _synthetic(O, cfg, I, J)
+    S = ru_condition_scale(O, inp, p0, u.X)
+    for backend, fn in (("accel2", gpu.run_algorithm2), ("naive", gpu.run_naive)):
+        if backend == "naive" and J > 5000:
+            continue
+        g = fn(inp, p0, _hyper(), u.X, _opts(iters=1)).params
+        o = O.run(backend, inp, p0, u.X, O.SolverOptions(iters=1)).params
+        r = check_params(g, o, S)
+        assert r["ok"], (backend, r)
+
+
+@pytest.mark.parametrize("cfg,I,J,iters", [(0, 64, 320, 100), (1, 32, 640, 100), (2, 4, 20000, 50), (4, 8, 4096, 100)])
+def test_synthetic_output_full_iterations(O, gpu, cfg, I, J, iters):
+    """<= 1e-6 on the extracted target STFT after the full iteration count."""
+    u, inp, p0 = _synthetic(O, cfg, I, J)
+    g = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=iters)).params
+    o = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=iters)).params
+    ge = gpu.extract_target(inp, g, u.X)
+    oimg, odry = O.extract_target(inp, o, u.X)
+    assert output_rel_err(ge.dry, odry) <= 1e-6
+    assert output_rel_err(ge.image, oimg) <= 1e-6
+
+
+def test_full_c1_one_iteration_and_output(O, gpu):
+    """Full BASELINE config 1 (M=4, I=1025, J=640): GPU vs oracle."""
+    from paper_1908_01964_b200 import synth
+
+    u = synth.make_config(1, utterances=1)[0]
+    inp = O.build_noise_scm(u.W, u.A, u.X, 0)
+    p0 = O.init_params(inp, u.T, u.V, u.W, u.A, u.X)
+    S = ru_condition_scale(O, inp, p0, u.X)
+    g = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=1)).params
+    o = O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=1, threads=8)).params
+    r = check_params(g, o, S)
+    assert r["ok"], r
+    g = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=100)).params
+    o = O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=100, threads=8)).params
+    assert output_rel_err(gpu.extract_target(inp, g, u.X).dry, O.extract_target(inp, o, u.X)[1]) <= 1e-6
+
+
+# ---- known answers of the reference's tests, on the GPU path --------------------------
+def _scalar_problem():
+    from paper_1908_01964_b200 import RcscmInputs, RcscmParams
+
+    inp = RcscmInputs(np.ones((1, 1), complex), np.zeros((1, 1, 1), complex), np.zeros((1, 1, 1), complex),
+                      np.ones((1, 1), complex), 0)
+    p = RcscmParams(np.ones((1, 1)), np.ones((1, 1)), np.array([2.0]))
+    return inp, p, np.full((1, 1, 1), 3.0 + 0j)
+
+
+def test_naive_scalar_known_answer(gpu):
+    """test_solver_naive.cpp:44-58: r^ = 5/3, so r_h = (5/3 + beta)/(alpha + 2)."""
+    inp, p, X = _scalar_problem()
+    r = gpu.run_naive(inp, p, _hyper(), X, _opts(iters=1)).params
+    assert r.r_h[0, 0] == pytest.approx((5 / 3 + 1e-16) / 3.1, rel=1e-12)
+
+
+def test_iters_zero_passthrough(O, gpu):  # test_solver_accel.cpp:289-298, test_solver_naive.cpp:147-156
+    inp, p, X = O.make_verify_instance(2, 4, 3, 12)
+    for fn in (gpu.run_algorithm2, gpu.run_naive):
+        r = fn(inp, p, _hyper(), X, _opts(iters=0)).params
+        assert np.array_equal(r.r_h, p.r_h) and np.array_equal(r.r_u, p.r_u) and np.array_equal(r.lam, p.lam)
+
+
+def test_rh_zero_collapse(O, gpu):  # test_solver_naive.cpp:60-65 / test_wiener.cpp:9-15
+    inp, p, X = O.make_verify_instance(2, 6, 3, 1)
+    p.r_h[:] = 0
+    r = gpu.run_naive(inp, p, _hyper(), X, _opts(iters=1)).params
+    assert np.all(r.r_h == max(1e-16 / 3.1, 1e-12))
+    e = gpu.extract_target(inp, p, X)
+    assert np.max(np.abs(e.dry)) == 0.0 and np.max(np.abs(e.image)) == 0.0
+
+
+def test_wiener_dense_and_complement(O, gpu):  # test_wiener.cpp:31-62
+    inp, p, X = O.make_verify_instance(4, 10, 4, 3)
+    e = gpu.extract_target(inp, p, X)
+    for i in range(4):
+        a = inp.a[i]
+        Ru = inp.R_prime[i] + p.lam[i] * np.outer(inp.b[i], inp.b[i].conj())
+        for t in range(10):
+            rh = p.r_h[i, t]
+            s = rh * (a.conj() @ np.linalg.solve(rh * np.outer(a, a.conj()) + p.r_u[i, t] * Ru, X[i, t]))
+            assert abs(e.dry[i, t] - s) < 1e-9 * max(1, abs(s))
+            assert np.linalg.norm(e.image[i, t] - e.dry[i, t] * a) < 1e-12
+    noise = gpu.extract_noise(inp, p, X)
+    assert np.max(np.abs(X - e.image - noise)) == 0.0  # bitwise complement
+    oimg, odry = O.extract_target(inp, p, X)
+    assert output_rel_err(e.dry, odry) < 1e-12
+
+
+def test_wiener_noiseless_limit(O, gpu):  # test_wiener.cpp:17-29
+    inp, p, X = O.make_verify_instance(2, 4, 3, 2)
+    c = 1.5 - 0.8j
+    X = c * np.repeat(inp.a[:, None, :], 4, axis=1)
+    p.r_u[:] = 1e-14
+    p.r_h[:] = 1.0
+    assert np.max(np.abs(gpu.extract_target(inp, p, X).dry - c)) < 1e-6
+
+
+def test_gamma_fault_detected(O, gpu):  # test_solver_accel.cpp:334-349
+    inp, p, X = O.make_verify_instance(3, 8, 3, 15)
+    naive = gpu.run_naive(inp, p, _hyper(), X, _opts(iters=10, record_trajectory=True))
+    bad = gpu.run_algorithm2(inp, p, _hyper(), X, _opts(iters=10, record_trajectory=True, gamma_fault=1e-3))
+    assert max(O.trajectory_distance(a, b) for a, b in zip(naive.trajectory, bad.trajectory)) > 1e-8
+
+
+def test_objective_and_monotone(O, gpu):  # test_solver_accel.cpp:320-332, test_solver_naive.cpp:170-181
+    inp, p, X = O.make_verify_instance(4, 12, 3, 14)
+    assert gpu.map_objective(inp, p, _hyper(), X) == pytest.approx(O.map_objective(inp, p, X), rel=1e-12)
+    for fn in (gpu.run_algorithm2, gpu.run_naive):
+        obj = fn(inp, p, _hyper(), X, _opts(iters=100, compute_objective=True)).objective
+        assert len(obj) == 101
+        for k in range(1, 101):
+            assert obj[k] >= obj[k - 1] - 1e-7 * abs(obj[k - 1])
+
+
+def test_early_stop(O, gpu):  # test_solver_naive.cpp:209-218
+    inp, p, X = O.make_verify_instance(2, 6, 2, 10)
+    res = gpu.run_naive(inp, p, _hyper(), X, _opts(iters=500, compute_objective=True, rel_obj_tol=1e-6))
+    assert len(res.iter_seconds) < 500
+
+
+def test_errors(O, gpu):
+    from paper_1908_01964_b200 import InvalidInputError, NumericalError
+
+    inp, p, X = O.make_verify_instance(2, 4, 2, 19)
+    with pytest.raises(InvalidInputError):
+        gpu.run_algorithm2(inp, p, _hyper(), X, _opts(iters=-1))
+    with pytest.raises(InvalidInputError):
+        gpu.build_noise_scm(np.stack([np.eye(2)] * 2), np.stack([np.eye(2)] * 2), X, 2)
+    # identity demixing on data with no energy in channel 1 -> R' = 0: two null eigenvalues
+    X0 = X.copy()
+    X0[:, :, 1] = 0
+    with pytest.raises(InvalidInputError, match="null_eigenvector"):
+        gpu.build_noise_scm(np.stack([np.eye(2, dtype=complex)] * 2), np.stack([np.eye(2, dtype=complex)] * 2), X0, 0)
+    bad = p.r_h.copy()
+    bad[1, 2] = np.nan
+    from paper_1908_01964_b200 import RcscmParams
+
+    with pytest.raises(NumericalError, match="bin 1, frame 2"):
+        gpu.map_objective(inp, RcscmParams(bad, p.r_u, p.lam), _hyper(), X)
+    # singular R_x: r_u = 0 and r_h = 0 -> e_step singular covariance at (bin 0, frame 0)
+    z = RcscmParams(np.zeros_like(p.r_h), np.zeros_like(p.r_u), p.lam)
+    with pytest.raises(NumericalError, match="e_step: singular covariance at bin 0, frame 0"):
+        gpu.run_naive(inp, z, _hyper(), X, _opts(iters=1))
+
+
+def test_empty_and_tiny_shapes(O, gpu):
+    from paper_1908_01964_b200 import RcscmInputs, RcscmParams
+
+    e = RcscmInputs(np.zeros((0, 2), complex), np.zeros((0, 2, 2), complex), np.zeros((0, 2, 2), complex),
+                    np.zeros((0, 2), complex), 0)
+    r = gpu.run_algorithm2(e, RcscmParams(np.zeros((0, 3)), np.zeros((0, 3)), np.zeros(0)), _hyper(),
+                           np.zeros((0, 3, 2), complex), _opts(iters=3))
+    assert r.params.r_h.shape == (0, 3)
+    inp, p, X = O.make_verify_instance(3, 1, 2, 5)  # J = 1
+    for backend, fn in (("accel2", gpu.run_algorithm2), ("naive", gpu.run_naive)):
+        g = fn(inp, p, _hyper(), X, _opts(iters=5)).params
+        o = O.run(backend, inp, p, X, O.SolverOptions(iters=5)).params
+        assert O.trajectory_distance(g, o) < 1e-9
+
+
+def test_deterministic_and_shard_invariant(O, gpu):
+    """Bitwise: repeated runs, and bins solved in two shards == one launch
+    (the multi-GPU sharding argument)."""
+    from paper_1908_01964_b200 import RcscmInputs, RcscmParams
+
+    inp, p, X = O.make_verify_instance(10, 40, 4, 21)
+    full = gpu.run_algorithm2(inp, p, _hyper(), X, _opts(iters=25)).params
+    again = gpu.run_algorithm2(inp, p, _hyper(), X, _opts(iters=25)).params
+    assert np.array_equal(full.r_u, again.r_u) and np.array_equal(full.lam, again.lam)
+    parts = []
+    for sl in (slice(0, 3), slice(3, 10)):
+        pi = RcscmInputs(inp.a[sl], inp.R_prime[sl], inp.R_prime_pinv[sl], inp.b[sl], 0)
+        pp = RcscmParams(p.r_h[sl], p.r_u[sl], p.lam[sl])
+        parts.append(gpu.run_algorithm2(pi, pp, _hyper(), X[sl], _opts(iters=25)).params)
+    assert np.array_equal(np.concatenate([q.r_h for q in parts]), full.r_h)
+    assert np.array_equal(np.concatenate([q.r_u for q in parts]), full.r_u)
+    assert np.array_equal(np.concatenate([q.lam for q in parts]), full.lam)
+
+
+def test_session_pipeline_matches_entry_points(O, gpu):
+    """Device-resident pipeline (setup -> precompute -> accel -> wiener) on a
+    batch of 3 utterances equals the oracle per utterance."""
+    from paper_1908_01964_b200 import synth
+    import paper_1908_01964_b200._capi as C
+
+    utts = synth.make_config(3, utterances=3, I=16, J=64)
+    X, W, A, T, V = synth.stack(utts)
+    gpu.session_load(X, W, A, T, V, 0)
+    gpu.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL | C.STAGE_WIENER, 30)
+    gpu.session_check()
+    out = gpu.session_fetch(want_image=True)
+    for k, u in enumerate(utts):
+        inp = O.build_noise_scm(u.W, u.A, u.X, 0)
+        p0 = O.init_params(inp, u.T, u.V, u.W, u.A, u.X)
+        o = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=30)).params
+        oimg, odry = O.extract_target(inp, o, u.X)
+        assert output_rel_err(out["dry"][k], odry) <= 1e-6
+        assert output_rel_err(out["image"][k], oimg) <= 1e-6

@@ -18,7 +18,7 @@ for cfg, I, J in [(0, 64, 320), (1, 64, 640), (4, 16, 4096), (2, 8, 20000), (1, 
     p0 = ctx.init_params(inp, u.T, u.V, u.W, u.A, u.X)
     print(f"cfg{cfg} I={I} J={J}: init parity {O.trajectory_distance(p0, op0):.2e}", flush=True)
     for it in (1, 10):
-        g = ctx.run_algorithm2(oinp_to := inp, op0, hyper, u.X, SolverOptions(iters=it)).params
+        g = ctx.run_algorithm2(oinp, op0, hyper, u.X, SolverOptions(iters=it)).params
         o = O.run("accel2", oinp, op0, u.X, O.SolverOptions(iters=it)).params
         line = f"   accel iters={it} {O.trajectory_distance(g, o):.2e}"
         if J <= 4096:

@@ -267,7 +267,7 @@ def run_gpu(args):
     step_stages_b = C.STAGE_ACCEL
 
     # warm-up
-    for _ in range(max(args.warmup, 3) if args.warmup >= 3 else args.warmup):
+    for _ in range(args.warmup):
         ctx.session_run(step_stages_a, 0, hyper)
         ctx.session_run(step_stages_b, iters, hyper)
     torch.cuda.synchronize(dev)
@@ -400,7 +400,6 @@ def run_gpu(args):
 def e2e_measure(ctx, u, iters, hyper, args, torch):
     """rcscm_gpu_run_algorithm2 with pinned host inputs/outputs (reference layout)."""
     import paper_1908_01964_b200._capi as C
-    from oracle import oracle as O
 
     lib = C.load()
     inp = ctx.build_noise_scm(u.W, u.A, u.X, 0)

@@ -11,7 +11,7 @@ recipe), trajectories <= 1e-8 over 50 iterations (acceptance.cpp:34-65), and
 import numpy as np
 import pytest
 
-from parity import check_params, output_rel_err, ru_condition_scale
+from parity import check_params, naive_condition, output_rel_err, ru_condition_scale
 
 pytestmark = pytest.mark.gpu
 
@@ -89,13 +89,16 @@ def test_synthetic_setup_parity(O, gpu, cfg, I, J):
 def test_synthetic_one_iteration(O, gpu, cfg, I, J):
     u, inp, p0 = _synthetic(O, cfg, I, J)
     S = ru_condition_scale(O, inp, p0, u.X)
-    for backend, fn in (("accel2", gpu.run_algorithm2), ("naive", gpu.run_naive)):
-        if backend == "naive" and J > 5000:
-            continue
-        g = fn(inp, p0, _hyper(), u.X, _opts(iters=1)).params
-        o = O.run(backend, inp, p0, u.X, O.SolverOptions(iters=1)).params
-        r = check_params(g, o, S)
-        assert r["ok"], (backend, r)
+    g = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=1)).params
+    o = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=1)).params
+    r = check_params(g, o, S)
+    assert r["ok"], ("accel2", r)
+    if J <= 5000:
+        kappa, S_h = naive_condition(inp, p0, u.X)
+        g = gpu.run_naive(inp, p0, _hyper(), u.X, _opts(iters=1)).params
+        o = O.run("naive", inp, p0, u.X, O.SolverOptions(iters=1)).params
+        r = check_params(g, o, S, kappa=kappa, S_h=S_h)
+        assert r["ok"], ("naive", r)
 
 
 @pytest.mark.parametrize("cfg,I,J,iters", [(0, 64, 320, 100), (1, 32, 640, 100), (2, 4, 20000, 50), (4, 8, 4096, 100)])

@@ -17,9 +17,12 @@
 // across the cluster), so results are deterministic and independent of how
 // many GPUs the bins are sharded over.
 //
-// Per slot-iteration the FP64 work is ~38 DP instructions for 47 canonical
-// flops; the two divisions of the reference share one MUFU reciprocal:
-// inv = 1/(D r~_u) gives gamma = r~_h r~_u inv and 1/r~_u = D inv.
+// Instruction budget per slot-iteration (47 canonical flops): 32 FP64 ops
+// (DFMA/DMUL/DADD) + 2 floor compares + 1 MUFU.RCP64H. The reference's two
+// divisions share one reciprocal (inv = 1/(D r~_u) gives gamma = r~_h r~_u inv
+// and 1/r~_u = D inv); gamma_fault rides in an FMA; 1/M is folded into the
+// per-slot constants (exact for power-of-two M); `max(v, eps)` keeps the
+// reference's std::max semantics (v < eps ? eps : v) without fmax's NaN fix-up.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -50,7 +53,12 @@ struct AccelArgs {
   double* traj_lambda;      // optional [it][bin]
 };
 
-template <int SPT, int CL>
+// std::max(v, eps) of the reference (returns v unless v < eps).
+__device__ __forceinline__ double floor_eps(double v, double eps) { return v < eps ? eps : v; }
+
+// FULL: every thread's SPT slots are inside the bin chunk (NT * SPT == chunk),
+// so no per-slot masks. TRAJ: record r_h / r_u / lambda after every iteration.
+template <int SPT, int CL, bool FULL, bool TRAJ>
 __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
   constexpr int kMaxWarps = 256 / 32;
@@ -66,6 +74,7 @@ __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
   const int64_t t0 = rank * Jc;
   const int64_t t_end = min(J, t0 + Jc);
   const int64_t base = bin * J;
+  const double inv_M = P.inv_M;
 
   const double2 sab = P.sigma_ab[bin];
   const double s2 = cnorm(sab);  // |sigma_ab|^2
@@ -74,54 +83,57 @@ __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
   double il = 1.0 / lam;
   double raa = fma(s2, il, taa);  // rho_aa (solver_accel.hpp:122)
 
+  // per-slot state: rh, ru evolve; rax = rho~_ax carried; the rest is constant.
+  // txx and dd are pre-scaled by 1/M (exact for M = 2, 4, 8, 16).
   double rh[SPT], ru[SPT], txx[SPT], dd[SPT];
   double2 rax[SPT], tax[SPT], cc[SPT], sbx[SPT];
   bool valid[SPT];
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
     const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
-    valid[k] = t < t_end;
+    valid[k] = FULL || t < t_end;
     const int64_t s = base + (valid[k] ? t : t0);
     rh[k] = P.r_h[s];
     ru[k] = P.r_u[s];
     sbx[k] = P.sigma_bx[s];
     tax[k] = P.tau_ax[s];
-    txx[k] = P.tau_xx[s];
-    cc[k] = cmul(sab, sbx[k]);  // sigma_ab * sigma_bx
-    dd[k] = cnorm(sbx[k]);      // |sigma_bx|^2
+    txx[k] = P.tau_xx[s] * inv_M;
+    cc[k] = cmul(sab, sbx[k]);     // sigma_ab * sigma_bx
+    dd[k] = cnorm(sbx[k]) * inv_M;  // |sigma_bx|^2 / M
     rax[k] = make_double2(fma(cc[k].x, il, tax[k].x), fma(cc[k].y, il, tax[k].y));
   }
 
   const double invJ = 1.0 / static_cast<double>(J);
+  const double m2M = -2.0 * inv_M;
+  const double fault = P.gamma_fault;
   for (int it = 0; it < P.iters; ++it) {
     const int buf = it & 1;
     double g[SPT], gq[SPT];
-    double acc_g = 0.0, acc_r = 0.0;
+    double acc = 0.0;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       const double D = fma(rh[k], raa, ru[k]);  // r~_u + r~_h rho~_aa
       const double inv = rcp_pos(D * ru[k]);
-      const double gk = (rh[k] * inv) * ru[k] + P.gamma_fault;
-      const double iru = D * inv;  // 1 / r~_u
+      const double gk = fma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
+      const double iru = D * inv;                         // 1 / r~_u
       const double n2 = cnorm(rax[k]);
       const double q = fma(gk, n2, ru[k]);
       const double gqk = gk * q;
-      rh[k] = fmax(fma(gqk, P.k1, P.k2), P.eps);
+      rh[k] = floor_eps(fma(gqk, P.k1, P.k2), P.eps);
       // resid = s_bx - gamma conj(s_ab) rho~_ax
       const double2 e = cmulc(sab, rax[k]);
       const double rx = fma(-gk, e.x, sbx[k].x);
       const double ry = fma(-gk, e.y, sbx[k].y);
       const double rr = fma(rx, rx, ry * ry);
-      if (valid[k]) {
-        acc_g += gk;
-        acc_r = fma(rr, iru, acc_r);
+      if (FULL || valid[k]) {
+        acc = fma(gk, s2, acc);
+        acc = fma(rr, iru, acc);
       }
-      g[k] = gk;
+      g[k] = gk * m2M;  // -2 gamma / M
       gq[k] = gqk;
     }
     // lambda: deterministic fixed-order reduction over the bin's frames.
-    double part = fma(s2, acc_g, acc_r);
-    part = warp_sum(part);
+    double part = warp_sum(acc);
     if (lane == 0) red[buf][warp] = part;
     __syncthreads();
     double total = 0.0;
@@ -134,20 +146,21 @@ __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
 #pragma unroll
       for (int r = 0; r < CL; ++r) total += *cluster.map_shared_rank(&cl_part[buf], r);
     }
-    lam = fmax(total * invJ, P.eps);
+    lam = floor_eps(total * invJ, P.eps);
     il = 1.0 / lam;
     raa = fma(s2, il, taa);
+    const double raaM = raa * inv_M;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       const double2 nax = make_double2(fma(cc[k].x, il, tax[k].x), fma(cc[k].y, il, tax[k].y));
-      const double rxx = fma(dd[k], il, txx[k]);
+      const double rxx = fma(dd[k], il, txx[k]);                 // rho_xx / M
       const double re = fma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
-      double val = fma(gq[k], raa, rxx);
-      val = fma(-2.0 * g[k], re, val);
-      ru[k] = fmax(val * P.inv_M, P.eps);
+      double val = fma(gq[k], raaM, rxx);
+      val = fma(g[k], re, val);
+      ru[k] = floor_eps(val, P.eps);
       rax[k] = nax;
     }
-    if (P.traj_r_h) {
+    if constexpr (TRAJ) {
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         if (valid[k]) {

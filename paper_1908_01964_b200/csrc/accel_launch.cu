@@ -1,0 +1,51 @@
+// accel_launch.cu -- K2 configuration choice and dispatch.
+#include <cstdlib>
+
+#include "accel_launch.cuh"
+
+namespace rcscm {
+
+AccelCfg choose_accel_cfg(int64_t J) {
+  AccelCfg best{0, 0, 0, false};
+  const char* e_spt = std::getenv("RCSCM_ACCEL_SPT");
+  const char* e_cl = std::getenv("RCSCM_ACCEL_CL");
+  const int force_spt = e_spt ? std::atoi(e_spt) : 0;
+  const int force_cl = e_cl ? std::atoi(e_cl) : 0;
+  for (int cl : {1, 2, 4, 8, 16}) {
+    if (force_cl && cl != force_cl) continue;
+    const int64_t jc = (J + cl - 1) / cl;
+    const int max_spt = (cl == 16) ? 8 : 6;
+    if (jc > 256LL * (force_spt ? force_spt : max_spt)) continue;
+    int64_t best_waste = -1;
+    for (int spt = 1; spt <= 8; ++spt) {
+      if (force_spt ? spt != force_spt : spt > max_spt) continue;
+      int64_t nt = (jc + spt - 1) / spt;
+      nt = (nt + 31) / 32 * 32;
+      if (nt > 256) continue;
+      const int64_t waste = nt * spt - jc;
+      // least idle lanes; ties go to more slots per thread (ILP, fewer warps)
+      if (best_waste < 0 || waste < best_waste || (waste == best_waste && spt > best.spt)) {
+        best_waste = waste;
+        // FULL needs every CTA of the cluster to own exactly nt * spt frames
+        const bool full = (waste == 0) && (jc * cl == J);
+        best = AccelCfg{cl, static_cast<int>(nt), spt, full};
+      }
+    }
+    if (best.cl) return best;
+  }
+  return best;
+}
+
+cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
+  if (A.nb * A.J == 0) return cudaSuccess;
+  switch (g.cl) {
+    case 1: return launch_accel_cl1(s, A, g);
+    case 2: return launch_accel_cl2(s, A, g);
+    case 4: return launch_accel_cl4(s, A, g);
+    case 8: return launch_accel_cl8(s, A, g);
+    case 16: return launch_accel_cl16(s, A, g);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace rcscm

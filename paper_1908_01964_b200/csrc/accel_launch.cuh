@@ -1,0 +1,65 @@
+// accel_launch.cuh -- K2 launcher for one cluster size (instantiated by the
+// accel_cl*.cu translation units so the variants compile in parallel).
+#pragma once
+
+#include "launch.h"
+
+namespace rcscm {
+
+template <int SPT, int CL, bool FULL, bool TRAJ>
+cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
+  auto kern = k_accel<SPT, CL, FULL, TRAJ>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  cfg.numAttrs = 0;
+  if (CL > 1) {
+    if (CL > 8) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CL;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.numAttrs = 1;
+  }
+  cfg.attrs = attr;
+  return cudaLaunchKernelEx(&cfg, kern, A);
+}
+
+template <int CL, bool FULL, bool TRAJ>
+cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt) {
+  switch (spt) {
+    case 1: return launch_accel_t<1, CL, FULL, TRAJ>(s, A, nt);
+    case 2: return launch_accel_t<2, CL, FULL, TRAJ>(s, A, nt);
+    case 3: return launch_accel_t<3, CL, FULL, TRAJ>(s, A, nt);
+    case 4: return launch_accel_t<4, CL, FULL, TRAJ>(s, A, nt);
+    case 5: return launch_accel_t<5, CL, FULL, TRAJ>(s, A, nt);
+    case 6: return launch_accel_t<6, CL, FULL, TRAJ>(s, A, nt);
+    case 7: return launch_accel_t<7, CL, FULL, TRAJ>(s, A, nt);
+    case 8: return launch_accel_t<8, CL, FULL, TRAJ>(s, A, nt);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <int CL>
+cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
+  const bool traj = A.traj_r_h != nullptr;
+  if (traj) return launch_accel_spt<CL, false, true>(s, A, g.nt, g.spt);
+  if (g.full) return launch_accel_spt<CL, true, false>(s, A, g.nt, g.spt);
+  return launch_accel_spt<CL, false, false>(s, A, g.nt, g.spt);
+}
+
+#define RCSCM_DECLARE_ACCEL_CL(CL) \
+  cudaError_t launch_accel_cl##CL(cudaStream_t s, const AccelArgs& A, const AccelCfg& g);
+RCSCM_DECLARE_ACCEL_CL(1)
+RCSCM_DECLARE_ACCEL_CL(2)
+RCSCM_DECLARE_ACCEL_CL(4)
+RCSCM_DECLARE_ACCEL_CL(8)
+RCSCM_DECLARE_ACCEL_CL(16)
+
+}  // namespace rcscm

@@ -4,23 +4,19 @@
 // wiener.hpp) becomes: host->device copies of the caller's reference-layout
 // buffers, one transpose of the I x J column-major parameters into the
 // device's bin-major layout, the CUDA kernels, and the way back. There is no
-// CPU fallback: every numeric step runs in the kernels of setup.cuh,
-// accel.cuh, naive.cuh and stream.cuh.
+// CPU fallback: every numeric step runs in the kernels launched through
+// launch.h (setup_launch.cu, accel_launch.cu, naive_launch.cu, stream_launch.cu).
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <string>
-#include <type_traits>
 #include <vector>
 
 #include "../../include/rcscm_gpu.h"
-#include "accel.cuh"
-#include "common.cuh"
-#include "naive.cuh"
-#include "setup.cuh"
-#include "stream.cuh"
+#include "launch.h"
 
 using namespace rcscm;
 
@@ -35,9 +31,9 @@ struct ApiError {
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw ApiError{code, msg}; }
 
-#define CK(expr)                                                                     \
-  do {                                                                               \
-    cudaError_t e_ = (expr);                                                         \
+#define CK(expr)                                                                                      \
+  do {                                                                                                \
+    cudaError_t e_ = (expr);                                                                          \
     if (e_ != cudaSuccess) fail(RCSCM_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
@@ -68,20 +64,8 @@ struct DBuf {
   }
 };
 
-template <class F>
-void dispatch_m(int M, F&& f) {
-  switch (M) {
-    case 1: f(std::integral_constant<int, 1>{}); break;
-    case 2: f(std::integral_constant<int, 2>{}); break;
-    case 3: f(std::integral_constant<int, 3>{}); break;
-    case 4: f(std::integral_constant<int, 4>{}); break;
-    case 5: f(std::integral_constant<int, 5>{}); break;
-    case 6: f(std::integral_constant<int, 6>{}); break;
-    case 7: f(std::integral_constant<int, 7>{}); break;
-    case 8: f(std::integral_constant<int, 8>{}); break;
-    case 16: f(std::integral_constant<int, 16>{}); break;
-    default: fail(RCSCM_UNSUPPORTED, "mics = " + std::to_string(M) + " is not supported (1..8 or 16)");
-  }
+void check_mics(int M) {
+  if (!mics_supported(M)) fail(RCSCM_UNSUPPORTED, "mics = " + std::to_string(M) + " is not supported (1..8 or 16)");
 }
 
 }  // namespace
@@ -101,9 +85,11 @@ struct rcscm_gpu_ctx {
   int64_t sB = 0, sI = 0, sJ = 0;
   int sM = 0, sK = 0, sn_h = 0;
 
-  void launched() {
-    CK(cudaGetLastError());
-    ++launches;
+  // Every kernel launch goes through here: the error is surfaced as
+  // RCSCM_CUDA_ERROR and the launch counter (rcscm_gpu_launch_count) advances.
+  void launched(cudaError_t e, int n = 1) {
+    if (e != cudaSuccess) fail(RCSCM_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+    launches += n;
   }
 };
 
@@ -129,23 +115,10 @@ void h2d(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
 void d2h(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
   if (bytes && dst) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->stream));
 }
+void d2d(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
+}
 void sync(rcscm_gpu_ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
-
-// I x J column-major (per utterance block) <-> [bin][t]
-template <class T>
-void to_bt(rcscm_gpu_ctx* c, const T* src, T* dst, int64_t B, int64_t I, int64_t J) {
-  if (B * I * J == 0) return;
-  dim3 grid((I + 31) / 32, (J + 31) / 32, B), block(32, 8);
-  k_ij_to_bt<T><<<grid, block, 0, c->stream>>>(src, dst, I, J);
-  c->launched();
-}
-template <class T>
-void to_ij(rcscm_gpu_ctx* c, const T* src, T* dst, int64_t B, int64_t I, int64_t J) {
-  if (B * I * J == 0) return;
-  dim3 grid((I + 31) / 32, (J + 31) / 32, B), block(32, 8);
-  k_bt_to_ij<T><<<grid, block, 0, c->stream>>>(src, dst, I, J);
-  c->launched();
-}
 
 void reset_err(rcscm_gpu_ctx* c) {
   unsigned long long* e = c->err.get<unsigned long long>(1);
@@ -248,117 +221,8 @@ void alloc_problem(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M) {
   c->err.get<unsigned long long>(1);
 }
 
-constexpr int kSlotNT = 128;
-
-template <int M>
-void launch_slots(rcscm_gpu_ctx* c, const DevProblem& P, bool init, bool pre, double eps) {
-  if (P.nb * P.J == 0) return;
-  dim3 grid(P.nb, (P.J + kSlotNT - 1) / kSlotNT);
-  if (init && pre)
-    k_slots<M, kSlotNT, true, true><<<grid, kSlotNT, 0, c->stream>>>(P, eps);
-  else if (init)
-    k_slots<M, kSlotNT, true, false><<<grid, kSlotNT, 0, c->stream>>>(P, eps);
-  else
-    k_slots<M, kSlotNT, false, true><<<grid, kSlotNT, 0, c->stream>>>(P, eps);
-  c->launched();
-}
-
-template <int M>
-void launch_setup(rcscm_gpu_ctx* c, const DevProblem& P, double rank_tol, double eps) {
-  if (P.nb == 0) return;
-  k_setup_power<M, 256><<<P.nb, 256, 0, c->stream>>>(P);
-  c->launched();
-  k_setup_bin<M, 0><<<(P.nb + 63) / 64, 64, 0, c->stream>>>(P, rank_tol, eps);
-  c->launched();
-}
-
-// ---- K2 launch configuration --------------------------------------------------
-struct AccelCfg {
-  int cl, nt, spt;
-};
-
-AccelCfg choose_accel_cfg(int64_t J) {
-  AccelCfg best{0, 0, 0};
-  const char* e_spt = std::getenv("RCSCM_ACCEL_SPT");
-  const char* e_cl = std::getenv("RCSCM_ACCEL_CL");
-  const int force_spt = e_spt ? std::atoi(e_spt) : 0;
-  const int force_cl = e_cl ? std::atoi(e_cl) : 0;
-  for (int cl : {1, 2, 4, 8, 16}) {
-    if (force_cl && cl != force_cl) continue;
-    const int64_t jc = (J + cl - 1) / cl;
-    const int max_spt = (cl == 16) ? 8 : 6;
-    if (jc > 256LL * (force_spt ? force_spt : max_spt)) continue;
-    int64_t best_waste = -1;
-    for (int spt = 1; spt <= 8; ++spt) {
-      if (force_spt ? spt != force_spt : spt > max_spt) continue;
-      int64_t nt = (jc + spt - 1) / spt;
-      nt = (nt + 31) / 32 * 32;
-      if (nt > 256) continue;
-      const int64_t waste = nt * spt - jc;
-      // least idle lanes; ties go to more slots per thread (ILP, fewer warps)
-      if (best_waste < 0 || waste < best_waste || (waste == best_waste && spt > best.spt)) {
-        best_waste = waste;
-        best = AccelCfg{cl, static_cast<int>(nt), spt};
-      }
-    }
-    if (best.cl) return best;
-  }
-  fail(RCSCM_UNSUPPORTED, "frames = " + std::to_string(J) + " exceeds the on-chip accel kernel capacity (16 x 2048)");
-}
-
-template <int SPT, int CL>
-void launch_accel_t(rcscm_gpu_ctx* c, const AccelArgs& A, int nt) {
-  auto kern = k_accel<SPT, CL>;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
-  cfg.blockDim = dim3(nt);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = c->stream;
-  cudaLaunchAttribute attr[1];
-  int na = 0;
-  if (CL > 1) {
-    if (CL > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CL;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    na = 1;
-  }
-  cfg.attrs = attr;
-  cfg.numAttrs = na;
-  CK(cudaLaunchKernelEx(&cfg, kern, A));
-  c->launched();
-}
-
-template <int CL>
-void launch_accel_spt(rcscm_gpu_ctx* c, const AccelArgs& A, const AccelCfg& g) {
-  switch (g.spt) {
-    case 1: launch_accel_t<1, CL>(c, A, g.nt); break;
-    case 2: launch_accel_t<2, CL>(c, A, g.nt); break;
-    case 3: launch_accel_t<3, CL>(c, A, g.nt); break;
-    case 4: launch_accel_t<4, CL>(c, A, g.nt); break;
-    case 5: launch_accel_t<5, CL>(c, A, g.nt); break;
-    case 6: launch_accel_t<6, CL>(c, A, g.nt); break;
-    case 7: launch_accel_t<7, CL>(c, A, g.nt); break;
-    case 8: launch_accel_t<8, CL>(c, A, g.nt); break;
-    default: fail(RCSCM_UNSUPPORTED, "bad slots-per-thread");
-  }
-}
-
-void launch_accel(rcscm_gpu_ctx* c, const AccelArgs& A) {
-  if (A.nb * A.J == 0) return;
-  const AccelCfg g = choose_accel_cfg(A.J);
-  switch (g.cl) {
-    case 1: launch_accel_spt<1>(c, A, g); break;
-    case 2: launch_accel_spt<2>(c, A, g); break;
-    case 4: launch_accel_spt<4>(c, A, g); break;
-    case 8: launch_accel_spt<8>(c, A, g); break;
-    case 16: launch_accel_spt<16>(c, A, g); break;
-  }
-}
-
-AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, const rcscm_hyper& h,
-                     double eps, double gamma_fault) {
+AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, const rcscm_hyper& h, double eps,
+                     double gamma_fault) {
   AccelArgs A{};
   A.nb = nb;
   A.J = J;
@@ -379,13 +243,13 @@ AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, 
   return A;
 }
 
-constexpr int kNaiveNT = 128;
-
-template <int M>
-void launch_naive(rcscm_gpu_ctx* c, NaiveArgs N) {
-  if (N.nb * N.J == 0) return;
-  k_naive<M, kNaiveNT><<<N.nb, kNaiveNT, 0, c->stream>>>(N);
-  c->launched();
+void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A) {
+  if (A.nb * A.J == 0) return;
+  const AccelCfg g = choose_accel_cfg(A.J);
+  if (!g.cl)
+    fail(RCSCM_UNSUPPORTED,
+         "frames = " + std::to_string(A.J) + " exceeds the on-chip accel kernel capacity (16 x 2048)");
+  c->launched(launch_accel(c->stream, A, g));
 }
 
 NaiveArgs naive_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int iters, const rcscm_hyper& h, double eps) {
@@ -408,22 +272,9 @@ NaiveArgs naive_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int iters, const r
   return N;
 }
 
-constexpr int kWienerNT = 128;
-
-template <int M, bool FROM_X, bool NOISE>
-void launch_wiener(rcscm_gpu_ctx* c, const WienerArgs& W) {
-  if (W.nb * W.J == 0) return;
-  dim3 grid(W.nb, (W.J + kWienerNT - 1) / kWienerNT);
-  k_wiener<M, kWienerNT, FROM_X, NOISE><<<grid, kWienerNT, 0, c->stream>>>(W);
-  c->launched();
-}
-
 // Objective of the current device state -> host double (synchronizes).
-template <int M>
-double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, const rcscm_hyper& h) {
+double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h) {
   if (nb * J == 0) return 0.0;
-  constexpr int NT = 128;
-  dim3 grid(nb, (J + NT - 1) / NT);
   ObjArgs O{};
   O.nb = nb;
   O.J = J;
@@ -436,14 +287,12 @@ double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, const rcscm_hyper& h) 
   O.r_h = c->rh.as<double>();
   O.r_u = c->ru.as<double>();
   O.lambda = c->lam.as<double>();
-  const int64_t np = static_cast<int64_t>(grid.x) * grid.y;
-  O.partial = c->partial.get<double>(np);
+  O.partial = c->partial.get<double>(static_cast<size_t>(nb * ((J + 127) / 128)));
   O.err = c->err.as<unsigned long long>();
-  k_objective<M, NT><<<grid, NT, 0, c->stream>>>(O);
-  c->launched();
+  int64_t np = 0;
+  c->launched(launch_objective(c->stream, M, O, &np));
   double* out = c->obj.get<double>(1);
-  k_sum_partials<<<1, 1024, 0, c->stream>>>(O.partial, np, out);
-  c->launched();
+  c->launched(launch_sum_partials(c->stream, O.partial, np, out));
   double v = 0.0;
   d2h(c, &v, out, sizeof(double));
   check_err(c, J);
@@ -461,6 +310,7 @@ void validate_inputs(const rcscm_inputs* in, bool need_rp, bool need_rpp) {
     if (need_rp && !in->R_prime) fail(RCSCM_INVALID_INPUT, "inputs.R_prime must not be NULL");
     if (need_rpp && !in->R_prime_pinv) fail(RCSCM_INVALID_INPUT, "inputs.R_prime_pinv must not be NULL");
   }
+  check_mics(in->mics);
 }
 
 // Upload inputs + params0 into the context's device buffers (device layout).
@@ -476,12 +326,12 @@ void upload_model(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* 
   if (rp) h2d(c, c->Rp.p, in->R_prime, I * M * M * sizeof(double2));
   if (rpp) h2d(c, c->Rpp.p, in->R_prime_pinv, I * M * M * sizeof(double2));
   if (p) {
-    double* tmp = c->tmp.get<double>(S);
-    double* tmp2 = c->tmp2.get<double>(S);
-    h2d(c, tmp, p->r_h, S * sizeof(double));
-    h2d(c, tmp2, p->r_u, S * sizeof(double));
-    to_bt<double>(c, tmp, c->rh.as<double>(), 1, I, J);
-    to_bt<double>(c, tmp2, c->ru.as<double>(), 1, I, J);
+    double* t1 = c->tmp.get<double>(S);
+    double* t2 = c->tmp2.get<double>(S);
+    h2d(c, t1, p->r_h, S * sizeof(double));
+    h2d(c, t2, p->r_u, S * sizeof(double));
+    c->launched(launch_to_bt(c->stream, t1, c->rh.as<double>(), 1, I, J));
+    c->launched(launch_to_bt(c->stream, t2, c->ru.as<double>(), 1, I, J));
     h2d(c, c->lam.p, p->lambda, I * sizeof(double));
   }
 }
@@ -490,8 +340,8 @@ void download_params(rcscm_gpu_ctx* c, int64_t I, int64_t J, rcscm_params* out) 
   const size_t S = static_cast<size_t>(I * J);
   double* t1 = c->tmp.get<double>(S);
   double* t2 = c->tmp2.get<double>(S);
-  to_ij<double>(c, c->rh.as<double>(), t1, 1, I, J);
-  to_ij<double>(c, c->ru.as<double>(), t2, 1, I, J);
+  c->launched(launch_to_ij(c->stream, c->rh.as<double>(), t1, 1, I, J));
+  c->launched(launch_to_ij(c->stream, c->ru.as<double>(), t2, 1, I, J));
   d2h(c, out->r_h, t1, S * sizeof(double));
   d2h(c, out->r_u, t2, S * sizeof(double));
   d2h(c, out->lambda, c->lam.p, I * sizeof(double));
@@ -519,83 +369,113 @@ void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcsc
     if (extra->n_iters) *extra->n_iters = 0;
   }
   if (I == 0) return;
-  dispatch_m(M, [&](auto mm) {
-    constexpr int MM = decltype(mm)::value;
-    upload_model(c, in, p0, X, !accel || opt->compute_objective, accel);
-    reset_err(c);
-    if (accel) launch_slots<MM>(c, problem(c, 1, I, J, M), false, true, opt->eps_var);
-    const bool traj = extra && opt->record_trajectory && (extra->traj_r_h || extra->traj_r_u || extra->traj_lambda);
-    const size_t S = static_cast<size_t>(I * J);
-    double* trh = traj ? c->traj_rh.get<double>(S * std::max(iters, 1)) : nullptr;
-    double* tru = traj ? c->traj_ru.get<double>(S * std::max(iters, 1)) : nullptr;
-    double* trl = traj ? c->traj_lam.get<double>(I * std::max(iters, 1)) : nullptr;
-    std::vector<double> objv, secs;
-    int iters_run = 0;
-    auto launch = [&](int first, int count) {
-      if (accel) {
-        AccelArgs A = accel_args(c, I, J, M, count, *hyper, opt->eps_var, opt->gamma_fault);
-        if (traj) {
-          A.traj_r_h = trh + static_cast<size_t>(first) * S;
-          A.traj_r_u = tru + static_cast<size_t>(first) * S;
-          A.traj_lambda = trl + static_cast<size_t>(first) * I;
-        }
-        launch_accel(c, A);
-      } else {
-        NaiveArgs N = naive_args(c, I, J, count, *hyper, opt->eps_var);
-        if (traj) {
-          N.traj_r_h = trh + static_cast<size_t>(first) * S;
-          N.traj_r_u = tru + static_cast<size_t>(first) * S;
-          N.traj_lambda = trl + static_cast<size_t>(first) * I;
-        }
-        launch_naive<MM>(c, N);
+  upload_model(c, in, p0, X, !accel || opt->compute_objective, accel);
+  reset_err(c);
+  if (accel) c->launched(launch_slots(c->stream, problem(c, 1, I, J, M), false, true, opt->eps_var));
+  const bool traj = extra && opt->record_trajectory && (extra->traj_r_h || extra->traj_r_u || extra->traj_lambda);
+  const size_t S = static_cast<size_t>(I * J);
+  double* trh = traj ? c->traj_rh.get<double>(S * std::max(iters, 1)) : nullptr;
+  double* tru = traj ? c->traj_ru.get<double>(S * std::max(iters, 1)) : nullptr;
+  double* trl = traj ? c->traj_lam.get<double>(I * std::max(iters, 1)) : nullptr;
+  std::vector<double> objv, secs;
+  int iters_run = 0;
+  auto launch = [&](int first, int count) {
+    if (accel) {
+      AccelArgs A = accel_args(c, I, J, M, count, *hyper, opt->eps_var, opt->gamma_fault);
+      if (traj) {
+        A.traj_r_h = trh + static_cast<size_t>(first) * S;
+        A.traj_r_u = tru + static_cast<size_t>(first) * S;
+        A.traj_lambda = trl + static_cast<size_t>(first) * I;
       }
-    };
-    if (!opt->compute_objective) {
+      run_accel(c, A);
+    } else {
+      NaiveArgs N = naive_args(c, I, J, count, *hyper, opt->eps_var);
+      if (traj) {
+        N.traj_r_h = trh + static_cast<size_t>(first) * S;
+        N.traj_r_u = tru + static_cast<size_t>(first) * S;
+        N.traj_lambda = trl + static_cast<size_t>(first) * I;
+      }
+      c->launched(launch_naive(c->stream, M, N));
+    }
+  };
+  if (!opt->compute_objective) {
+    CK(cudaEventRecord(c->ev0, c->stream));
+    if (iters > 0) launch(0, iters);
+    CK(cudaEventRecord(c->ev1, c->stream));
+    iters_run = iters;
+    check_err(c, J);
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    // one launch runs every iteration on-chip: each gets the mean time
+    secs.assign(iters, iters ? (ms * 1e-3) / iters : 0.0);
+  } else {
+    objv.push_back(objective(c, I, J, M, *hyper));
+    for (int it = 0; it < iters; ++it) {
       CK(cudaEventRecord(c->ev0, c->stream));
-      launch(0, iters);
+      launch(it, 1);
       CK(cudaEventRecord(c->ev1, c->stream));
-      iters_run = iters;
-      check_err(c, J);
+      ++iters_run;
+      objv.push_back(objective(c, I, J, M, *hyper));  // synchronizes + checks errors
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-      secs.assign(iters, iters ? (ms * 1e-3) / iters : 0.0);
-    } else {
-      objv.push_back(objective<MM>(c, I, J, *hyper));
-      for (int it = 0; it < iters; ++it) {
-        CK(cudaEventRecord(c->ev0, c->stream));
-        launch(it, 1);
-        CK(cudaEventRecord(c->ev1, c->stream));
-        ++iters_run;
-        objv.push_back(objective<MM>(c, I, J, *hyper));  // synchronizes + checks errors
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
-        secs.push_back(ms * 1e-3);
-        const double prev = objv[objv.size() - 2], cur = objv.back();
-        if (opt->rel_obj_tol > 0.0 && std::abs(cur - prev) <= opt->rel_obj_tol * std::abs(prev)) break;
-      }
+      secs.push_back(ms * 1e-3);
+      const double prev = objv[objv.size() - 2], cur = objv.back();
+      if (opt->rel_obj_tol > 0.0 && std::abs(cur - prev) <= opt->rel_obj_tol * std::abs(prev)) break;
     }
-    download_params(c, I, J, out);
-    if (traj && iters_run > 0) {
-      double* th = c->tmp.get<double>(S * iters_run);
-      if (extra->traj_r_h) {
-        to_ij<double>(c, trh, th, iters_run, I, J);
-        d2h(c, extra->traj_r_h, th, S * iters_run * sizeof(double));
-      }
-      if (extra->traj_r_u) {
-        to_ij<double>(c, tru, th, iters_run, I, J);
-        d2h(c, extra->traj_r_u, th, S * iters_run * sizeof(double));
-      }
-      d2h(c, extra->traj_lambda, trl, static_cast<size_t>(I) * iters_run * sizeof(double));
+  }
+  download_params(c, I, J, out);
+  if (traj && iters_run > 0) {
+    double* th = c->tmp.get<double>(S * iters_run);
+    if (extra->traj_r_h) {
+      c->launched(launch_to_ij(c->stream, trh, th, iters_run, I, J));
+      d2h(c, extra->traj_r_h, th, S * iters_run * sizeof(double));
     }
-    sync(c);
-    if (extra) {
-      if (extra->objective)
-        std::memcpy(extra->objective, objv.data(), objv.size() * sizeof(double));
-      if (extra->n_objective) *extra->n_objective = static_cast<int>(objv.size());
-      if (extra->iter_seconds) std::memcpy(extra->iter_seconds, secs.data(), secs.size() * sizeof(double));
-      if (extra->n_iters) *extra->n_iters = iters_run;
+    if (extra->traj_r_u) {
+      c->launched(launch_to_ij(c->stream, tru, th, iters_run, I, J));
+      d2h(c, extra->traj_r_u, th, S * iters_run * sizeof(double));
     }
-  });
+    d2h(c, extra->traj_lambda, trl, static_cast<size_t>(I) * iters_run * sizeof(double));
+  }
+  sync(c);
+  if (extra) {
+    if (extra->objective) std::memcpy(extra->objective, objv.data(), objv.size() * sizeof(double));
+    if (extra->n_objective) *extra->n_objective = static_cast<int>(objv.size());
+    if (extra->iter_seconds) std::memcpy(extra->iter_seconds, secs.data(), secs.size() * sizeof(double));
+    if (extra->n_iters) *extra->n_iters = iters_run;
+  }
+}
+
+void extract_impl(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p, const double* X, double* image,
+                  double* dry, double* noise) {
+  if (!c || !p) fail(RCSCM_INVALID_INPUT, "extract: NULL argument");
+  validate_inputs(in, false, true);
+  const int64_t I = in->num_bins, J = in->frames;
+  const int M = in->mics;
+  if (I == 0) return;
+  upload_model(c, in, p, X, false, true);
+  const size_t S = static_cast<size_t>(I * J);
+  WienerArgs Wa{};
+  Wa.nb = I;
+  Wa.J = J;
+  Wa.X = c->X.as<double2>();
+  Wa.a = c->a.as<double2>();
+  Wa.b = c->b.as<double2>();
+  Wa.Rpp = c->Rpp.as<double2>();
+  Wa.r_h = c->rh.as<double>();
+  Wa.r_u = c->ru.as<double>();
+  Wa.lambda = c->lam.as<double>();
+  Wa.dry = dry ? c->dry.get<double2>(S) : nullptr;
+  Wa.image = image ? c->image.get<double2>(S * M) : nullptr;
+  if (noise) Wa.noise = c->noise.get<double2>(S * M);
+  c->launched(launch_wiener(c->stream, M, Wa, true, noise != nullptr));
+  if (dry) {
+    double2* t = c->tmp.get<double2>(S);
+    c->launched(launch_to_ij_c(c->stream, Wa.dry, t, 1, I, J));
+    d2h(c, dry, t, S * sizeof(double2));
+  }
+  if (image) d2h(c, image, Wa.image, S * M * sizeof(double2));
+  if (noise) d2h(c, noise, Wa.noise, S * M * sizeof(double2));
+  sync(c);
 }
 
 }  // namespace
@@ -613,8 +493,7 @@ int rcscm_gpu_create(const rcscm_gpu_config* cfg, rcscm_gpu_ctx** out) {
     *out = nullptr;
     rcscm_gpu_config d{0, RCSCM_C128, nullptr};
     if (cfg) d = *cfg;
-    if (d.precision != RCSCM_C128)
-      fail(RCSCM_UNSUPPORTED, "precision: only RCSCM_C128 is implemented in this build");
+    if (d.precision != RCSCM_C128) fail(RCSCM_UNSUPPORTED, "precision: only RCSCM_C128 is implemented in this build");
     int n = 0;
     CK(cudaGetDeviceCount(&n));
     if (d.device < 0 || d.device >= n) fail(RCSCM_INVALID_INPUT, "device ordinal out of range");
@@ -643,8 +522,8 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->X, &c->W, &c->A, &c->T, &c->V, &c->a, &c->b, &c->Rp, &c->Rpp, &c->power, &c->sab, &c->taa,
-                  &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->rh0, &c->ru0, &c->lam0, &c->tmp, &c->tmp2,
-                  &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->dry, &c->image, &c->noise,
+                  &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->rh0, &c->ru0, &c->lam0, &c->tmp,
+                  &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -666,25 +545,22 @@ int rcscm_gpu_build_noise_scm(rcscm_gpu_ctx* c, int64_t I, int64_t J, int M, con
     if (I < 0 || J < 0 || M < 1) fail(RCSCM_INVALID_INPUT, "build_noise_scm: bad shape");
     if (I == 0) return;
     if (J < 1) fail(RCSCM_INVALID_INPUT, "build_noise_scm: frames must be >= 1");
-    dispatch_m(M, [&](auto mm) {
-      constexpr int MM = decltype(mm)::value;
-      alloc_problem(c, I, J, M);
-      c->W.get<double2>(I * M * M);
-      c->A.get<double2>(I * M * M);
-      h2d(c, c->X.p, X, static_cast<size_t>(I * J * M) * sizeof(double2));
-      h2d(c, c->W.p, W, I * M * M * sizeof(double2));
-      h2d(c, c->A.p, A, I * M * M * sizeof(double2));
-      reset_err(c);
-      c->sn_h = n_h;
-      DevProblem P = problem(c, 1, I, J, M);
-      launch_setup<MM>(c, P, rank_tol, 1e-12);
-      check_err(c, J);
-      d2h(c, a, c->a.p, I * M * sizeof(double2));
-      d2h(c, b, c->b.p, I * M * sizeof(double2));
-      d2h(c, Rp, c->Rp.p, I * M * M * sizeof(double2));
-      d2h(c, Rpp, c->Rpp.p, I * M * M * sizeof(double2));
-      sync(c);
-    });
+    check_mics(M);
+    alloc_problem(c, I, J, M);
+    c->W.get<double2>(I * M * M);
+    c->A.get<double2>(I * M * M);
+    h2d(c, c->X.p, X, static_cast<size_t>(I * J * M) * sizeof(double2));
+    h2d(c, c->W.p, W, I * M * M * sizeof(double2));
+    h2d(c, c->A.p, A, I * M * M * sizeof(double2));
+    reset_err(c);
+    c->sn_h = n_h;
+    c->launched(launch_setup(c->stream, problem(c, 1, I, J, M), rank_tol, 1e-12), 2);
+    check_err(c, J);
+    d2h(c, a, c->a.p, I * M * sizeof(double2));
+    d2h(c, b, c->b.p, I * M * sizeof(double2));
+    d2h(c, Rp, c->Rp.p, I * M * M * sizeof(double2));
+    d2h(c, Rpp, c->Rpp.p, I * M * M * sizeof(double2));
+    sync(c);
   });
 }
 
@@ -699,28 +575,24 @@ int rcscm_gpu_init_params(rcscm_gpu_ctx* c, const rcscm_inputs* in, int K, const
     if (in->n_h < 0 || in->n_h >= M) fail(RCSCM_INVALID_INPUT, "init_params: target index out of range");
     if (K < 0) fail(RCSCM_INVALID_INPUT, "init_params: K must be >= 0");
     if (I == 0) return;
-    dispatch_m(M, [&](auto mm) {
-      constexpr int MM = decltype(mm)::value;
-      upload_model(c, in, nullptr, X, true, true);
-      c->W.get<double2>(I * M * M);
-      c->A.get<double2>(I * M * M);
-      c->T.get<double>(std::max<int64_t>(I * K, 1));
-      c->V.get<double>(std::max<int64_t>(K * J, 1));
-      h2d(c, c->W.p, W, I * M * M * sizeof(double2));
-      h2d(c, c->A.p, A, I * M * M * sizeof(double2));
-      h2d(c, c->T.p, T, I * K * sizeof(double));
-      h2d(c, c->V.p, V, K * J * sizeof(double));
-      reset_err(c);
-      c->sn_h = in->n_h;
-      c->sK = K;
-      DevProblem P = problem(c, 1, I, J, M);
-      launch_slots<MM>(c, P, true, false, 1e-12);
-      k_setup_bin<MM, 1><<<(I + 63) / 64, 64, 0, c->stream>>>(P, 1e-10, 1e-12);
-      c->launched();
-      check_err(c, J);
-      download_params(c, I, J, out);
-      sync(c);
-    });
+    upload_model(c, in, nullptr, X, true, true);
+    c->W.get<double2>(I * M * M);
+    c->A.get<double2>(I * M * M);
+    c->T.get<double>(std::max<int64_t>(I * K, 1));
+    c->V.get<double>(std::max<int64_t>(K * J, 1));
+    h2d(c, c->W.p, W, I * M * M * sizeof(double2));
+    h2d(c, c->A.p, A, I * M * M * sizeof(double2));
+    h2d(c, c->T.p, T, I * K * sizeof(double));
+    h2d(c, c->V.p, V, K * J * sizeof(double));
+    reset_err(c);
+    c->sn_h = in->n_h;
+    c->sK = K;
+    DevProblem P = problem(c, 1, I, J, M);
+    c->launched(launch_slots(c->stream, P, true, false, 1e-12));
+    c->launched(launch_lambda0(c->stream, P, 1e-12));
+    check_err(c, J);
+    download_params(c, I, J, out);
+    sync(c);
   });
 }
 
@@ -732,18 +604,15 @@ int rcscm_gpu_map_objective(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcsc
     const int64_t I = in->num_bins, J = in->frames;
     *out = 0.0;
     if (I == 0) return;
-    dispatch_m(in->mics, [&](auto mm) {
-      constexpr int MM = decltype(mm)::value;
-      upload_model(c, in, p, X, true, false);
-      reset_err(c);
-      *out = objective<MM>(c, I, J, *hyper);
-    });
+    upload_model(c, in, p, X, true, false);
+    reset_err(c);
+    *out = objective(c, I, J, in->mics, *hyper);
   });
 }
 
 int rcscm_gpu_run_naive(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* params0,
-                        const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt,
-                        rcscm_params* out, rcscm_result* extra) {
+                        const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt, rcscm_params* out,
+                        rcscm_result* extra) {
   return guarded([&] {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
     run_solver(c, false, in, params0, hyper, X, opt, out, extra);
@@ -756,46 +625,6 @@ int rcscm_gpu_run_algorithm2(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcs
   return guarded([&] {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
     run_solver(c, true, in, params0, hyper, X, opt, out, extra);
-  });
-}
-
-static void extract_impl(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p, const double* X,
-                         double* image, double* dry, double* noise) {
-  if (!c || !p) fail(RCSCM_INVALID_INPUT, "extract: NULL argument");
-  validate_inputs(in, false, true);
-  const int64_t I = in->num_bins, J = in->frames;
-  const int M = in->mics;
-  if (I == 0) return;
-  dispatch_m(M, [&](auto mm) {
-    constexpr int MM = decltype(mm)::value;
-    upload_model(c, in, p, X, false, true);
-    const size_t S = static_cast<size_t>(I * J);
-    WienerArgs Wa{};
-    Wa.nb = I;
-    Wa.J = J;
-    Wa.X = c->X.as<double2>();
-    Wa.a = c->a.as<double2>();
-    Wa.b = c->b.as<double2>();
-    Wa.Rpp = c->Rpp.as<double2>();
-    Wa.r_h = c->rh.as<double>();
-    Wa.r_u = c->ru.as<double>();
-    Wa.lambda = c->lam.as<double>();
-    Wa.dry = dry ? c->dry.get<double2>(S) : nullptr;
-    Wa.image = image ? c->image.get<double2>(S * M) : nullptr;
-    if (noise) {
-      Wa.noise = c->noise.get<double2>(S * M);
-      launch_wiener<MM, true, true>(c, Wa);
-    } else {
-      launch_wiener<MM, true, false>(c, Wa);
-    }
-    if (dry) {
-      double2* t = reinterpret_cast<double2*>(c->tmp.get<double2>(S));
-      to_ij<double2>(c, Wa.dry, t, 1, I, J);
-      d2h(c, dry, t, S * sizeof(double2));
-    }
-    if (image) d2h(c, image, Wa.image, S * M * sizeof(double2));
-    if (noise) d2h(c, noise, Wa.noise, S * M * sizeof(double2));
-    sync(c);
   });
 }
 
@@ -813,13 +642,13 @@ int rcscm_gpu_extract_noise(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcsc
 }
 
 // ---- session ------------------------------------------------------------------
-int rcscm_gpu_session_load(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M, int K, int n_h,
-                           const double* X, const double* W, const double* A, const double* T, const double* V) {
+int rcscm_gpu_session_load(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M, int K, int n_h, const double* X,
+                           const double* W, const double* A, const double* T, const double* V) {
   return guarded([&] {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
     if (B < 1 || I < 1 || J < 1 || M < 1 || K < 0) fail(RCSCM_INVALID_INPUT, "session_load: bad shape");
     if (n_h < 0 || n_h >= M) fail(RCSCM_INVALID_INPUT, "session_load: target index out of range");
-    dispatch_m(M, [&](auto) {});
+    check_mics(M);
     const int64_t nb = B * I;
     alloc_problem(c, nb, J, M);
     c->W.get<double2>(nb * M * M);
@@ -860,59 +689,56 @@ int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_h
     const int64_t nb = c->sB * c->sI, J = c->sJ;
     const int M = c->sM;
     const size_t S = static_cast<size_t>(nb * J);
-    dispatch_m(M, [&](auto mm) {
-      constexpr int MM = decltype(mm)::value;
-      DevProblem P = problem(c, c->sB, c->sI, J, M);
-      bool pre_done = false;
-      if (stages & RCSCM_STAGE_SETUP) {
-        launch_setup<MM>(c, P, 1e-10, eps_var);
-        const bool pre = (stages & RCSCM_STAGE_PRECOMPUTE) != 0;
-        launch_slots<MM>(c, P, true, pre, eps_var);
-        pre_done = pre;
-        CK(cudaMemcpyAsync(c->rh0.p, c->rh.p, S * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->ru0.p, c->ru.p, S * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->lam0.p, c->lam.p, nb * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-        c->s_setup = true;
-        if (pre) c->s_pre = true;
-      }
-      if (!c->s_setup) fail(RCSCM_INVALID_INPUT, "session_run: run RCSCM_STAGE_SETUP first");
-      if (stages & RCSCM_STAGE_RESET) {
-        CK(cudaMemcpyAsync(c->rh.p, c->rh0.p, S * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->ru.p, c->ru0.p, S * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->lam.p, c->lam0.p, nb * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-      }
-      if ((stages & RCSCM_STAGE_PRECOMPUTE) && !pre_done) {
-        launch_slots<MM>(c, P, false, true, eps_var);
-        c->s_pre = true;
-      }
-      if (stages & RCSCM_STAGE_ACCEL) {
-        if (!c->s_pre) fail(RCSCM_INVALID_INPUT, "session_run: ACCEL needs PRECOMPUTE");
-        launch_accel(c, accel_args(c, nb, J, M, iters, h, eps_var, 0.0));
-      }
-      if (stages & RCSCM_STAGE_NAIVE) launch_naive<MM>(c, naive_args(c, nb, J, iters, h, eps_var));
-      if (stages & RCSCM_STAGE_WIENER) {
-        if (!c->s_pre) fail(RCSCM_INVALID_INPUT, "session_run: WIENER needs PRECOMPUTE");
-        WienerArgs Wa{};
-        Wa.nb = nb;
-        Wa.J = J;
-        Wa.a = c->a.as<double2>();
-        Wa.sigma_ab = c->sab.as<double2>();
-        Wa.tau_aa = c->taa.as<double>();
-        Wa.sigma_bx = c->sbx.as<double2>();
-        Wa.tau_ax = c->tax.as<double2>();
-        Wa.r_h = c->rh.as<double>();
-        Wa.r_u = c->ru.as<double>();
-        Wa.lambda = c->lam.as<double>();
-        Wa.dry = c->dry.as<double2>();
-        Wa.image = c->image.as<double2>();
-        launch_wiener<MM, false, false>(c, Wa);
-      }
-    });
+    DevProblem P = problem(c, c->sB, c->sI, J, M);
+    bool pre_done = false;
+    if (stages & RCSCM_STAGE_SETUP) {
+      c->launched(launch_setup(c->stream, P, 1e-10, eps_var), 2);
+      const bool pre = (stages & RCSCM_STAGE_PRECOMPUTE) != 0;
+      c->launched(launch_slots(c->stream, P, true, pre, eps_var));
+      pre_done = pre;
+      d2d(c, c->rh0.p, c->rh.p, S * sizeof(double));
+      d2d(c, c->ru0.p, c->ru.p, S * sizeof(double));
+      d2d(c, c->lam0.p, c->lam.p, nb * sizeof(double));
+      c->s_setup = true;
+      if (pre) c->s_pre = true;
+    }
+    if (!c->s_setup) fail(RCSCM_INVALID_INPUT, "session_run: run RCSCM_STAGE_SETUP first");
+    if (stages & RCSCM_STAGE_RESET) {
+      d2d(c, c->rh.p, c->rh0.p, S * sizeof(double));
+      d2d(c, c->ru.p, c->ru0.p, S * sizeof(double));
+      d2d(c, c->lam.p, c->lam0.p, nb * sizeof(double));
+    }
+    if ((stages & RCSCM_STAGE_PRECOMPUTE) && !pre_done) {
+      c->launched(launch_slots(c->stream, P, false, true, eps_var));
+      c->s_pre = true;
+    }
+    if (stages & RCSCM_STAGE_ACCEL) {
+      if (!c->s_pre) fail(RCSCM_INVALID_INPUT, "session_run: ACCEL needs PRECOMPUTE");
+      run_accel(c, accel_args(c, nb, J, M, iters, h, eps_var, 0.0));
+    }
+    if (stages & RCSCM_STAGE_NAIVE) c->launched(launch_naive(c->stream, M, naive_args(c, nb, J, iters, h, eps_var)));
+    if (stages & RCSCM_STAGE_WIENER) {
+      if (!c->s_pre) fail(RCSCM_INVALID_INPUT, "session_run: WIENER needs PRECOMPUTE");
+      WienerArgs Wa{};
+      Wa.nb = nb;
+      Wa.J = J;
+      Wa.a = c->a.as<double2>();
+      Wa.sigma_ab = c->sab.as<double2>();
+      Wa.tau_aa = c->taa.as<double>();
+      Wa.sigma_bx = c->sbx.as<double2>();
+      Wa.tau_ax = c->tax.as<double2>();
+      Wa.r_h = c->rh.as<double>();
+      Wa.r_u = c->ru.as<double>();
+      Wa.lambda = c->lam.as<double>();
+      Wa.dry = c->dry.as<double2>();
+      Wa.image = c->image.as<double2>();
+      c->launched(launch_wiener(c->stream, M, Wa, false, false));
+    }
   });
 }
 
-int rcscm_gpu_session_fetch(rcscm_gpu_ctx* c, double* r_h, double* r_u, double* lambda, double* dry,
-                            double* image, int do_sync) {
+int rcscm_gpu_session_fetch(rcscm_gpu_ctx* c, double* r_h, double* r_u, double* lambda, double* dry, double* image,
+                            int do_sync) {
   return guarded([&] {
     if (!c || !c->s_loaded) fail(RCSCM_INVALID_INPUT, "session_fetch: no session loaded");
     const int64_t nb = c->sB * c->sI, J = c->sJ;
@@ -938,19 +764,17 @@ int rcscm_gpu_probe_fp64(rcscm_gpu_ctx* c, double* tflops, double* ms) {
     if (!c || !tflops) fail(RCSCM_INVALID_INPUT, "probe_fp64: NULL argument");
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-    constexpr int NACC = 8, NT = 256;
+    constexpr int kNacc = 8, kNt = 256;
     const int blocks = sms * 8, iters = 20000;
     double* out = c->obj.get<double>(1);
-    k_fp64_probe<NACC><<<blocks, NT, 0, c->stream>>>(1.0, iters / 10, out);  // warm-up
-    c->launched();
+    c->launched(launch_fp64_probe(c->stream, blocks, iters / 10, out));  // warm-up
     CK(cudaEventRecord(c->ev0, c->stream));
-    k_fp64_probe<NACC><<<blocks, NT, 0, c->stream>>>(1.0, iters, out);
-    c->launched();
+    c->launched(launch_fp64_probe(c->stream, blocks, iters, out));
     CK(cudaEventRecord(c->ev1, c->stream));
     CK(cudaEventSynchronize(c->ev1));
     float t = 0.f;
     CK(cudaEventElapsedTime(&t, c->ev0, c->ev1));
-    const double flops = 2.0 * NACC * static_cast<double>(iters) * blocks * NT;
+    const double flops = 2.0 * kNacc * static_cast<double>(iters) * blocks * kNt;
     *tflops = flops / (t * 1e-3) / 1e12;
     if (ms) *ms = t;
   });

@@ -1,0 +1,24 @@
+// dispatch.cuh -- run-time channel-count dispatch to M-templated kernels.
+#pragma once
+
+#include <type_traits>
+
+namespace rcscm {
+
+template <class F>
+cudaError_t dispatch_mics(int M, F&& f) {
+  switch (M) {
+    case 1: return f(std::integral_constant<int, 1>{});
+    case 2: return f(std::integral_constant<int, 2>{});
+    case 3: return f(std::integral_constant<int, 3>{});
+    case 4: return f(std::integral_constant<int, 4>{});
+    case 5: return f(std::integral_constant<int, 5>{});
+    case 6: return f(std::integral_constant<int, 6>{});
+    case 7: return f(std::integral_constant<int, 7>{});
+    case 8: return f(std::integral_constant<int, 8>{});
+    case 16: return f(std::integral_constant<int, 16>{});
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace rcscm

@@ -1,0 +1,49 @@
+// launch.h -- host-side launchers of the rcscm kernels, one translation unit
+// per kernel family (setup_launch.cu, accel_launch.cu, naive_launch.cu,
+// stream_launch.cu). Each returns cudaSuccess or the launch error; M-templated
+// kernels are dispatched at run time over the supported channel counts.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "accel.cuh"
+#include "naive.cuh"
+#include "setup.cuh"
+#include "stream.cuh"
+
+namespace rcscm {
+
+// true if this build has kernels for M channels (1..8 and 16)
+bool mics_supported(int M);
+
+// K1a + K1b (build_noise_scm): mean powers, then per-bin R', b, R'^+, a, lambda0.
+cudaError_t launch_setup(cudaStream_t s, const DevProblem& P, double rank_tol, double eps);
+// K1b in MODE 1: lambda0 only from a given R' (init_params).
+cudaError_t launch_lambda0(cudaStream_t s, const DevProblem& P, double eps);
+// K1: slot stream kernel (INIT: r_h0 / r_u0, PRE: sigma / tau).
+cudaError_t launch_slots(cudaStream_t s, const DevProblem& P, bool init, bool pre, double eps);
+
+// K2 launch configuration (cluster size, threads, slots per thread).
+struct AccelCfg {
+  int cl, nt, spt;
+  bool full;  // nt * spt == chunk: no per-slot masks
+};
+// Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL
+// force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
+AccelCfg choose_accel_cfg(int64_t J);
+cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg);
+
+cudaError_t launch_naive(cudaStream_t s, int M, const NaiveArgs& N);
+
+cudaError_t launch_wiener(cudaStream_t s, int M, const WienerArgs& W, bool from_x, bool noise);
+// objective partial sums (np = grid size written to *np) and the final sum
+cudaError_t launch_objective(cudaStream_t s, int M, ObjArgs O, int64_t* np);
+cudaError_t launch_sum_partials(cudaStream_t s, const double* partial, int64_t n, double* out);
+// reference I x J column-major <-> device [bin][t] (B blocks of I bins)
+cudaError_t launch_to_bt(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J);
+cudaError_t launch_to_ij(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J);
+cudaError_t launch_to_ij_c(cudaStream_t s, const double2* src, double2* dst, int64_t B, int64_t I, int64_t J);
+cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out);
+
+}  // namespace rcscm

@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(NT) k_objective(ObjArgs P) {
 }
 
 // Deterministic single-CTA sum of n partials (fixed strided order + tree).
-__global__ void k_sum_partials(const double* partial, int64_t n, double* out) {
+static __global__ void k_sum_partials(const double* partial, int64_t n, double* out) {
   __shared__ double red[32];
   double s = 0.0;
   for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s += partial[k];

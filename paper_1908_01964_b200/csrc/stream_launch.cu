@@ -1,0 +1,68 @@
+// stream_launch.cu -- launchers of K4 (Wiener), the objective, the layout
+// transposes and the FP64 probe (stream.cuh).
+#include "dispatch.cuh"
+#include "launch.h"
+
+namespace rcscm {
+
+constexpr int kWienerNT = 128;
+constexpr int kObjNT = 128;
+
+cudaError_t launch_wiener(cudaStream_t s, int M, const WienerArgs& W, bool from_x, bool noise) {
+  if (W.nb * W.J == 0) return cudaSuccess;
+  return dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    dim3 grid(W.nb, (W.J + kWienerNT - 1) / kWienerNT);
+    if (from_x && noise)
+      k_wiener<MM, kWienerNT, true, true><<<grid, kWienerNT, 0, s>>>(W);
+    else if (from_x)
+      k_wiener<MM, kWienerNT, true, false><<<grid, kWienerNT, 0, s>>>(W);
+    else
+      k_wiener<MM, kWienerNT, false, false><<<grid, kWienerNT, 0, s>>>(W);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_objective(cudaStream_t s, int M, ObjArgs O, int64_t* np) {
+  dim3 grid(O.nb, (O.J + kObjNT - 1) / kObjNT);
+  *np = static_cast<int64_t>(grid.x) * grid.y;
+  if (O.nb * O.J == 0) return cudaSuccess;
+  return dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    k_objective<MM, kObjNT><<<grid, kObjNT, 0, s>>>(O);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_sum_partials(cudaStream_t s, const double* partial, int64_t n, double* out) {
+  k_sum_partials<<<1, 1024, 0, s>>>(partial, n, out);
+  return cudaGetLastError();
+}
+
+template <class T, bool TO_BT>
+static cudaError_t transpose(cudaStream_t s, const T* src, T* dst, int64_t B, int64_t I, int64_t J) {
+  if (B * I * J == 0) return cudaSuccess;
+  dim3 grid((I + 31) / 32, (J + 31) / 32, B), block(32, 8);
+  if (TO_BT)
+    k_ij_to_bt<T><<<grid, block, 0, s>>>(src, dst, I, J);
+  else
+    k_bt_to_ij<T><<<grid, block, 0, s>>>(src, dst, I, J);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_to_bt(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J) {
+  return transpose<double, true>(s, src, dst, B, I, J);
+}
+cudaError_t launch_to_ij(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J) {
+  return transpose<double, false>(s, src, dst, B, I, J);
+}
+cudaError_t launch_to_ij_c(cudaStream_t s, const double2* src, double2* dst, int64_t B, int64_t I, int64_t J) {
+  return transpose<double2, false>(s, src, dst, B, I, J);
+}
+
+cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out) {
+  k_fp64_probe<8><<<blocks, 256, 0, s>>>(1.0, iters, out);
+  return cudaGetLastError();
+}
+
+}  // namespace rcscm

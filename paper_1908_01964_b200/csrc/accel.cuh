@@ -58,12 +58,18 @@ __device__ __forceinline__ double floor_eps(double v, double eps) { return v < e
 
 // FULL: every thread's SPT slots are inside the bin chunk (NT * SPT == chunk),
 // so no per-slot masks. TRAJ: record r_h / r_u / lambda after every iteration.
-template <int SPT, int CL, bool FULL, bool TRAJ>
-__global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
+// SMEMC: the four per-slot constants used only after the lambda reduction
+// (tau_ax, s_ab*s_bx, tau_xx/M, |s_bx|^2/M: 48 B/slot) live in dynamic shared
+// memory ([k][tid] planes, conflict-free) instead of registers, which roughly
+// halves the register footprint and doubles the resident warps per SM.
+template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC>
+__global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
   constexpr int kMaxWarps = 256 / 32;
   __shared__ double red[2][kMaxWarps];
   __shared__ double cl_part[2];
+  __shared__ double cl_total[2];
+  extern __shared__ double2 dyn[];
   const int NT = blockDim.x;
   const int nwarps = NT >> 5;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -75,6 +81,11 @@ __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
   const int64_t t_end = min(J, t0 + Jc);
   const int64_t base = bin * J;
   const double inv_M = P.inv_M;
+  // shared planes (SMEMC): tax[k][tid], cc[k][tid] (double2), txx[k][tid], dd[k][tid] (double)
+  double2* s_tax = dyn;
+  double2* s_cc = dyn + SPT * NT;
+  double* s_txx = reinterpret_cast<double*>(dyn + 2 * SPT * NT);
+  double* s_dd = s_txx + SPT * NT;
 
   const double2 sab = P.sigma_ab[bin];
   const double s2 = cnorm(sab);  // |sigma_ab|^2
@@ -85,8 +96,9 @@ __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
 
   // per-slot state: rh, ru evolve; rax = rho~_ax carried; the rest is constant.
   // txx and dd are pre-scaled by 1/M (exact for M = 2, 4, 8, 16).
-  double rh[SPT], ru[SPT], txx[SPT], dd[SPT];
-  double2 rax[SPT], tax[SPT], cc[SPT], sbx[SPT];
+  constexpr int SR = SMEMC ? 1 : SPT;  // register copies of the constants
+  double rh[SPT], ru[SPT], txx[SR], dd[SR];
+  double2 rax[SPT], tax[SR], cc[SR], sbx[SPT];
   bool valid[SPT];
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
@@ -96,11 +108,22 @@ __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
     rh[k] = P.r_h[s];
     ru[k] = P.r_u[s];
     sbx[k] = P.sigma_bx[s];
-    tax[k] = P.tau_ax[s];
-    txx[k] = P.tau_xx[s] * inv_M;
-    cc[k] = cmul(sab, sbx[k]);     // sigma_ab * sigma_bx
-    dd[k] = cnorm(sbx[k]) * inv_M;  // |sigma_bx|^2 / M
-    rax[k] = make_double2(fma(cc[k].x, il, tax[k].x), fma(cc[k].y, il, tax[k].y));
+    const double2 tk = P.tau_ax[s];
+    const double xk = P.tau_xx[s] * inv_M;
+    const double2 ck = cmul(sab, sbx[k]);   // sigma_ab * sigma_bx
+    const double dk = cnorm(sbx[k]) * inv_M;  // |sigma_bx|^2 / M
+    rax[k] = make_double2(fma(ck.x, il, tk.x), fma(ck.y, il, tk.y));
+    if constexpr (SMEMC) {
+      s_tax[k * NT + tid] = tk;
+      s_cc[k * NT + tid] = ck;
+      s_txx[k * NT + tid] = xk;
+      s_dd[k * NT + tid] = dk;
+    } else {
+      tax[k] = tk;
+      cc[k] = ck;
+      txx[k] = xk;
+      dd[k] = dk;
+    }
   }
 
   const double invJ = 1.0 / static_cast<double>(J);
@@ -137,14 +160,30 @@ __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
     if (lane == 0) red[buf][warp] = part;
     __syncthreads();
     double total = 0.0;
-    for (int w = 0; w < nwarps; ++w) total += red[buf][w];
-    if constexpr (CL > 1) {
+    if constexpr (CL == 1) {
+      for (int w = 0; w < nwarps; ++w) total += red[buf][w];
+    } else {
+      // CTA partial -> cluster: warp 0 gathers the CL partials over DSMEM in
+      // rank order and every CTA forms the same total.
       cg::cluster_group cluster = cg::this_cluster();
-      if (tid == 0) cl_part[buf] = total;
+      if (tid == 0) {
+        double c = 0.0;
+        for (int w = 0; w < nwarps; ++w) c += red[buf][w];
+        cl_part[buf] = c;
+      }
       cluster.sync();
-      total = 0.0;
+      if (warp == 0) {
+        double v = lane < CL ? *cluster.map_shared_rank(&cl_part[buf], lane) : 0.0;
+        // fixed-order pairwise tree over ranks 0..CL-1 (same on every CTA)
 #pragma unroll
-      for (int r = 0; r < CL; ++r) total += *cluster.map_shared_rank(&cl_part[buf], r);
+        for (int off = 1; off < CL; off <<= 1) {
+          const double o = __shfl_down_sync(0xffffffffu, v, off);
+          if ((lane & (2 * off - 1)) == 0) v += o;
+        }
+        if (lane == 0) cl_total[buf] = v;
+      }
+      __syncthreads();
+      total = cl_total[buf];
     }
     lam = floor_eps(total * invJ, P.eps);
     il = 1.0 / lam;
@@ -152,8 +191,21 @@ __global__ void __launch_bounds__(256, 1) k_accel(AccelArgs P) {
     const double raaM = raa * inv_M;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      const double2 nax = make_double2(fma(cc[k].x, il, tax[k].x), fma(cc[k].y, il, tax[k].y));
-      const double rxx = fma(dd[k], il, txx[k]);                 // rho_xx / M
+      double2 tk, ck;
+      double xk, dk;
+      if constexpr (SMEMC) {
+        tk = s_tax[k * NT + tid];
+        ck = s_cc[k * NT + tid];
+        xk = s_txx[k * NT + tid];
+        dk = s_dd[k * NT + tid];
+      } else {
+        tk = tax[k];
+        ck = cc[k];
+        xk = txx[k];
+        dk = dd[k];
+      }
+      const double2 nax = make_double2(fma(ck.x, il, tk.x), fma(ck.y, il, tk.y));
+      const double rxx = fma(dk, il, xk);                        // rho_xx / M
       const double re = fma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
       double val = fma(gq[k], raaM, rxx);
       val = fma(g[k], re, val);

@@ -6,9 +6,11 @@
 namespace rcscm {
 
 AccelCfg choose_accel_cfg(int64_t J) {
-  AccelCfg best{0, 0, 0, false};
+  AccelCfg best{0, 0, 0, false, false};
   const char* e_spt = std::getenv("RCSCM_ACCEL_SPT");
   const char* e_cl = std::getenv("RCSCM_ACCEL_CL");
+  const char* e_sm = std::getenv("RCSCM_ACCEL_SMEM");
+  const bool smem = e_sm ? std::atoi(e_sm) != 0 : false;
   const int force_spt = e_spt ? std::atoi(e_spt) : 0;
   const int force_cl = e_cl ? std::atoi(e_cl) : 0;
   for (int cl : {1, 2, 4, 8, 16}) {
@@ -18,6 +20,7 @@ AccelCfg choose_accel_cfg(int64_t J) {
     if (jc > 256LL * (force_spt ? force_spt : max_spt)) continue;
     int64_t best_waste = -1;
     for (int spt = 1; spt <= 8; ++spt) {
+      if (spt == 7) continue;  // not instantiated
       if (force_spt ? spt != force_spt : spt > max_spt) continue;
       int64_t nt = (jc + spt - 1) / spt;
       nt = (nt + 31) / 32 * 32;
@@ -28,7 +31,7 @@ AccelCfg choose_accel_cfg(int64_t J) {
         best_waste = waste;
         // FULL needs every CTA of the cluster to own exactly nt * spt frames
         const bool full = (waste == 0) && (jc * cl == J);
-        best = AccelCfg{cl, static_cast<int>(nt), spt, full};
+        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem};
       }
     }
     if (best.cl) return best;

@@ -6,13 +6,18 @@
 
 namespace rcscm {
 
-template <int SPT, int CL, bool FULL, bool TRAJ>
+template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC>
 cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
-  auto kern = k_accel<SPT, CL, FULL, TRAJ>;
+  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);
-  cfg.dynamicSmemBytes = 0;
+  cfg.dynamicSmemBytes = SMEMC ? static_cast<size_t>(SPT) * nt * 48 : 0;
+  if (cfg.dynamicSmemBytes > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(cfg.dynamicSmemBytes));
+    if (e != cudaSuccess) return e;
+  }
   cfg.stream = s;
   cudaLaunchAttribute attr[1];
   cfg.numAttrs = 0;
@@ -31,17 +36,16 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
   return cudaLaunchKernelEx(&cfg, kern, A);
 }
 
-template <int CL, bool FULL, bool TRAJ>
+template <int CL, bool FULL, bool TRAJ, bool SMEMC>
 cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt) {
   switch (spt) {
-    case 1: return launch_accel_t<1, CL, FULL, TRAJ>(s, A, nt);
-    case 2: return launch_accel_t<2, CL, FULL, TRAJ>(s, A, nt);
-    case 3: return launch_accel_t<3, CL, FULL, TRAJ>(s, A, nt);
-    case 4: return launch_accel_t<4, CL, FULL, TRAJ>(s, A, nt);
-    case 5: return launch_accel_t<5, CL, FULL, TRAJ>(s, A, nt);
-    case 6: return launch_accel_t<6, CL, FULL, TRAJ>(s, A, nt);
-    case 7: return launch_accel_t<7, CL, FULL, TRAJ>(s, A, nt);
-    case 8: return launch_accel_t<8, CL, FULL, TRAJ>(s, A, nt);
+    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC>(s, A, nt);
+    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC>(s, A, nt);
+    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC>(s, A, nt);
+    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC>(s, A, nt);
+    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC>(s, A, nt);
+    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC>(s, A, nt);
+    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC>(s, A, nt);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -49,9 +53,13 @@ cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt
 template <int CL>
 cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
   const bool traj = A.traj_r_h != nullptr;
-  if (traj) return launch_accel_spt<CL, false, true>(s, A, g.nt, g.spt);
-  if (g.full) return launch_accel_spt<CL, true, false>(s, A, g.nt, g.spt);
-  return launch_accel_spt<CL, false, false>(s, A, g.nt, g.spt);
+  if (traj) return launch_accel_spt<CL, false, true, false>(s, A, g.nt, g.spt);
+  if (g.smem) {
+    if (g.full) return launch_accel_spt<CL, true, false, true>(s, A, g.nt, g.spt);
+    return launch_accel_spt<CL, false, false, true>(s, A, g.nt, g.spt);
+  }
+  if (g.full) return launch_accel_spt<CL, true, false, false>(s, A, g.nt, g.spt);
+  return launch_accel_spt<CL, false, false, false>(s, A, g.nt, g.spt);
 }
 
 #define RCSCM_DECLARE_ACCEL_CL(CL) \

@@ -28,9 +28,10 @@ cudaError_t launch_slots(cudaStream_t s, const DevProblem& P, bool init, bool pr
 struct AccelCfg {
   int cl, nt, spt;
   bool full;  // nt * spt == chunk: no per-slot masks
+  bool smem;  // phase-B constants in shared memory (k_accel SMEMC)
 };
-// Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL
-// force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
+// Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL /
+// RCSCM_ACCEL_SMEM force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
 AccelCfg choose_accel_cfg(int64_t J);
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg);
 

@@ -53,8 +53,24 @@ struct AccelArgs {
   double* traj_lambda;      // optional [it][bin]
 };
 
-// std::max(v, eps) of the reference (returns v unless v < eps).
-__device__ __forceinline__ double floor_eps(double v, double eps) { return v < eps ? eps : v; }
+// std::max(v, eps) of the reference (returns v unless v < eps) for eps > 0,
+// evaluated as a signed 64-bit compare of the bit patterns: IEEE doubles of
+// either sign order like their two's-complement images against a positive eps
+// (negative v and -0.0 map below eps, +NaN stays NaN as in std::max). Keeps the
+// floor on the integer ALUs instead of the FP64 pipe.
+__device__ __forceinline__ double floor_eps(double v, double eps) {
+  const long long iv = __double_as_longlong(v), ie = __double_as_longlong(eps);
+  return __longlong_as_double(iv < ie ? ie : iv);
+}
+
+// Sum of the nw (<= 32) per-warp partials red[0..nw-1], formed identically by
+// every thread: lanes < nw load one partial each (zero-padded to the next power
+// of two), a xor butterfly adds them and lane 0's sum is broadcast.
+__device__ __forceinline__ double block_total(const double* red, int nw, int lane) {
+  double v = lane < nw ? red[lane] : 0.0;
+  for (int off = 1; off < nw; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return __shfl_sync(0xffffffffu, v, 0);
+}
 
 // FULL: every thread's SPT slots are inside the bin chunk (NT * SPT == chunk),
 // so no per-slot masks. TRAJ: record r_h / r_u / lambda after every iteration.
@@ -161,15 +177,14 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
     __syncthreads();
     double total = 0.0;
     if constexpr (CL == 1) {
-      for (int w = 0; w < nwarps; ++w) total += red[buf][w];
+      total = block_total(red[buf], nwarps, lane);
     } else {
       // CTA partial -> cluster: warp 0 gathers the CL partials over DSMEM in
       // rank order and every CTA forms the same total.
       cg::cluster_group cluster = cg::this_cluster();
-      if (tid == 0) {
-        double c = 0.0;
-        for (int w = 0; w < nwarps; ++w) c += red[buf][w];
-        cl_part[buf] = c;
+      if (warp == 0) {
+        const double c = block_total(red[buf], nwarps, lane);
+        if (lane == 0) cl_part[buf] = c;
       }
       cluster.sync();
       if (warp == 0) {
@@ -186,7 +201,7 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
       total = cl_total[buf];
     }
     lam = floor_eps(total * invJ, P.eps);
-    il = 1.0 / lam;
+    il = rcp_pos(lam);
     raa = fma(s2, il, taa);
     const double raaM = raa * inv_M;
 #pragma unroll

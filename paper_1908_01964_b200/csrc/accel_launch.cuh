@@ -13,7 +13,7 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);
   cfg.dynamicSmemBytes = SMEMC ? static_cast<size_t>(SPT) * nt * 48 : 0;
-  if (cfg.dynamicSmemBytes > 48 * 1024) {
+  if (SMEMC) {  // opt in to the full dynamic allowance (static + dynamic may pass 48 KB)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(cfg.dynamicSmemBytes));
     if (e != cudaSuccess) return e;

@@ -17,12 +17,19 @@
 // across the cluster), so results are deterministic and independent of how
 // many GPUs the bins are sharded over.
 //
-// Instruction budget per slot-iteration (47 canonical flops): 32 FP64 ops
-// (DFMA/DMUL/DADD) + 2 floor compares + 1 MUFU.RCP64H. The reference's two
-// divisions share one reciprocal (inv = 1/(D r~_u) gives gamma = r~_h r~_u inv
+// Latency structure: the lambda reduction is the only serial step of an
+// iteration, so each iteration computes the lambda-critical values first,
+// starts the warp reduction, and overlaps it with everything that does not
+// depend on the new lambda -- r_h and the two coefficients of r_u, which is
+// affine in 1/lambda_new (M r_u = P0 + P1/lambda_new). After the block total only
+// three FMAs per slot remain (r_u, and rho_ax for the next iteration).
+//
+// Instruction budget per slot-iteration (47 canonical flops): 35 FP64 ops
+// (DFMA/DMUL) + 1 MUFU.RCP64H; floors run on the integer ALUs. The reference's
+// two divisions share one reciprocal (inv = 1/(D r~_u) gives gamma = r~_h r~_u inv
 // and 1/r~_u = D inv); gamma_fault rides in an FMA; 1/M is folded into the
 // per-slot constants (exact for power-of-two M); `max(v, eps)` keeps the
-// reference's std::max semantics (v < eps ? eps : v) without fmax's NaN fix-up.
+// reference's std::max semantics.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -144,21 +151,19 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
 
   const double invJ = 1.0 / static_cast<double>(J);
   const double m2M = -2.0 * inv_M;
+  const double taaM = taa * inv_M, s2M = s2 * inv_M;
   const double fault = P.gamma_fault;
   for (int it = 0; it < P.iters; ++it) {
     const int buf = it & 1;
-    double g[SPT], gq[SPT];
-    double acc = 0.0;
+    // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
+    //     (solver_accel.hpp:67-76, :143-158).
+    double g[SPT], acc = 0.0;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       const double D = fma(rh[k], raa, ru[k]);  // r~_u + r~_h rho~_aa
       const double inv = rcp_pos(D * ru[k]);
       const double gk = fma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
       const double iru = D * inv;                         // 1 / r~_u
-      const double n2 = cnorm(rax[k]);
-      const double q = fma(gk, n2, ru[k]);
-      const double gqk = gk * q;
-      rh[k] = floor_eps(fma(gqk, P.k1, P.k2), P.eps);
       // resid = s_bx - gamma conj(s_ab) rho~_ax
       const double2 e = cmulc(sab, rax[k]);
       const double rx = fma(-gk, e.x, sbx[k].x);
@@ -168,12 +173,42 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
         acc = fma(gk, s2, acc);
         acc = fma(rr, iru, acc);
       }
-      g[k] = gk * m2M;  // -2 gamma / M
-      gq[k] = gqk;
+      g[k] = gk;
     }
-    // lambda: deterministic fixed-order reduction over the bin's frames.
     double part = warp_sum(acc);
     if (lane == 0) red[buf][warp] = part;
+    // (2) everything that does not need the new lambda, overlapping the
+    //     reduction: r_h (solver_accel.hpp:134-141) and the two halves of the
+    //     r_u update, which is affine in 1/lambda_new (:160-176 with :121-127):
+    //       M r_u = P0 + P1 / lambda_new,
+    //       P0 = g q tau_aa + tau_xx - 2 g Re(rho~_ax conj tau_ax)
+    //       P1 = g q |s_ab|^2 + |s_bx|^2 - 2 g Re(rho~_ax conj(s_ab s_bx))
+    //     (stored pre-scaled by 1/M; q = r~_u + g |rho~_ax|^2).
+    double p0[SPT], p1[SPT];
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      double2 tk, ck;
+      double xk, dk;
+      if constexpr (SMEMC) {
+        tk = s_tax[k * NT + tid];
+        ck = s_cc[k * NT + tid];
+        xk = s_txx[k * NT + tid];
+        dk = s_dd[k * NT + tid];
+      } else {
+        tk = tax[k];
+        ck = cc[k];
+        xk = txx[k];
+        dk = dd[k];
+      }
+      const double q = fma(g[k], cnorm(rax[k]), ru[k]);
+      const double gq = g[k] * q;
+      rh[k] = floor_eps(fma(gq, P.k1, P.k2), P.eps);
+      const double m2g = g[k] * m2M;                              // -2 gamma / M
+      const double re0 = fma(rax[k].x, tk.x, rax[k].y * tk.y);    // Re(rho~_ax conj tau_ax)
+      const double re1 = fma(rax[k].x, ck.x, rax[k].y * ck.y);    // Re(rho~_ax conj(s_ab s_bx))
+      p0[k] = fma(m2g, re0, fma(gq, taaM, xk));
+      p1[k] = fma(m2g, re1, fma(gq, s2M, dk));
+    }
     __syncthreads();
     double total = 0.0;
     if constexpr (CL == 1) {
@@ -200,32 +235,22 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
       __syncthreads();
       total = cl_total[buf];
     }
+    // (3) the short tail that needs lambda_new
     lam = floor_eps(total * invJ, P.eps);
     il = rcp_pos(lam);
     raa = fma(s2, il, taa);
-    const double raaM = raa * inv_M;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       double2 tk, ck;
-      double xk, dk;
       if constexpr (SMEMC) {
         tk = s_tax[k * NT + tid];
         ck = s_cc[k * NT + tid];
-        xk = s_txx[k * NT + tid];
-        dk = s_dd[k * NT + tid];
       } else {
         tk = tax[k];
         ck = cc[k];
-        xk = txx[k];
-        dk = dd[k];
       }
-      const double2 nax = make_double2(fma(ck.x, il, tk.x), fma(ck.y, il, tk.y));
-      const double rxx = fma(dk, il, xk);                        // rho_xx / M
-      const double re = fma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
-      double val = fma(gq[k], raaM, rxx);
-      val = fma(g[k], re, val);
-      ru[k] = floor_eps(val, P.eps);
-      rax[k] = nax;
+      ru[k] = floor_eps(fma(p1[k], il, p0[k]), P.eps);
+      rax[k] = make_double2(fma(ck.x, il, tk.x), fma(ck.y, il, tk.y));  // rho_ax with lambda_new
     }
     if constexpr (TRAJ) {
 #pragma unroll

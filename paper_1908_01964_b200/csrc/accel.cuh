@@ -58,6 +58,8 @@ struct AccelArgs {
   double* traj_r_h;         // optional [it][bin][t]
   double* traj_r_u;
   double* traj_lambda;      // optional [it][bin]
+  long long stagger;        // experiment: cycles of start delay for alternate CTA groups
+  int stagger_mod;
 };
 
 // std::max(v, eps) of the reference (returns v unless v < eps) for eps > 0,
@@ -149,6 +151,11 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
     }
   }
 
+  if (P.stagger > 0 && ((blockIdx.x / P.stagger_mod) & 1)) {
+    const long long c0 = clock64();
+    while (clock64() - c0 < P.stagger) {
+    }
+  }
   const double invJ = 1.0 / static_cast<double>(J);
   const double m2M = -2.0 * inv_M;
   const double taaM = taa * inv_M, s2M = s2 * inv_M;

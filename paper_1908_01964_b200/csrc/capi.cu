@@ -78,7 +78,7 @@ struct rcscm_gpu_ctx {
   int64_t launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // device buffers
-  DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam;
+  DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
   // session geometry
   bool s_loaded = false, s_setup = false, s_pre = false;
@@ -197,6 +197,7 @@ DevProblem problem(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M) {
   P.r_h = c->rh.as<double>();
   P.r_u = c->ru.as<double>();
   P.lambda = c->lam.as<double>();
+  P.logpdet = c->lpd.as<double>();
   P.err = c->err.as<unsigned long long>();
   return P;
 }
@@ -218,6 +219,7 @@ void alloc_problem(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M) {
   c->rh.get<double>(S);
   c->ru.get<double>(S);
   c->lam.get<double>(nb);
+  c->lpd.get<double>(nb);
   c->err.get<unsigned long long>(1);
 }
 
@@ -240,6 +242,10 @@ AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, 
   A.r_h = c->rh.as<double>();
   A.r_u = c->ru.as<double>();
   A.lambda = c->lam.as<double>();
+  const char* st = std::getenv("RCSCM_ACCEL_STAGGER");
+  A.stagger = st ? std::atoll(st) : 0;
+  const char* sm = std::getenv("RCSCM_ACCEL_STAGGER_MOD");
+  A.stagger_mod = sm ? std::max(1, std::atoi(sm)) : 148;
   return A;
 }
 
@@ -291,6 +297,37 @@ double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyp
   O.err = c->err.as<unsigned long long>();
   int64_t np = 0;
   c->launched(launch_objective(c->stream, M, O, &np));
+  double* out = c->obj.get<double>(1);
+  c->launched(launch_sum_partials(c->stream, O.partial, np, out));
+  double v = 0.0;
+  d2h(c, &v, out, sizeof(double));
+  check_err(c, J);
+  return v;
+}
+
+// O(1)-per-slot objective from the resident sigma/tau precompute (needs
+// logpdet, see launch_logpdet); synchronizes.
+double objective_fast(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h) {
+  if (nb * J == 0) return 0.0;
+  ObjFastArgs O{};
+  O.nb = nb;
+  O.J = J;
+  O.M = M;
+  O.alpha = h.alpha;
+  O.beta = h.beta;
+  O.sigma_ab = c->sab.as<double2>();
+  O.tau_aa = c->taa.as<double>();
+  O.sigma_bx = c->sbx.as<double2>();
+  O.tau_ax = c->tax.as<double2>();
+  O.tau_xx = c->txx.as<double>();
+  O.logpdet = c->lpd.as<double>();
+  O.r_h = c->rh.as<double>();
+  O.r_u = c->ru.as<double>();
+  O.lambda = c->lam.as<double>();
+  O.partial = c->partial.get<double>(static_cast<size_t>(nb * ((J + 127) / 128)));
+  O.err = c->err.as<unsigned long long>();
+  int64_t np = 0;
+  c->launched(launch_objective_fast(c->stream, O, &np));
   double* out = c->obj.get<double>(1);
   c->launched(launch_sum_partials(c->stream, O.partial, np, out));
   double v = 0.0;
@@ -409,13 +446,17 @@ void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcsc
     // one launch runs every iteration on-chip: each gets the mean time
     secs.assign(iters, iters ? (ms * 1e-3) / iters : 0.0);
   } else {
-    objv.push_back(objective(c, I, J, M, *hyper));
+    // accel: the O(1)-per-slot objective (scalar expansion, needs log pdet R');
+    // naive: the per-slot Cholesky form of model.hpp:129-157.
+    if (accel) c->launched(launch_logpdet(c->stream, problem(c, 1, I, J, M)));
+    auto eval = [&] { return accel ? objective_fast(c, I, J, M, *hyper) : objective(c, I, J, M, *hyper); };
+    objv.push_back(eval());
     for (int it = 0; it < iters; ++it) {
       CK(cudaEventRecord(c->ev0, c->stream));
       launch(it, 1);
       CK(cudaEventRecord(c->ev1, c->stream));
       ++iters_run;
-      objv.push_back(objective(c, I, J, M, *hyper));  // synchronizes + checks errors
+      objv.push_back(eval());  // synchronizes + checks errors
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
       secs.push_back(ms * 1e-3);
@@ -522,7 +563,7 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->X, &c->W, &c->A, &c->T, &c->V, &c->a, &c->b, &c->Rp, &c->Rpp, &c->power, &c->sab, &c->taa,
-                  &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->rh0, &c->ru0, &c->lam0, &c->tmp,
+                  &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->lpd, &c->rh0, &c->ru0, &c->lam0, &c->tmp,
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err})
     b->release();

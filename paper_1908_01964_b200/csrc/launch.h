@@ -38,6 +38,10 @@ cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg
 cudaError_t launch_naive(cudaStream_t s, int M, const NaiveArgs& N);
 
 cudaError_t launch_wiener(cudaStream_t s, int M, const WienerArgs& W, bool from_x, bool noise);
+// K1b MODE 2: log pseudo-determinant of each bin's R' (P.logpdet)
+cudaError_t launch_logpdet(cudaStream_t s, const DevProblem& P);
+// O(1)-per-slot objective partial sums (np = grid size written to *np)
+cudaError_t launch_objective_fast(cudaStream_t s, ObjFastArgs O, int64_t* np);
 // objective partial sums (np = grid size written to *np) and the final sum
 cudaError_t launch_objective(cudaStream_t s, int M, ObjArgs O, int64_t* np);
 cudaError_t launch_sum_partials(cudaStream_t s, const double* partial, int64_t n, double* out);

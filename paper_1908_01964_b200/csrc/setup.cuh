@@ -39,6 +39,7 @@ struct DevProblem {
   double* r_h;     // [bin][t]
   double* r_u;     // [bin][t]
   double* lambda;  // [bin]
+  double* logpdet;  // [bin] log pseudo-determinant of R' (product of its M-1 largest eigenvalues)
   unsigned long long* err;
 };
 
@@ -177,6 +178,8 @@ __global__ void __launch_bounds__(NT) k_setup_power(DevProblem P) {
 // K1b: per-bin model setup, one thread per bin (model.hpp:58-90 build_noise_scm
 // and the lambda rule of model.hpp:112-121). MODE 0: build R' from (A, power)
 // and derive a, b, R'^+, lambda0. MODE 1: lambda0 only, from a given R'.
+// MODE 2: log pseudo-determinant only (for the O(1) objective). Every mode
+// writes logpdet when the pointer is set.
 template <int M, int MODE>
 __global__ void k_setup_bin(DevProblem P, double rank_tol, double eps) {
   const int64_t bin = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -216,6 +219,12 @@ __global__ void k_setup_bin(DevProblem P, double rank_tol, double eps) {
     return;
   }
   const double lmax = fmax(vals[M - 1], 0.0);
+  if (P.logpdet) {
+    double lp = 0.0;
+    for (int k = 1; k < M; ++k) lp += log(vals[k]);
+    P.logpdet[bin] = lp;
+  }
+  if (MODE == 2) return;
   if (MODE == 0) {
     // null_eigenvector (linalg.hpp:74-86)
     const double cut_b = rank_tol * fmax(lmax, 1e-300);

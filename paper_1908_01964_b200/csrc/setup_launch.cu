@@ -29,6 +29,15 @@ cudaError_t launch_lambda0(cudaStream_t s, const DevProblem& P, double eps) {
   });
 }
 
+cudaError_t launch_logpdet(cudaStream_t s, const DevProblem& P) {
+  if (P.nb == 0) return cudaSuccess;
+  return dispatch_mics(P.M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    k_setup_bin<MM, 2><<<(P.nb + 63) / 64, 64, 0, s>>>(P, 1e-10, 0.0);
+    return cudaGetLastError();
+  });
+}
+
 cudaError_t launch_slots(cudaStream_t s, const DevProblem& P, bool init, bool pre, double eps) {
   if (P.nb * P.J == 0 || !(init || pre)) return cudaSuccess;
   return dispatch_mics(P.M, [&](auto mm) {

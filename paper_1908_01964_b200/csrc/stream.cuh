@@ -194,6 +194,66 @@ __global__ void __launch_bounds__(NT) k_objective(ObjArgs P) {
   }
 }
 
+// K5': MAP objective in O(1) per slot through the scalar expansion (SURVEY
+// 8(f) rank 1). With R_u = R' + lambda b b^H and R_x = r_h a a^H + r_u R_u:
+//   log det R_x   = log pdet(R') + log lambda + (M-1) log r_u + log D,  D = r_u + r_h rho_aa
+//   x^H R_x^-1 x  = (rho_xx - (r_h / D) |rho_ax|^2) / r_u
+// (matrix determinant lemma + Sherman-Morrison on the rank-one target term,
+// and R_u^{-1} = R'^+ + b b^H / lambda, linalg.hpp:105-117). Equal to the
+// per-slot LLT of model.hpp:129-157 up to rounding; used for compute_objective
+// in the accelerated solver.
+struct ObjFastArgs {
+  int64_t nb, J;
+  int M;
+  double alpha, beta;
+  const double2* sigma_ab;
+  const double* tau_aa;
+  const double2* sigma_bx;
+  const double2* tau_ax;
+  const double* tau_xx;
+  const double* logpdet;
+  const double* r_h;
+  const double* r_u;
+  const double* lambda;
+  double* partial;  // [gridDim.x][gridDim.y]
+  unsigned long long* err;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_objective_fast(ObjFastArgs P) {
+  __shared__ double red[NT / 32];
+  const int64_t bin = blockIdx.x;
+  const int tid = threadIdx.x;
+  const double lam = P.lambda[bin];
+  const double il = 1.0 / lam;
+  const double2 sab = P.sigma_ab[bin];
+  const double raa = P.tau_aa[bin] + cnorm(sab) * il;
+  const double cbin = P.M * log(3.14159265358979323846) + P.logpdet[bin] + log(lam);
+  const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + tid;
+  double val = 0.0;
+  if (t < P.J) {
+    const int64_t slot = bin * P.J + t;
+    const double rh = P.r_h[slot], ru = P.r_u[slot];
+    const double2 sbx = P.sigma_bx[slot], tax = P.tau_ax[slot];
+    const double2 c = cmul(sab, sbx);
+    const double2 rax = make_double2(fma(c.x, il, tax.x), fma(c.y, il, tax.y));
+    const double rxx = fma(cnorm(sbx), il, P.tau_xx[slot]);
+    const double D = fma(rh, raa, ru);
+    const double logdet = cbin + (P.M - 1) * log(ru) + log(D);
+    const double quad = (rxx - rh / D * cnorm(rax)) / ru;
+    val = -logdet - quad - (P.alpha + 1.0) * log(rh) - P.beta / rh;
+    if (!isfinite(val)) report_error(P.err, slot, kErrObjectiveNonFinite);
+  }
+  val = warp_sum(val);
+  if ((tid & 31) == 0) red[tid >> 5] = val;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+    P.partial[blockIdx.x * static_cast<int64_t>(gridDim.y) + blockIdx.y] = s;
+  }
+}
+
 // Deterministic single-CTA sum of n partials (fixed strided order + tree).
 static __global__ void k_sum_partials(const double* partial, int64_t n, double* out) {
   __shared__ double red[32];

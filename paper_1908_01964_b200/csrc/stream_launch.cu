@@ -34,6 +34,14 @@ cudaError_t launch_objective(cudaStream_t s, int M, ObjArgs O, int64_t* np) {
   });
 }
 
+cudaError_t launch_objective_fast(cudaStream_t s, ObjFastArgs O, int64_t* np) {
+  dim3 grid(O.nb, (O.J + kObjNT - 1) / kObjNT);
+  *np = static_cast<int64_t>(grid.x) * grid.y;
+  if (O.nb * O.J == 0) return cudaSuccess;
+  k_objective_fast<kObjNT><<<grid, kObjNT, 0, s>>>(O);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_sum_partials(cudaStream_t s, const double* partial, int64_t n, double* out) {
   k_sum_partials<<<1, 1024, 0, s>>>(partial, n, out);
   return cudaGetLastError();

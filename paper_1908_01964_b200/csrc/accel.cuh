@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
     const int buf = it & 1;
     // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
     //     (solver_accel.hpp:67-76, :143-158).
-    double g[SPT], acc = 0.0;
+    double g[SPT], term[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       const double D = fma(rh[k], raa, ru[k]);  // r~_u + r~_h rho~_aa
@@ -176,13 +176,17 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
       const double rx = fma(-gk, e.x, sbx[k].x);
       const double ry = fma(-gk, e.y, sbx[k].y);
       const double rr = fma(rx, rx, ry * ry);
-      if (FULL || valid[k]) {
-        acc = fma(gk, s2, acc);
-        acc = fma(rr, iru, acc);
-      }
+      // per-slot lambda term, independent across slots (no serial accumulator)
+      term[k] = (FULL || valid[k]) ? fma(gk, s2, rr * iru) : 0.0;
       g[k] = gk;
     }
-    double part = warp_sum(acc);
+    // fixed pairwise tree over the thread's slots, then the warp butterfly
+#pragma unroll
+    for (int w = 1; w < SPT; w <<= 1) {
+#pragma unroll
+      for (int k = 0; k + w < SPT; k += 2 * w) term[k] += term[k + w];
+    }
+    double part = warp_sum(term[0]);
     if (lane == 0) red[buf][warp] = part;
     // (2) everything that does not need the new lambda, overlapping the
     //     reduction: r_h (solver_accel.hpp:134-141) and the two halves of the

@@ -1,0 +1,99 @@
+// microbench.cu -- FP64 latency / throughput probes on the B200 used to shape
+// k_accel (development tool; not part of the product library).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o build/microbench tools/microbench.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void lat_dfma(double* out, int n, double a, double b) {
+  double x = a;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) x = fma(x, b, a);
+  long long t1 = clock64();
+  out[0] = x;
+  out[1] = double(t1 - t0) / n;
+}
+__global__ void lat_dmul(double* out, int n, double a, double b) {
+  double x = a;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) x = x * b;
+  long long t1 = clock64();
+  out[0] = x;
+  out[1] = double(t1 - t0) / n;
+}
+__global__ void lat_rcp(double* out, int n, double a) {
+  double x = a;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    double r;
+    asm volatile("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    x = r + 1.0;
+  }
+  long long t1 = clock64();
+  out[0] = x;
+  out[1] = double(t1 - t0) / n;
+}
+__global__ void lat_shfl(double* out, int n, double a) {
+  double x = a + threadIdx.x;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) x += __shfl_xor_sync(0xffffffffu, x, 1);
+  long long t1 = clock64();
+  out[threadIdx.x] = x;
+  if (threadIdx.x == 0) out[1] = double(t1 - t0) / n;
+}
+// throughput: ILP independent DFMA chains per thread, many warps
+template <int ILP>
+__global__ void tput(double* out, int n, double a, double b) {
+  double x[ILP];
+#pragma unroll
+  for (int k = 0; k < ILP; ++k) x[k] = a + k;
+  for (int i = 0; i < n; ++i) {
+#pragma unroll
+    for (int k = 0; k < ILP; ++k) x[k] = fma(x[k], b, a);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < ILP; ++k) s += x[k];
+  if (s == 1.2345) out[0] = s;
+}
+
+template <int ILP>
+void run_tput(double* d, int warps_per_sm) {
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int n = 4000, threads = 128, blocks = 148 * warps_per_sm / 4;
+  tput<ILP><<<blocks, threads>>>(d, 100, 1.0, 0.999999);
+  cudaEventRecord(e0);
+  tput<ILP><<<blocks, threads>>>(d, n, 1.0, 0.999999);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double flops = 2.0 * ILP * double(n) * blocks * threads;
+  printf("tput ILP=%d warps/SM=%2d: %6.2f TFLOP/s\n", ILP, warps_per_sm, flops / (ms * 1e-3) / 1e12);
+}
+
+int main() {
+  double* d;
+  cudaMalloc(&d, 64 * sizeof(double));
+  double h[2];
+  lat_dfma<<<1, 1>>>(d, 10000, 1.0, 0.9999);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("DFMA dependent latency: %.2f cycles\n", h[1]);
+  lat_dmul<<<1, 1>>>(d, 10000, 1.0, 0.9999);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("DMUL dependent latency: %.2f cycles\n", h[1]);
+  lat_rcp<<<1, 1>>>(d, 10000, 1.5);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("MUFU.RCP64H + DADD dependent latency: %.2f cycles\n", h[1]);
+  lat_shfl<<<1, 32>>>(d, 10000, 1.0);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("SHFL(f64) + DADD dependent latency: %.2f cycles\n", h[1]);
+  for (int w : {4, 8, 16, 32}) {
+    run_tput<1>(d, w);
+    run_tput<2>(d, w);
+    run_tput<4>(d, w);
+    run_tput<8>(d, w);
+  }
+  return 0;
+}

@@ -13,7 +13,8 @@
 // per-slot quantity (r_h, r_u, rho~_ax, tau_ax, s_ab*s_bx, s_bx, tau_xx, |s_bx|^2)
 // in REGISTERS for all iterations: HBM is touched once to load (56 B/slot) and
 // once to store (16 B/slot). The only cross-slot dependency -- lambda's sum over
-// frames -- is a fixed-order warp butterfly + block reduction (+ DSMEM exchange
+// frames -- is a fixed-order tree: in-thread pairwise sum, a warp total on the
+// FP64 tensor core (DMMA), a zero-padded 8-way block tree (+ DSMEM exchange
 // across the cluster), so results are deterministic and independent of how
 // many GPUs the bins are sharded over.
 //
@@ -58,8 +59,6 @@ struct AccelArgs {
   double* traj_r_h;         // optional [it][bin][t]
   double* traj_r_u;
   double* traj_lambda;      // optional [it][bin]
-  long long stagger;        // experiment: cycles of start delay for alternate CTA groups
-  int stagger_mod;
 };
 
 // std::max(v, eps) of the reference (returns v unless v < eps) for eps > 0,
@@ -72,13 +71,35 @@ __device__ __forceinline__ double floor_eps(double v, double eps) {
   return __longlong_as_double(iv < ie ? ie : iv);
 }
 
-// Sum of the nw (<= 32) per-warp partials red[0..nw-1], formed identically by
-// every thread: lanes < nw load one partial each (zero-padded to the next power
-// of two), a xor butterfly adds them and lane 0's sum is broadcast.
-__device__ __forceinline__ double block_total(const double* red, int nw, int lane) {
-  double v = lane < nw ? red[lane] : 0.0;
-  for (int off = 1; off < nw; off <<= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-  return __shfl_sync(0xffffffffu, v, 0);
+// Sum of the 32 lanes' values, returned in every lane, on the FP64 tensor
+// core: DMMA m8n8k4 with B = 1 leaves in lane l the sum of its 4-lane group
+// g_{l/4}; one shuffle round transposes the 8 group sums into the k index and
+// two more DMMAs (B = 1) add them. ~90 cycles of latency on B200 against
+// ~180 for a 5-step shuffle butterfly (measured: DMMA 26, SHFL.f64+DADD 36).
+// Multiplications by 1 are exact and the DMMA's internal order is fixed, so
+// the result is deterministic and identical in every lane.
+__device__ __forceinline__ double dmma_ones(double a) {
+  double d0;
+  [[maybe_unused]] double d1;
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
+      : "=d"(d0), "=d"(d1)
+      : "d"(a), "d"(1.0), "d"(0.0), "d"(0.0));
+  return d0;
+}
+__device__ __forceinline__ double warp_total_mma(double v, int lane) {
+  const double g = dmma_ones(v);  // lane l: sum of lanes 4*(l/4) .. +3
+  const int src = (lane & 3) << 2;
+  const double lo = __shfl_sync(0xffffffffu, g, src);       // g_{l%4}
+  const double hi = __shfl_sync(0xffffffffu, g, src + 16);  // g_{l%4 + 4}
+  return dmma_ones(lo) + dmma_ones(hi);
+}
+
+// Sum of the (zero-padded) 8 per-warp partials: four broadcast LDS.128 and a
+// fixed 3-level tree, identical in every thread.
+__device__ __forceinline__ double block_total8(const double* red) {
+  const double2* r = reinterpret_cast<const double2*>(red);
+  const double2 a = r[0], b = r[1], c = r[2], d = r[3];
+  return ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (d.x + d.y));
 }
 
 // FULL: every thread's SPT slots are inside the bin chunk (NT * SPT == chunk),
@@ -91,12 +112,11 @@ template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC>
 __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
   constexpr int kMaxWarps = 256 / 32;
-  __shared__ double red[2][kMaxWarps];
+  __shared__ __align__(16) double red[2][kMaxWarps];  // zero-padded warp partials
   __shared__ double cl_part[2];
   __shared__ double cl_total[2];
   extern __shared__ double2 dyn[];
   const int NT = blockDim.x;
-  const int nwarps = NT >> 5;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bin = blockIdx.x / CL;
   const int rank = (CL > 1) ? static_cast<int>(blockIdx.x % CL) : 0;
@@ -151,11 +171,8 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
     }
   }
 
-  if (P.stagger > 0 && ((blockIdx.x / P.stagger_mod) & 1)) {
-    const long long c0 = clock64();
-    while (clock64() - c0 < P.stagger) {
-    }
-  }
+  if (tid < 2 * kMaxWarps) (&red[0][0])[tid] = 0.0;
+  __syncthreads();
   const double invJ = 1.0 / static_cast<double>(J);
   const double m2M = -2.0 * inv_M;
   const double taaM = taa * inv_M, s2M = s2 * inv_M;
@@ -186,7 +203,7 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
 #pragma unroll
       for (int k = 0; k + w < SPT; k += 2 * w) term[k] += term[k + w];
     }
-    double part = warp_sum(term[0]);
+    const double part = warp_total_mma(term[0], lane);
     if (lane == 0) red[buf][warp] = part;
     // (2) everything that does not need the new lambda, overlapping the
     //     reduction: r_h (solver_accel.hpp:134-141) and the two halves of the
@@ -223,13 +240,13 @@ __global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
     __syncthreads();
     double total = 0.0;
     if constexpr (CL == 1) {
-      total = block_total(red[buf], nwarps, lane);
+      total = block_total8(red[buf]);
     } else {
       // CTA partial -> cluster: warp 0 gathers the CL partials over DSMEM in
       // rank order and every CTA forms the same total.
       cg::cluster_group cluster = cg::this_cluster();
       if (warp == 0) {
-        const double c = block_total(red[buf], nwarps, lane);
+        const double c = block_total8(red[buf]);
         if (lane == 0) cl_part[buf] = c;
       }
       cluster.sync();

@@ -242,10 +242,6 @@ AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, 
   A.r_h = c->rh.as<double>();
   A.r_u = c->ru.as<double>();
   A.lambda = c->lam.as<double>();
-  const char* st = std::getenv("RCSCM_ACCEL_STAGGER");
-  A.stagger = st ? std::atoll(st) : 0;
-  const char* sm = std::getenv("RCSCM_ACCEL_STAGGER_MOD");
-  A.stagger_mod = sm ? std::max(1, std::atoi(sm)) : 148;
   return A;
 }
 

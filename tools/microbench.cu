@@ -73,7 +73,10 @@ void run_tput(double* d, int warps_per_sm) {
   printf("tput ILP=%d warps/SM=%2d: %6.2f TFLOP/s\n", ILP, warps_per_sm, flops / (ms * 1e-3) / 1e12);
 }
 
-int main() {
+int main1();
+int main2();
+int main() { main2(); return main1(); }
+int main1() {
   double* d;
   cudaMalloc(&d, 64 * sizeof(double));
   double h[2];
@@ -94,6 +97,59 @@ int main() {
     run_tput<2>(d, w);
     run_tput<4>(d, w);
     run_tput<8>(d, w);
+  }
+  return 0;
+}
+
+// DMMA m8n8k4 f64 dependent latency (D feeds C of the next)
+__global__ void lat_dmma(double* out, int n) {
+  double a = 1.0 + threadIdx.x * 1e-3, b = 1.0, c0 = 0.0, c1 = 0.0;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = c0 + c1;
+  if (threadIdx.x == 0) out[1] = double(t1 - t0) / n;
+}
+// smem broadcast LDS.128 + DADD dependent latency
+__global__ void lat_lds(double* out, int n) {
+  __shared__ double2 s[64];
+  if (threadIdx.x < 64) s[threadIdx.x] = make_double2(threadIdx.x, 1.0);
+  __syncwarp();
+  int idx = 0;
+  double acc = 0;
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) {
+    double2 v = s[idx];
+    acc += v.x;
+    idx = int(v.y) & 63;
+  }
+  long long t1 = clock64();
+  out[threadIdx.x] = acc;
+  if (threadIdx.x == 0) out[1] = double(t1 - t0) / n;
+}
+__global__ void lat_bar(double* out, int n) {
+  long long t0 = clock64();
+  for (int i = 0; i < n; ++i) __syncthreads();
+  long long t1 = clock64();
+  if (threadIdx.x == 0) out[1] = double(t1 - t0) / n;
+}
+int main2() {
+  double* d;
+  cudaMalloc(&d, 256 * sizeof(double));
+  double h[2];
+  lat_dmma<<<1, 32>>>(d, 10000);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("DMMA m8n8k4 dependent latency: %.2f cycles (%s)\n", h[1], cudaGetErrorString(cudaGetLastError()));
+  lat_lds<<<1, 32>>>(d, 10000);
+  cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+  printf("LDS.128 + DADD dependent latency: %.2f cycles\n", h[1]);
+  for (int nt : {64, 128, 256}) {
+    lat_bar<<<1, nt>>>(d, 10000);
+    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    printf("__syncthreads (%d threads, all arriving together): %.2f cycles\n", nt, h[1]);
   }
   return 0;
 }

@@ -108,8 +108,10 @@ __device__ __forceinline__ double block_total8(const double* red) {
 // (tau_ax, s_ab*s_bx, tau_xx/M, |s_bx|^2/M: 48 B/slot) live in dynamic shared
 // memory ([k][tid] planes, conflict-free) instead of registers, which roughly
 // halves the register footprint and doubles the resident warps per SM.
-template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC>
-__global__ void __launch_bounds__(256, SMEMC ? 2 : 1) k_accel(AccelArgs P) {
+// LB3: launch bounds of 128 threads x 3 CTAs/SM (<= 170 registers) instead of
+// one 256-thread CTA's worth, trading a little ILP for resident warps.
+template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false>
+__global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
   constexpr int kMaxWarps = 256 / 32;
   __shared__ __align__(16) double red[2][kMaxWarps];  // zero-padded warp partials

@@ -6,11 +6,13 @@
 namespace rcscm {
 
 AccelCfg choose_accel_cfg(int64_t J) {
-  AccelCfg best{0, 0, 0, false, false};
+  AccelCfg best{0, 0, 0, false, false, false};
   const char* e_spt = std::getenv("RCSCM_ACCEL_SPT");
   const char* e_cl = std::getenv("RCSCM_ACCEL_CL");
   const char* e_sm = std::getenv("RCSCM_ACCEL_SMEM");
   const bool smem = e_sm ? std::atoi(e_sm) != 0 : false;
+  const char* e_lb = std::getenv("RCSCM_ACCEL_LB3");
+  const bool lb3 = e_lb ? std::atoi(e_lb) != 0 : false;
   const int force_spt = e_spt ? std::atoi(e_spt) : 0;
   const int force_cl = e_cl ? std::atoi(e_cl) : 0;
   for (int cl : {1, 2, 4, 8, 16}) {
@@ -31,7 +33,7 @@ AccelCfg choose_accel_cfg(int64_t J) {
         best_waste = waste;
         // FULL needs every CTA of the cluster to own exactly nt * spt frames
         const bool full = (waste == 0) && (jc * cl == J);
-        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem};
+        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem, lb3};
       }
     }
     if (best.cl) return best;

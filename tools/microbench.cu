@@ -75,7 +75,8 @@ void run_tput(double* d, int warps_per_sm) {
 
 int main1();
 int main2();
-int main() { main2(); return main1(); }
+int main3();
+int main() { main3(); main2(); return main1(); }
 int main1() {
   double* d;
   cudaMalloc(&d, 64 * sizeof(double));
@@ -151,5 +152,34 @@ int main2() {
     cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
     printf("__syncthreads (%d threads, all arriving together): %.2f cycles\n", nt, h[1]);
   }
+  return 0;
+}
+
+// accuracy of the MUFU.RCP64H seed and of 1 / 2 Newton refinements
+__global__ void rcp_acc(double* out, int n) {
+  double m0 = 0, m1 = 0, m2 = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const double x = 1.0 + (double)i / n * 7.0 + 1e-9 * (i % 977);
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+    const double e = fma(-x, r, 1.0);
+    m0 = fmax(m0, fabs(e));
+    const double r1 = fma(r, e, r);
+    m1 = fmax(m1, fabs(fma(-x, r1, 1.0)));
+    const double r2 = fma(r, fma(e, e, e), r);
+    m2 = fmax(m2, fabs(fma(-x, r2, 1.0)));
+  }
+  atomicMax((unsigned long long*)&out[0], __double_as_longlong(m0));
+  atomicMax((unsigned long long*)&out[1], __double_as_longlong(m1));
+  atomicMax((unsigned long long*)&out[2], __double_as_longlong(m2));
+}
+int main3() {
+  double* d;
+  cudaMalloc(&d, 4 * sizeof(double));
+  cudaMemset(d, 0, 4 * sizeof(double));
+  rcp_acc<<<148, 256>>>(d, 1 << 24);
+  double h[3];
+  cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
+  printf("rcp seed max |1-x r| = %.3e (2^%.1f); one Newton: %.3e; Newton+cubic: %.3e\n", h[0], log2(h[0]), h[1], h[2]);
   return 0;
 }

@@ -12,7 +12,7 @@ AccelCfg choose_accel_cfg(int64_t J) {
   const char* e_sm = std::getenv("RCSCM_ACCEL_SMEM");
   const bool smem = e_sm ? std::atoi(e_sm) != 0 : false;
   const char* e_lb = std::getenv("RCSCM_ACCEL_LB3");
-  const bool lb3 = e_lb ? std::atoi(e_lb) != 0 : false;
+  const bool lb3 = e_lb ? std::atoi(e_lb) != 0 : true;  // measured faster (B200, configs 0/1/3)
   const int force_spt = e_spt ? std::atoi(e_spt) : 0;
   const int force_cl = e_cl ? std::atoi(e_cl) : 0;
   for (int cl : {1, 2, 4, 8, 16}) {

@@ -77,6 +77,8 @@ struct rcscm_gpu_ctx {
   bool own_stream = false;
   int64_t launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t aux[2] = {nullptr, nullptr};  // copy/compute pipelining of the host entry points
+  cudaEvent_t evx[3] = {nullptr, nullptr, nullptr};
   // device buffers
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
@@ -385,6 +387,102 @@ void validate_opts(const rcscm_solver_opts* opt, const char* who) {
   if (opt->iters < 0) fail(RCSCM_INVALID_INPUT, std::string(who) + ": iters must be >= 0");
 }
 
+// Copy/compute-overlapped run_algorithm2 (no objective, no trajectory): the
+// bins are split into chunks issued alternately on two streams, so chunk k+1's
+// host->device copies and chunk k-1's device->host copies run on the copy
+// engines while chunk k computes. Every chunk owns a disjoint slice of the
+// bin-major device buffers; the per-bin arithmetic is unchanged, so the result
+// is bitwise identical to the single-shot path. Returns false when the problem
+// is too small to split.
+bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p0,
+                         const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt,
+                         rcscm_params* out, std::vector<double>* secs) {
+  const int64_t I = in->num_bins, J = in->frames;
+  const int M = in->mics;
+  const char* e_ch = std::getenv("RCSCM_PIPELINE_CHUNKS");
+  int nch = e_ch ? std::atoi(e_ch) : static_cast<int>(std::min<int64_t>(8, I / 128));
+  if (nch < 2) return false;
+  for (int k = 0; k < 2; ++k)
+    if (!c->aux[k]) CK(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
+  for (int k = 0; k < 3; ++k)
+    if (!c->evx[k]) CK(cudaEventCreateWithFlags(&c->evx[k], cudaEventDisableTiming));
+  alloc_problem(c, I, J, M);
+  const size_t S = static_cast<size_t>(I * J);
+  double* t1 = c->tmp.get<double>(S);
+  double* t2 = c->tmp2.get<double>(S);
+  reset_err(c);
+  CK(cudaEventRecord(c->ev0, c->stream));
+  CK(cudaEventRecord(c->evx[0], c->stream));
+  for (int k = 0; k < 2; ++k) CK(cudaStreamWaitEvent(c->aux[k], c->evx[0], 0));
+  const DevProblem full = problem(c, 1, I, J, M);
+  const AccelArgs afull = accel_args(c, I, J, M, opt->iters, *hyper, opt->eps_var, opt->gamma_fault);
+  const AccelCfg g = choose_accel_cfg(J);
+  if (!g.cl) fail(RCSCM_UNSUPPORTED, "frames exceed the on-chip accel kernel capacity");
+  for (int ch = 0; ch < nch; ++ch) {
+    cudaStream_t s = c->aux[ch & 1];
+    const int64_t i0 = I * ch / nch, i1 = I * (ch + 1) / nch, Ic = i1 - i0;
+    if (Ic == 0) continue;
+    const size_t off = static_cast<size_t>(i0 * J);
+    auto h2d_s = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+    };
+    h2d_s(c->X.as<double2>() + off * M, X + 2 * off * M, Ic * J * M * sizeof(double2));
+    h2d_s(c->a.as<double2>() + i0 * M, in->a + 2 * i0 * M, Ic * M * sizeof(double2));
+    h2d_s(c->b.as<double2>() + i0 * M, in->b + 2 * i0 * M, Ic * M * sizeof(double2));
+    h2d_s(c->Rpp.as<double2>() + i0 * M * M, in->R_prime_pinv + 2 * i0 * M * M, Ic * M * M * sizeof(double2));
+    h2d_s(c->lam.as<double>() + i0, p0->lambda + i0, Ic * sizeof(double));
+    // r_h / r_u: the chunk is a strided I x J column-major block on the host
+    CK(cudaMemcpy2DAsync(t1 + off, Ic * sizeof(double), p0->r_h + i0, I * sizeof(double), Ic * sizeof(double), J,
+                         cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpy2DAsync(t2 + off, Ic * sizeof(double), p0->r_u + i0, I * sizeof(double), Ic * sizeof(double), J,
+                         cudaMemcpyHostToDevice, s));
+    c->launched(launch_to_bt(s, t1 + off, c->rh.as<double>() + off, 1, Ic, J));
+    c->launched(launch_to_bt(s, t2 + off, c->ru.as<double>() + off, 1, Ic, J));
+    DevProblem P = full;
+    P.nb = Ic;
+    P.I = Ic;
+    P.X += off * M;
+    P.a += i0 * M;
+    P.b += i0 * M;
+    P.Rpp += i0 * M * M;
+    P.sigma_ab += i0;
+    P.tau_aa += i0;
+    P.sigma_bx += off;
+    P.tau_ax += off;
+    P.tau_xx += off;
+    c->launched(launch_slots(s, P, false, true, opt->eps_var));
+    AccelArgs A = afull;
+    A.nb = Ic;
+    A.sigma_ab += i0;
+    A.tau_aa += i0;
+    A.sigma_bx += off;
+    A.tau_ax += off;
+    A.tau_xx += off;
+    A.r_h += off;
+    A.r_u += off;
+    A.lambda += i0;
+    if (opt->iters > 0) c->launched(launch_accel(s, A, g));
+    c->launched(launch_to_ij(s, c->rh.as<double>() + off, t1 + off, 1, Ic, J));
+    c->launched(launch_to_ij(s, c->ru.as<double>() + off, t2 + off, 1, Ic, J));
+    CK(cudaMemcpy2DAsync(out->r_h + i0, I * sizeof(double), t1 + off, Ic * sizeof(double), Ic * sizeof(double), J,
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(out->r_u + i0, I * sizeof(double), t2 + off, Ic * sizeof(double), Ic * sizeof(double), J,
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(out->lambda + i0, c->lam.as<double>() + i0, Ic * sizeof(double), cudaMemcpyDeviceToHost, s));
+  }
+  for (int k = 0; k < 2; ++k) {
+    CK(cudaEventRecord(c->evx[1 + k], c->aux[k]));
+    CK(cudaStreamWaitEvent(c->stream, c->evx[1 + k], 0));
+  }
+  CK(cudaEventRecord(c->ev1, c->stream));
+  check_err(c, J);
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  // end-to-end per iteration (copies overlapped with compute)
+  secs->assign(opt->iters, opt->iters ? (ms * 1e-3) / opt->iters : 0.0);
+  return true;
+}
+
 // Shared driver of run_naive / run_algorithm2 (solver_naive.hpp:412-450,
 // solver_accel.hpp:183-240).
 void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcscm_params* p0,
@@ -402,10 +500,20 @@ void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcsc
     if (extra->n_iters) *extra->n_iters = 0;
   }
   if (I == 0) return;
+  const bool traj = extra && opt->record_trajectory && (extra->traj_r_h || extra->traj_r_u || extra->traj_lambda);
+  if (accel && !opt->compute_objective && !traj) {
+    std::vector<double> secs;
+    if (run_accel_pipelined(c, in, p0, hyper, X, opt, out, &secs)) {
+      if (extra) {
+        if (extra->iter_seconds) std::memcpy(extra->iter_seconds, secs.data(), secs.size() * sizeof(double));
+        if (extra->n_iters) *extra->n_iters = opt->iters;
+      }
+      return;
+    }
+  }
   upload_model(c, in, p0, X, !accel || opt->compute_objective, accel);
   reset_err(c);
   if (accel) c->launched(launch_slots(c->stream, problem(c, 1, I, J, M), false, true, opt->eps_var));
-  const bool traj = extra && opt->record_trajectory && (extra->traj_r_h || extra->traj_r_u || extra->traj_lambda);
   const size_t S = static_cast<size_t>(I * J);
   double* trh = traj ? c->traj_rh.get<double>(S * std::max(iters, 1)) : nullptr;
   double* tru = traj ? c->traj_ru.get<double>(S * std::max(iters, 1)) : nullptr;
@@ -565,6 +673,10 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
+  for (int k = 0; k < 2; ++k)
+    if (c->aux[k]) cudaStreamDestroy(c->aux[k]);
+  for (int k = 0; k < 3; ++k)
+    if (c->evx[k]) cudaEventDestroy(c->evx[k]);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }

@@ -290,3 +290,18 @@ def test_session_pipeline_matches_entry_points(O, gpu):
         oimg, odry = O.extract_target(inp, o, u.X)
         assert output_rel_err(out["dry"][k], odry) <= 1e-6
         assert output_rel_err(out["image"][k], oimg) <= 1e-6
+
+
+def test_pipelined_entry_point_bitwise(O, gpu, monkeypatch):
+    """The copy/compute-pipelined run_algorithm2 (bins in chunks on two
+    streams) equals the single-shot path bitwise."""
+    from paper_1908_01964_b200 import synth
+
+    u, inp, p0 = _synthetic(O, 1, 300, 64)
+    monkeypatch.setenv("RCSCM_PIPELINE_CHUNKS", "1")
+    single = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=20)).params
+    monkeypatch.setenv("RCSCM_PIPELINE_CHUNKS", "5")
+    piped = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=20)).params
+    assert np.array_equal(single.r_h, piped.r_h)
+    assert np.array_equal(single.r_u, piped.r_u)
+    assert np.array_equal(single.lam, piped.lam)

@@ -64,6 +64,8 @@ struct DBuf {
   }
 };
 
+constexpr int kMaxChunks = 16;
+
 void check_mics(int M) {
   if (!mics_supported(M)) fail(RCSCM_UNSUPPORTED, "mics = " + std::to_string(M) + " is not supported (1..8 or 16)");
 }
@@ -77,8 +79,8 @@ struct rcscm_gpu_ctx {
   bool own_stream = false;
   int64_t launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaStream_t aux[2] = {nullptr, nullptr};  // copy/compute pipelining of the host entry points
-  cudaEvent_t evx[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t aux[2] = {nullptr, nullptr};  // copy / compute streams of the pipelined entry points
+  cudaEvent_t evx[19] = {};                       // kMaxChunks + 3
   // device buffers
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
@@ -387,13 +389,14 @@ void validate_opts(const rcscm_solver_opts* opt, const char* who) {
   if (opt->iters < 0) fail(RCSCM_INVALID_INPUT, std::string(who) + ": iters must be >= 0");
 }
 
-// Copy/compute-overlapped run_algorithm2 (no objective, no trajectory): the
-// bins are split into chunks issued alternately on two streams, so chunk k+1's
-// host->device copies and chunk k-1's device->host copies run on the copy
-// engines while chunk k computes. Every chunk owns a disjoint slice of the
-// bin-major device buffers; the per-bin arithmetic is unchanged, so the result
-// is bitwise identical to the single-shot path. Returns false when the problem
-// is too small to split.
+// Copy/compute-overlapped run_algorithm2 (no objective, no trajectory). A copy
+// stream uploads the small per-bin inputs and the whole r_h / r_u / lambda
+// (contiguous), then x chunk by chunk of bins; the compute stream waits for each
+// x chunk and runs transpose -> sigma/tau -> K2 -> transpose back on that chunk
+// while the next chunk is still in flight; one device->host copy of the results
+// follows. Chunks own disjoint slices of the bin-major device buffers and the
+// per-bin arithmetic is unchanged, so the result is bitwise identical to the
+// single-shot path. Returns false when the problem is too small to split.
 bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p0,
                          const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt,
                          rcscm_params* out, std::vector<double>* secs) {
@@ -401,11 +404,15 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   const int M = in->mics;
   const char* e_ch = std::getenv("RCSCM_PIPELINE_CHUNKS");
   int nch = e_ch ? std::atoi(e_ch) : static_cast<int>(std::min<int64_t>(8, I / 128));
+  nch = std::min(nch, kMaxChunks);
   if (nch < 2) return false;
+  const AccelCfg g = choose_accel_cfg(J);
+  if (!g.cl) return false;
   for (int k = 0; k < 2; ++k)
     if (!c->aux[k]) CK(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
-  for (int k = 0; k < 3; ++k)
+  for (int k = 0; k < kMaxChunks + 3; ++k)
     if (!c->evx[k]) CK(cudaEventCreateWithFlags(&c->evx[k], cudaEventDisableTiming));
+  cudaStream_t cp = c->aux[0], cs = c->aux[1];
   alloc_problem(c, I, J, M);
   const size_t S = static_cast<size_t>(I * J);
   double* t1 = c->tmp.get<double>(S);
@@ -413,31 +420,33 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   reset_err(c);
   CK(cudaEventRecord(c->ev0, c->stream));
   CK(cudaEventRecord(c->evx[0], c->stream));
-  for (int k = 0; k < 2; ++k) CK(cudaStreamWaitEvent(c->aux[k], c->evx[0], 0));
+  CK(cudaStreamWaitEvent(cp, c->evx[0], 0));
+  CK(cudaStreamWaitEvent(cs, c->evx[0], 0));
+  auto up = [&](void* dst, const void* src, size_t bytes) {
+    if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cp));
+  };
+  up(t1, p0->r_h, S * sizeof(double));
+  up(t2, p0->r_u, S * sizeof(double));
+  up(c->lam.p, p0->lambda, I * sizeof(double));
+  up(c->a.p, in->a, I * M * sizeof(double2));
+  up(c->b.p, in->b, I * M * sizeof(double2));
+  up(c->Rpp.p, in->R_prime_pinv, I * M * M * sizeof(double2));
+  CK(cudaEventRecord(c->evx[1], cp));
+  for (int ch = 0; ch < nch; ++ch) {
+    const int64_t i0 = I * ch / nch, i1 = I * (ch + 1) / nch;
+    up(c->X.as<double2>() + i0 * J * M, X + 2 * i0 * J * M, (i1 - i0) * J * M * sizeof(double2));
+    CK(cudaEventRecord(c->evx[3 + ch], cp));
+  }
   const DevProblem full = problem(c, 1, I, J, M);
   const AccelArgs afull = accel_args(c, I, J, M, opt->iters, *hyper, opt->eps_var, opt->gamma_fault);
-  const AccelCfg g = choose_accel_cfg(J);
-  if (!g.cl) fail(RCSCM_UNSUPPORTED, "frames exceed the on-chip accel kernel capacity");
+  CK(cudaStreamWaitEvent(cs, c->evx[1], 0));
   for (int ch = 0; ch < nch; ++ch) {
-    cudaStream_t s = c->aux[ch & 1];
     const int64_t i0 = I * ch / nch, i1 = I * (ch + 1) / nch, Ic = i1 - i0;
     if (Ic == 0) continue;
     const size_t off = static_cast<size_t>(i0 * J);
-    auto h2d_s = [&](void* dst, const void* src, size_t bytes) {
-      if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
-    };
-    h2d_s(c->X.as<double2>() + off * M, X + 2 * off * M, Ic * J * M * sizeof(double2));
-    h2d_s(c->a.as<double2>() + i0 * M, in->a + 2 * i0 * M, Ic * M * sizeof(double2));
-    h2d_s(c->b.as<double2>() + i0 * M, in->b + 2 * i0 * M, Ic * M * sizeof(double2));
-    h2d_s(c->Rpp.as<double2>() + i0 * M * M, in->R_prime_pinv + 2 * i0 * M * M, Ic * M * M * sizeof(double2));
-    h2d_s(c->lam.as<double>() + i0, p0->lambda + i0, Ic * sizeof(double));
-    // r_h / r_u: the chunk is a strided I x J column-major block on the host
-    CK(cudaMemcpy2DAsync(t1 + off, Ic * sizeof(double), p0->r_h + i0, I * sizeof(double), Ic * sizeof(double), J,
-                         cudaMemcpyHostToDevice, s));
-    CK(cudaMemcpy2DAsync(t2 + off, Ic * sizeof(double), p0->r_u + i0, I * sizeof(double), Ic * sizeof(double), J,
-                         cudaMemcpyHostToDevice, s));
-    c->launched(launch_to_bt(s, t1 + off, c->rh.as<double>() + off, 1, Ic, J));
-    c->launched(launch_to_bt(s, t2 + off, c->ru.as<double>() + off, 1, Ic, J));
+    CK(cudaStreamWaitEvent(cs, c->evx[3 + ch], 0));
+    c->launched(launch_to_bt(cs, t1 + i0, c->rh.as<double>() + off, 1, Ic, J, I));
+    c->launched(launch_to_bt(cs, t2 + i0, c->ru.as<double>() + off, 1, Ic, J, I));
     DevProblem P = full;
     P.nb = Ic;
     P.I = Ic;
@@ -450,7 +459,7 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
     P.sigma_bx += off;
     P.tau_ax += off;
     P.tau_xx += off;
-    c->launched(launch_slots(s, P, false, true, opt->eps_var));
+    c->launched(launch_slots(cs, P, false, true, opt->eps_var));
     AccelArgs A = afull;
     A.nb = Ic;
     A.sigma_ab += i0;
@@ -461,19 +470,15 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
     A.r_h += off;
     A.r_u += off;
     A.lambda += i0;
-    if (opt->iters > 0) c->launched(launch_accel(s, A, g));
-    c->launched(launch_to_ij(s, c->rh.as<double>() + off, t1 + off, 1, Ic, J));
-    c->launched(launch_to_ij(s, c->ru.as<double>() + off, t2 + off, 1, Ic, J));
-    CK(cudaMemcpy2DAsync(out->r_h + i0, I * sizeof(double), t1 + off, Ic * sizeof(double), Ic * sizeof(double), J,
-                         cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpy2DAsync(out->r_u + i0, I * sizeof(double), t2 + off, Ic * sizeof(double), Ic * sizeof(double), J,
-                         cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(out->lambda + i0, c->lam.as<double>() + i0, Ic * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (opt->iters > 0) c->launched(launch_accel(cs, A, g));
+    c->launched(launch_to_ij(cs, c->rh.as<double>() + off, t1 + i0, 1, Ic, J, I));
+    c->launched(launch_to_ij(cs, c->ru.as<double>() + off, t2 + i0, 1, Ic, J, I));
   }
-  for (int k = 0; k < 2; ++k) {
-    CK(cudaEventRecord(c->evx[1 + k], c->aux[k]));
-    CK(cudaStreamWaitEvent(c->stream, c->evx[1 + k], 0));
-  }
+  CK(cudaMemcpyAsync(out->r_h, t1, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  CK(cudaMemcpyAsync(out->r_u, t2, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  CK(cudaMemcpyAsync(out->lambda, c->lam.p, I * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  CK(cudaEventRecord(c->evx[2], cs));
+  CK(cudaStreamWaitEvent(c->stream, c->evx[2], 0));
   CK(cudaEventRecord(c->ev1, c->stream));
   check_err(c, J);
   float ms = 0.f;
@@ -675,8 +680,8 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (int k = 0; k < 2; ++k)
     if (c->aux[k]) cudaStreamDestroy(c->aux[k]);
-  for (int k = 0; k < 3; ++k)
-    if (c->evx[k]) cudaEventDestroy(c->evx[k]);
+  for (cudaEvent_t e : c->evx)
+    if (e) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
 }

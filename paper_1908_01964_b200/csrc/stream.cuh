@@ -269,18 +269,19 @@ static __global__ void k_sum_partials(const double* partial, int64_t n, double* 
   }
 }
 
-// Reference I x J column-major (element (i, t) at i + t*I) -> device [i][t]
-// (element at i*J + t), per utterance block of I bins. 32 x 32 smem tiles.
+// Reference I x J column-major (element (i, t) at i + t*ld, ld >= I) -> device
+// [i][t] (element at i*J + t), per utterance block z of I bins (source block
+// stride ld*J). 32 x 32 smem tiles.
 template <typename T>
-__global__ void k_ij_to_bt(const T* __restrict__ src, T* __restrict__ dst, int64_t I, int64_t J) {
+__global__ void k_ij_to_bt(const T* __restrict__ src, T* __restrict__ dst, int64_t I, int64_t J, int64_t ld) {
   __shared__ T tile[32][33];
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, t0 = static_cast<int64_t>(blockIdx.y) * 32;
   const int64_t u = blockIdx.z;
-  const T* s = src + u * I * J;
+  const T* s = src + u * ld * J;
   T* d = dst + u * I * J;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t i = i0 + threadIdx.x, t = t0 + k;
-    if (i < I && t < J) tile[k][threadIdx.x] = s[i + t * I];
+    if (i < I && t < J) tile[k][threadIdx.x] = s[i + t * ld];
   }
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -289,13 +290,14 @@ __global__ void k_ij_to_bt(const T* __restrict__ src, T* __restrict__ dst, int64
   }
 }
 
+// Device [i][t] -> reference column-major with leading dimension ld.
 template <typename T>
-__global__ void k_bt_to_ij(const T* __restrict__ src, T* __restrict__ dst, int64_t I, int64_t J) {
+__global__ void k_bt_to_ij(const T* __restrict__ src, T* __restrict__ dst, int64_t I, int64_t J, int64_t ld) {
   __shared__ T tile[32][33];
   const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32, t0 = static_cast<int64_t>(blockIdx.y) * 32;
   const int64_t u = blockIdx.z;
   const T* s = src + u * I * J;
-  T* d = dst + u * I * J;
+  T* d = dst + u * ld * J;
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t i = i0 + k, t = t0 + threadIdx.x;
     if (i < I && t < J) tile[k][threadIdx.x] = s[i * J + t];
@@ -303,7 +305,7 @@ __global__ void k_bt_to_ij(const T* __restrict__ src, T* __restrict__ dst, int64
   __syncthreads();
   for (int k = threadIdx.y; k < 32; k += blockDim.y) {
     const int64_t i = i0 + threadIdx.x, t = t0 + k;
-    if (i < I && t < J) d[i + t * I] = tile[threadIdx.x][k];
+    if (i < I && t < J) d[i + t * ld] = tile[threadIdx.x][k];
   }
 }
 

@@ -48,24 +48,24 @@ cudaError_t launch_sum_partials(cudaStream_t s, const double* partial, int64_t n
 }
 
 template <class T, bool TO_BT>
-static cudaError_t transpose(cudaStream_t s, const T* src, T* dst, int64_t B, int64_t I, int64_t J) {
+static cudaError_t transpose(cudaStream_t s, const T* src, T* dst, int64_t B, int64_t I, int64_t J, int64_t ld) {
   if (B * I * J == 0) return cudaSuccess;
   dim3 grid((I + 31) / 32, (J + 31) / 32, B), block(32, 8);
   if (TO_BT)
-    k_ij_to_bt<T><<<grid, block, 0, s>>>(src, dst, I, J);
+    k_ij_to_bt<T><<<grid, block, 0, s>>>(src, dst, I, J, ld > 0 ? ld : I);
   else
-    k_bt_to_ij<T><<<grid, block, 0, s>>>(src, dst, I, J);
+    k_bt_to_ij<T><<<grid, block, 0, s>>>(src, dst, I, J, ld > 0 ? ld : I);
   return cudaGetLastError();
 }
 
-cudaError_t launch_to_bt(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J) {
-  return transpose<double, true>(s, src, dst, B, I, J);
+cudaError_t launch_to_bt(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J, int64_t ld) {
+  return transpose<double, true>(s, src, dst, B, I, J, ld);
 }
-cudaError_t launch_to_ij(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J) {
-  return transpose<double, false>(s, src, dst, B, I, J);
+cudaError_t launch_to_ij(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J, int64_t ld) {
+  return transpose<double, false>(s, src, dst, B, I, J, ld);
 }
 cudaError_t launch_to_ij_c(cudaStream_t s, const double2* src, double2* dst, int64_t B, int64_t I, int64_t J) {
-  return transpose<double2, false>(s, src, dst, B, I, J);
+  return transpose<double2, false>(s, src, dst, B, I, J, I);
 }
 
 cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out) {

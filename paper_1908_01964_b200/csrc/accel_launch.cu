@@ -10,7 +10,9 @@ AccelCfg choose_accel_cfg(int64_t J) {
   const char* e_spt = std::getenv("RCSCM_ACCEL_SPT");
   const char* e_cl = std::getenv("RCSCM_ACCEL_CL");
   const char* e_sm = std::getenv("RCSCM_ACCEL_SMEM");
-  const bool smem = e_sm ? std::atoi(e_sm) != 0 : false;
+  // -1: per-configuration default (shared-memory constants for clusters, where
+  // the cluster barrier needs more resident CTAs to hide; measured on B200)
+  const int smem_env = e_sm ? std::atoi(e_sm) : -1;
   const char* e_lb = std::getenv("RCSCM_ACCEL_LB3");
   const bool lb3 = e_lb ? std::atoi(e_lb) != 0 : true;  // measured faster (B200, configs 0/1/3)
   const int force_spt = e_spt ? std::atoi(e_spt) : 0;
@@ -33,6 +35,7 @@ AccelCfg choose_accel_cfg(int64_t J) {
         best_waste = waste;
         // FULL needs every CTA of the cluster to own exactly nt * spt frames
         const bool full = (waste == 0) && (jc * cl == J);
+        const bool smem = smem_env >= 0 ? smem_env != 0 : cl > 1;
         best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem, lb3};
       }
     }

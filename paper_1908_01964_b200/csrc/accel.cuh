@@ -115,8 +115,10 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   namespace cg = cooperative_groups;
   constexpr int kMaxWarps = 256 / 32;
   __shared__ __align__(16) double red[2][kMaxWarps];  // zero-padded warp partials
-  __shared__ double cl_part[2];
-  __shared__ double cl_total[2];
+  // cluster exchange: cl_vals[buf][r] receives rank r's CTA partial, cl_bar[buf]
+  // counts the CL arrivals (double-buffered by iteration parity)
+  __shared__ __align__(16) double cl_vals[2][16];
+  __shared__ __align__(8) unsigned long long cl_bar[2];
   extern __shared__ double2 dyn[];
   const int NT = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -174,7 +176,16 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   }
 
   if (tid < 2 * kMaxWarps) (&red[0][0])[tid] = 0.0;
-  __syncthreads();
+  if constexpr (CL > 1) {
+    if (tid < 2) {
+      const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[tid]));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(lb), "r"(CL) : "memory");
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    cg::this_cluster().sync();  // every peer's barriers exist before the first remote arrive
+  } else {
+    __syncthreads();
+  }
   const double invJ = 1.0 / static_cast<double>(J);
   const double m2M = -2.0 * inv_M;
   const double taaM = taa * inv_M, s2M = s2 * inv_M;
@@ -244,26 +255,45 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     if constexpr (CL == 1) {
       total = block_total8(red[buf]);
     } else {
-      // CTA partial -> cluster: warp 0 gathers the CL partials over DSMEM in
-      // rank order and every CTA forms the same total.
-      cg::cluster_group cluster = cg::this_cluster();
-      if (warp == 0) {
-        const double c = block_total8(red[buf]);
-        if (lane == 0) cl_part[buf] = c;
+      // CTA partial -> cluster: lanes r < CL of warp 0 store this CTA's partial
+      // into cl_vals[buf][rank] of CTA r (st.shared::cluster) and arrive on its
+      // cl_bar[buf] with release semantics; every thread then waits on the local
+      // barrier (acquire) and sums the CL partials in rank order -- the same
+      // fixed tree in every CTA. One DSMEM write latency instead of a
+      // cluster-wide barrier plus a remote read.
+      const double c = block_total8(red[buf]);
+      if (warp == 0 && lane < CL) {
+        const unsigned lv = static_cast<unsigned>(__cvta_generic_to_shared(&cl_vals[buf][rank]));
+        const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
+        unsigned rv, rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rv) : "r"(lv), "r"(lane));
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(lane));
+        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rv), "d"(c) : "memory");
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
       }
-      cluster.sync();
-      if (warp == 0) {
-        double v = lane < CL ? *cluster.map_shared_rank(&cl_part[buf], lane) : 0.0;
-        // fixed-order pairwise tree over ranks 0..CL-1 (same on every CTA)
-#pragma unroll
-        for (int off = 1; off < CL; off <<= 1) {
-          const double o = __shfl_down_sync(0xffffffffu, v, off);
-          if ((lane & (2 * off - 1)) == 0) v += o;
+      {
+        const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
+        const unsigned parity = static_cast<unsigned>((it >> 1) & 1);
+        unsigned done = 0;
+        while (!done) {
+          asm volatile(
+              "{\n .reg .pred p;\n"
+              " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+              " selp.u32 %0, 1, 0, p;\n}"
+              : "=r"(done)
+              : "r"(lb), "r"(parity)
+              : "memory");
         }
-        if (lane == 0) cl_total[buf] = v;
       }
-      __syncthreads();
-      total = cl_total[buf];
+      double v[CL];
+#pragma unroll
+      for (int r = 0; r < CL; ++r) v[r] = cl_vals[buf][r];
+#pragma unroll
+      for (int w = 1; w < CL; w <<= 1) {
+#pragma unroll
+        for (int r = 0; r + w < CL; r += 2 * w) v[r] += v[r + w];
+      }
+      total = v[0];
     }
     // (3) the short tail that needs lambda_new
     lam = floor_eps(total * invJ, P.eps);
@@ -305,7 +335,7 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   }
   if (rank == 0 && tid == 0) P.lambda[bin] = lam;
   if constexpr (CL > 1) {
-    // No CTA may leave while a peer can still read its cl_part via DSMEM.
+    // No CTA leaves while a peer may still be writing into its shared memory.
     cooperative_groups::this_cluster().sync();
   }
 }

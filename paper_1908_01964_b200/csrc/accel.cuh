@@ -94,6 +94,13 @@ __device__ __forceinline__ double warp_total_mma(double v, int lane) {
   return dmma_ones(lo) + dmma_ones(hi);
 }
 
+// Sum of the (zero-padded) first 4 per-warp partials (CTAs of <= 128 threads).
+__device__ __forceinline__ double block_total4(const double* red) {
+  const double2* r = reinterpret_cast<const double2*>(red);
+  const double2 a = r[0], b = r[1];
+  return (a.x + a.y) + (b.x + b.y);
+}
+
 // Sum of the (zero-padded) 8 per-warp partials: four broadcast LDS.128 and a
 // fixed 3-level tree, identical in every thread.
 __device__ __forceinline__ double block_total8(const double* red) {
@@ -110,7 +117,10 @@ __device__ __forceinline__ double block_total8(const double* red) {
 // halves the register footprint and doubles the resident warps per SM.
 // LB3: launch bounds of 128 threads x 3 CTAs/SM (<= 170 registers) instead of
 // one 256-thread CTA's worth, trading a little ILP for resident warps.
-template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false>
+// DIRECT: form r_u after the reduction from rho with the new lambda (8 FP64 ops
+// per slot, the reference's own order) instead of the affine P0 + P1/lambda
+// split (10 ops, but all but 3 of them overlap the reduction).
+template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false>
 __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
   constexpr int kMaxWarps = 256 / 32;
@@ -228,6 +238,14 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     double p0[SPT], p1[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
+      if constexpr (DIRECT) {
+        const double q = fma(g[k], cnorm(rax[k]), ru[k]);
+        const double gq = g[k] * q;
+        rh[k] = floor_eps(fma(gq, P.k1, P.k2), P.eps);
+        p0[k] = gq;             // gamma q
+        p1[k] = g[k] * m2M;     // -2 gamma / M
+        continue;
+      }
       double2 tk, ck;
       double xk, dk;
       if constexpr (SMEMC) {
@@ -253,7 +271,7 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     __syncthreads();
     double total = 0.0;
     if constexpr (CL == 1) {
-      total = block_total8(red[buf]);
+      total = NT <= 128 ? block_total4(red[buf]) : block_total8(red[buf]);
     } else {
       // CTA partial -> cluster: lanes r < CL of warp 0 store this CTA's partial
       // into cl_vals[buf][rank] of CTA r (st.shared::cluster) and arrive on its
@@ -299,18 +317,36 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     lam = floor_eps(total * invJ, P.eps);
     il = rcp_pos(lam);
     raa = fma(s2, il, taa);
+    const double raaM = raa * inv_M;
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       double2 tk, ck;
+      double xk = 0.0, dk = 0.0;
       if constexpr (SMEMC) {
         tk = s_tax[k * NT + tid];
         ck = s_cc[k * NT + tid];
+        if constexpr (DIRECT) {
+          xk = s_txx[k * NT + tid];
+          dk = s_dd[k * NT + tid];
+        }
       } else {
         tk = tax[k];
         ck = cc[k];
+        if constexpr (DIRECT) {
+          xk = txx[k];
+          dk = dd[k];
+        }
       }
-      ru[k] = floor_eps(fma(p1[k], il, p0[k]), P.eps);
-      rax[k] = make_double2(fma(ck.x, il, tk.x), fma(ck.y, il, tk.y));  // rho_ax with lambda_new
+      const double2 nax = make_double2(fma(ck.x, il, tk.x), fma(ck.y, il, tk.y));  // rho_ax, lambda_new
+      if constexpr (DIRECT) {
+        // solver_accel.hpp:167-173 with rho_xx / M = tau_xx/M + |s_bx|^2/M / lambda
+        const double rxx = fma(dk, il, xk);
+        const double re = fma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
+        ru[k] = floor_eps(fma(p1[k], re, fma(p0[k], raaM, rxx)), P.eps);
+      } else {
+        ru[k] = floor_eps(fma(p1[k], il, p0[k]), P.eps);
+      }
+      rax[k] = nax;
     }
     if constexpr (TRAJ) {
 #pragma unroll

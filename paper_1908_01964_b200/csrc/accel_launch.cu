@@ -6,7 +6,9 @@
 namespace rcscm {
 
 AccelCfg choose_accel_cfg(int64_t J) {
-  AccelCfg best{0, 0, 0, false, false, false};
+  AccelCfg best{0, 0, 0, false, false, false, false};
+  const char* e_dir = std::getenv("RCSCM_ACCEL_DIRECT");
+  const bool direct = e_dir ? std::atoi(e_dir) != 0 : false;
   const char* e_spt = std::getenv("RCSCM_ACCEL_SPT");
   const char* e_cl = std::getenv("RCSCM_ACCEL_CL");
   const char* e_sm = std::getenv("RCSCM_ACCEL_SMEM");
@@ -36,7 +38,7 @@ AccelCfg choose_accel_cfg(int64_t J) {
         // FULL needs every CTA of the cluster to own exactly nt * spt frames
         const bool full = (waste == 0) && (jc * cl == J);
         const bool smem = smem_env >= 0 ? smem_env != 0 : cl > 1;
-        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem, lb3};
+        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem, lb3, direct};
       }
     }
     if (best.cl) return best;

@@ -6,9 +6,9 @@
 
 namespace rcscm {
 
-template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false>
+template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false>
 cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
-  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, LB3>;
+  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);
@@ -36,16 +36,16 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
   return cudaLaunchKernelEx(&cfg, kern, A);
 }
 
-template <int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false>
+template <int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false>
 cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt) {
   switch (spt) {
-    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, LB3>(s, A, nt);
-    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, LB3>(s, A, nt);
-    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, LB3>(s, A, nt);
-    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, LB3>(s, A, nt);
-    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, LB3>(s, A, nt);
-    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, LB3>(s, A, nt);
-    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, LB3>(s, A, nt);
+    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
+    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
+    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
+    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
+    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
+    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
+    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -59,7 +59,10 @@ cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& 
     return launch_accel_spt<CL, false, false, true>(s, A, g.nt, g.spt);
   }
   if constexpr (CL == 1) {
-    if (g.full && g.lb3 && g.nt <= 128) return launch_accel_spt<CL, true, false, false, true>(s, A, g.nt, g.spt);
+    if (g.full && g.lb3 && g.nt <= 128) {
+      if (g.direct) return launch_accel_spt<CL, true, false, false, true, true>(s, A, g.nt, g.spt);
+      return launch_accel_spt<CL, true, false, false, true>(s, A, g.nt, g.spt);
+    }
   }
   if (g.full) return launch_accel_spt<CL, true, false, false>(s, A, g.nt, g.spt);
   return launch_accel_spt<CL, false, false, false>(s, A, g.nt, g.spt);

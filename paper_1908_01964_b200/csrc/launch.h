@@ -30,6 +30,7 @@ struct AccelCfg {
   bool full;  // nt * spt == chunk: no per-slot masks
   bool smem;  // phase-B constants in shared memory (k_accel SMEMC)
   bool lb3;   // 128-thread x 3-CTA launch bounds (k_accel LB3), CL == 1 and nt <= 128 only
+  bool direct;  // r_u from rho(lambda_new) after the reduction (k_accel DIRECT), LB3 path only
 };
 // Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL /
 // RCSCM_ACCEL_SMEM force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.

@@ -59,6 +59,12 @@ struct AccelArgs {
   double* traj_r_h;         // optional [it][bin][t]
   double* traj_r_u;
   double* traj_lambda;      // optional [it][bin]
+  // complex64 (FP32) mode: the per-slot arrays in single precision
+  const float2* sigma_bx_f;
+  const float2* tau_ax_f;
+  const float* tau_xx_f;
+  float* r_h_f;
+  float* r_u_f;
 };
 
 // std::max(v, eps) of the reference (returns v unless v < eps) for eps > 0,
@@ -109,6 +115,14 @@ __device__ __forceinline__ double block_total8(const double* red) {
   return ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (d.x + d.y));
 }
 
+// FP32-mode counterpart of floor_eps (32-bit compare of the bit patterns).
+__device__ __forceinline__ float floor_eps(float v, float eps) {
+  const int iv = __float_as_int(v), ie = __float_as_int(eps);
+  return __int_as_float(iv < ie ? ie : iv);
+}
+__device__ __forceinline__ double tfma(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float tfma(float a, float b, float c) { return fmaf(a, b, c); }
+
 // FULL: every thread's SPT slots are inside the bin chunk (NT * SPT == chunk),
 // so no per-slot masks. TRAJ: record r_h / r_u / lambda after every iteration.
 // SMEMC: the four per-slot constants used only after the lambda reduction
@@ -120,16 +134,22 @@ __device__ __forceinline__ double block_total8(const double* red) {
 // DIRECT: form r_u after the reduction from rho with the new lambda (8 FP64 ops
 // per slot, the reference's own order) instead of the affine P0 + P1/lambda
 // split (10 ops, but all but 3 of them overlap the reduction).
-template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false>
+// T: the per-slot arithmetic type -- double (complex128, reference-exact) or
+// float (the complex64 / FP32 mode); lambda, its reduction and the per-bin
+// scalars stay in double in both.
+template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false,
+          typename T = double>
 __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
+  using CT = typename CplxOf<T>::type;
+  constexpr bool F32 = sizeof(T) == 4;
   constexpr int kMaxWarps = 256 / 32;
   __shared__ __align__(16) double red[2][kMaxWarps];  // zero-padded warp partials
   // cluster exchange: cl_vals[buf][r] receives rank r's CTA partial, cl_bar[buf]
   // counts the CL arrivals (double-buffered by iteration parity)
   __shared__ __align__(16) double cl_vals[2][16];
   __shared__ __align__(8) unsigned long long cl_bar[2];
-  extern __shared__ double2 dyn[];
+  extern __shared__ __align__(16) unsigned char dyn_raw[];
   const int NT = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bin = blockIdx.x / CL;
@@ -140,11 +160,11 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   const int64_t t_end = min(J, t0 + Jc);
   const int64_t base = bin * J;
   const double inv_M = P.inv_M;
-  // shared planes (SMEMC): tax[k][tid], cc[k][tid] (double2), txx[k][tid], dd[k][tid] (double)
-  double2* s_tax = dyn;
-  double2* s_cc = dyn + SPT * NT;
-  double* s_txx = reinterpret_cast<double*>(dyn + 2 * SPT * NT);
-  double* s_dd = s_txx + SPT * NT;
+  // shared planes (SMEMC): tax[k][tid], cc[k][tid] (complex), txx[k][tid], dd[k][tid] (real)
+  CT* s_tax = reinterpret_cast<CT*>(dyn_raw);
+  CT* s_cc = s_tax + SPT * NT;
+  T* s_txx = reinterpret_cast<T*>(s_cc + SPT * NT);
+  T* s_dd = s_txx + SPT * NT;
 
   const double2 sab = P.sigma_ab[bin];
   const double s2 = cnorm(sab);  // |sigma_ab|^2
@@ -152,26 +172,41 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   double lam = P.lambda[bin];
   double il = 1.0 / lam;
   double raa = fma(s2, il, taa);  // rho_aa (solver_accel.hpp:122)
+  const CT sabT = to_c(sab, T());
+  const T s2T = static_cast<T>(s2);
+  T ilT = static_cast<T>(il);
 
   // per-slot state: rh, ru evolve; rax = rho~_ax carried; the rest is constant.
   // txx and dd are pre-scaled by 1/M (exact for M = 2, 4, 8, 16).
   constexpr int SR = SMEMC ? 1 : SPT;  // register copies of the constants
-  double rh[SPT], ru[SPT], txx[SR], dd[SR];
-  double2 rax[SPT], tax[SR], cc[SR], sbx[SPT];
+  T rh[SPT], ru[SPT], txx[SR], dd[SR];
+  CT rax[SPT], tax[SR], cc[SR], sbx[SPT];
   bool valid[SPT];
+  const T invMT = static_cast<T>(inv_M);
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
     const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
     valid[k] = FULL || t < t_end;
     const int64_t s = base + (valid[k] ? t : t0);
-    rh[k] = P.r_h[s];
-    ru[k] = P.r_u[s];
-    sbx[k] = P.sigma_bx[s];
-    const double2 tk = P.tau_ax[s];
-    const double xk = P.tau_xx[s] * inv_M;
-    const double2 ck = cmul(sab, sbx[k]);   // sigma_ab * sigma_bx
-    const double dk = cnorm(sbx[k]) * inv_M;  // |sigma_bx|^2 / M
-    rax[k] = make_double2(fma(ck.x, il, tk.x), fma(ck.y, il, tk.y));
+    CT tk;
+    T xk;
+    if constexpr (F32) {
+      rh[k] = P.r_h_f[s];
+      ru[k] = P.r_u_f[s];
+      sbx[k] = P.sigma_bx_f[s];
+      tk = P.tau_ax_f[s];
+      xk = P.tau_xx_f[s] * invMT;
+    } else {
+      rh[k] = P.r_h[s];
+      ru[k] = P.r_u[s];
+      sbx[k] = P.sigma_bx[s];
+      tk = P.tau_ax[s];
+      xk = P.tau_xx[s] * invMT;
+    }
+    const CT ck = cmul(sabT, sbx[k]);     // sigma_ab * sigma_bx
+    const T dk = cnorm(sbx[k]) * invMT;   // |sigma_bx|^2 / M
+    rax[k].x = tfma(ck.x, ilT, tk.x);
+    rax[k].y = tfma(ck.y, ilT, tk.y);
     if constexpr (SMEMC) {
       s_tax[k * NT + tid] = tk;
       s_cc[k * NT + tid] = ck;
@@ -197,57 +232,60 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     __syncthreads();
   }
   const double invJ = 1.0 / static_cast<double>(J);
-  const double m2M = -2.0 * inv_M;
-  const double taaM = taa * inv_M, s2M = s2 * inv_M;
-  const double fault = P.gamma_fault;
+  const T m2M = static_cast<T>(-2.0 * inv_M);
+  const T taaM = static_cast<T>(taa * inv_M), s2M = static_cast<T>(s2 * inv_M);
+  const T fault = static_cast<T>(P.gamma_fault);
+  const T k1 = static_cast<T>(P.k1), k2 = static_cast<T>(P.k2), epsT = static_cast<T>(P.eps);
   for (int it = 0; it < P.iters; ++it) {
     const int buf = it & 1;
+    const T raaT = static_cast<T>(raa);
     // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
     //     (solver_accel.hpp:67-76, :143-158).
-    double g[SPT], term[SPT];
+    T g[SPT], term[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      const double D = fma(rh[k], raa, ru[k]);  // r~_u + r~_h rho~_aa
-      const double inv = rcp_pos(D * ru[k]);
-      const double gk = fma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
-      const double iru = D * inv;                         // 1 / r~_u
+      const T D = tfma(rh[k], raaT, ru[k]);  // r~_u + r~_h rho~_aa
+      const T inv = rcp_pos(D * ru[k]);
+      const T gk = tfma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
+      const T iru = D * inv;                          // 1 / r~_u
       // resid = s_bx - gamma conj(s_ab) rho~_ax
-      const double2 e = cmulc(sab, rax[k]);
-      const double rx = fma(-gk, e.x, sbx[k].x);
-      const double ry = fma(-gk, e.y, sbx[k].y);
-      const double rr = fma(rx, rx, ry * ry);
+      const CT e = cmulc(sabT, rax[k]);
+      const T rx = tfma(-gk, e.x, sbx[k].x);
+      const T ry = tfma(-gk, e.y, sbx[k].y);
+      const T rr = tfma(rx, rx, ry * ry);
       // per-slot lambda term, independent across slots (no serial accumulator)
-      term[k] = (FULL || valid[k]) ? fma(gk, s2, rr * iru) : 0.0;
+      term[k] = (FULL || valid[k]) ? tfma(gk, s2T, rr * iru) : T(0);
       g[k] = gk;
     }
-    // fixed pairwise tree over the thread's slots, then the warp butterfly
+    // fixed pairwise tree over the thread's slots, then the warp total (FP64)
 #pragma unroll
     for (int w = 1; w < SPT; w <<= 1) {
 #pragma unroll
       for (int k = 0; k + w < SPT; k += 2 * w) term[k] += term[k + w];
     }
-    const double part = warp_total_mma(term[0], lane);
+    const double part = warp_total_mma(static_cast<double>(term[0]), lane);
     if (lane == 0) red[buf][warp] = part;
     // (2) everything that does not need the new lambda, overlapping the
-    //     reduction: r_h (solver_accel.hpp:134-141) and the two halves of the
-    //     r_u update, which is affine in 1/lambda_new (:160-176 with :121-127):
+    //     reduction: r_h (solver_accel.hpp:134-141) and (non-DIRECT) the two
+    //     halves of the r_u update, which is affine in 1/lambda_new
+    //     (:160-176 with :121-127):
     //       M r_u = P0 + P1 / lambda_new,
     //       P0 = g q tau_aa + tau_xx - 2 g Re(rho~_ax conj tau_ax)
     //       P1 = g q |s_ab|^2 + |s_bx|^2 - 2 g Re(rho~_ax conj(s_ab s_bx))
     //     (stored pre-scaled by 1/M; q = r~_u + g |rho~_ax|^2).
-    double p0[SPT], p1[SPT];
+    T p0[SPT], p1[SPT];
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       if constexpr (DIRECT) {
-        const double q = fma(g[k], cnorm(rax[k]), ru[k]);
-        const double gq = g[k] * q;
-        rh[k] = floor_eps(fma(gq, P.k1, P.k2), P.eps);
-        p0[k] = gq;             // gamma q
-        p1[k] = g[k] * m2M;     // -2 gamma / M
+        const T q = tfma(g[k], cnorm(rax[k]), ru[k]);
+        const T gq = g[k] * q;
+        rh[k] = floor_eps(tfma(gq, k1, k2), epsT);
+        p0[k] = gq;          // gamma q
+        p1[k] = g[k] * m2M;  // -2 gamma / M
         continue;
       }
-      double2 tk, ck;
-      double xk, dk;
+      CT tk, ck;
+      T xk, dk;
       if constexpr (SMEMC) {
         tk = s_tax[k * NT + tid];
         ck = s_cc[k * NT + tid];
@@ -259,14 +297,14 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
         xk = txx[k];
         dk = dd[k];
       }
-      const double q = fma(g[k], cnorm(rax[k]), ru[k]);
-      const double gq = g[k] * q;
-      rh[k] = floor_eps(fma(gq, P.k1, P.k2), P.eps);
-      const double m2g = g[k] * m2M;                              // -2 gamma / M
-      const double re0 = fma(rax[k].x, tk.x, rax[k].y * tk.y);    // Re(rho~_ax conj tau_ax)
-      const double re1 = fma(rax[k].x, ck.x, rax[k].y * ck.y);    // Re(rho~_ax conj(s_ab s_bx))
-      p0[k] = fma(m2g, re0, fma(gq, taaM, xk));
-      p1[k] = fma(m2g, re1, fma(gq, s2M, dk));
+      const T q = tfma(g[k], cnorm(rax[k]), ru[k]);
+      const T gq = g[k] * q;
+      rh[k] = floor_eps(tfma(gq, k1, k2), epsT);
+      const T m2g = g[k] * m2M;                                 // -2 gamma / M
+      const T re0 = tfma(rax[k].x, tk.x, rax[k].y * tk.y);      // Re(rho~_ax conj tau_ax)
+      const T re1 = tfma(rax[k].x, ck.x, rax[k].y * ck.y);      // Re(rho~_ax conj(s_ab s_bx))
+      p0[k] = tfma(m2g, re0, tfma(gq, taaM, xk));
+      p1[k] = tfma(m2g, re1, tfma(gq, s2M, dk));
     }
     __syncthreads();
     double total = 0.0;
@@ -317,11 +355,12 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     lam = floor_eps(total * invJ, P.eps);
     il = rcp_pos(lam);
     raa = fma(s2, il, taa);
-    const double raaM = raa * inv_M;
+    ilT = static_cast<T>(il);
+    const T raaM = static_cast<T>(raa * inv_M);
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      double2 tk, ck;
-      double xk = 0.0, dk = 0.0;
+      CT tk, ck;
+      T xk = T(0), dk = T(0);
       if constexpr (SMEMC) {
         tk = s_tax[k * NT + tid];
         ck = s_cc[k * NT + tid];
@@ -337,14 +376,16 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
           dk = dd[k];
         }
       }
-      const double2 nax = make_double2(fma(ck.x, il, tk.x), fma(ck.y, il, tk.y));  // rho_ax, lambda_new
+      CT nax;  // rho_ax with lambda_new
+      nax.x = tfma(ck.x, ilT, tk.x);
+      nax.y = tfma(ck.y, ilT, tk.y);
       if constexpr (DIRECT) {
         // solver_accel.hpp:167-173 with rho_xx / M = tau_xx/M + |s_bx|^2/M / lambda
-        const double rxx = fma(dk, il, xk);
-        const double re = fma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
-        ru[k] = floor_eps(fma(p1[k], re, fma(p0[k], raaM, rxx)), P.eps);
+        const T rxx = tfma(dk, ilT, xk);
+        const T re = tfma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
+        ru[k] = floor_eps(tfma(p1[k], re, tfma(p0[k], raaM, rxx)), epsT);
       } else {
-        ru[k] = floor_eps(fma(p1[k], il, p0[k]), P.eps);
+        ru[k] = floor_eps(tfma(p1[k], ilT, p0[k]), epsT);
       }
       rax[k] = nax;
     }
@@ -365,8 +406,13 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   for (int k = 0; k < SPT; ++k) {
     if (valid[k]) {
       const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
-      P.r_h[base + t] = rh[k];
-      P.r_u[base + t] = ru[k];
+      if constexpr (F32) {
+        P.r_h_f[base + t] = rh[k];
+        P.r_u_f[base + t] = ru[k];
+      } else {
+        P.r_h[base + t] = rh[k];
+        P.r_u[base + t] = ru[k];
+      }
     }
   }
   if (rank == 0 && tid == 0) P.lambda[bin] = lam;

@@ -5,8 +5,8 @@
 
 namespace rcscm {
 
-AccelCfg choose_accel_cfg(int64_t J) {
-  AccelCfg best{0, 0, 0, false, false, false, false};
+AccelCfg choose_accel_cfg(int64_t J, bool f32) {
+  AccelCfg best{0, 0, 0, false, false, false, false, f32};
   const char* e_dir = std::getenv("RCSCM_ACCEL_DIRECT");
   const bool direct = e_dir ? std::atoi(e_dir) != 0 : true;  // measured faster (B200)
   const char* e_spt = std::getenv("RCSCM_ACCEL_SPT");
@@ -22,7 +22,7 @@ AccelCfg choose_accel_cfg(int64_t J) {
   for (int cl : {1, 2, 4, 8, 16}) {
     if (force_cl && cl != force_cl) continue;
     const int64_t jc = (J + cl - 1) / cl;
-    const int max_spt = (cl == 16) ? 8 : 6;
+    const int max_spt = (cl == 16 || f32) ? 8 : 6;  // FP32 state takes half the registers
     if (jc > 256LL * (force_spt ? force_spt : max_spt)) continue;
     int64_t best_waste = -1;
     for (int spt = 1; spt <= 8; ++spt) {
@@ -38,7 +38,7 @@ AccelCfg choose_accel_cfg(int64_t J) {
         // FULL needs every CTA of the cluster to own exactly nt * spt frames
         const bool full = (waste == 0) && (jc * cl == J);
         const bool smem = smem_env >= 0 ? smem_env != 0 : cl > 1;
-        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem, lb3, direct};
+        best = AccelCfg{cl, static_cast<int>(nt), spt, full, f32 ? false : smem, lb3, direct, f32};
       }
     }
     if (best.cl) return best;

@@ -6,13 +6,14 @@
 
 namespace rcscm {
 
-template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false>
+template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false,
+          typename T = double>
 cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
-  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>;
+  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);
-  cfg.dynamicSmemBytes = SMEMC ? static_cast<size_t>(SPT) * nt * 48 : 0;
+  cfg.dynamicSmemBytes = SMEMC ? static_cast<size_t>(SPT) * nt * 6 * sizeof(T) : 0;
   if (SMEMC) {  // opt in to the full dynamic allowance (static + dynamic may pass 48 KB)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(cfg.dynamicSmemBytes));
@@ -36,16 +37,16 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
   return cudaLaunchKernelEx(&cfg, kern, A);
 }
 
-template <int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false>
+template <int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false, typename T = double>
 cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt) {
   switch (spt) {
-    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
-    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
-    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
-    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
-    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
-    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
-    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, LB3, DIRECT>(s, A, nt);
+    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
+    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
+    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
+    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
+    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
+    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
+    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -53,6 +54,13 @@ cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt
 template <int CL>
 cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
   const bool traj = A.traj_r_h != nullptr;
+  if (g.f32) {  // complex64 mode: direct form, registers only
+    if constexpr (CL == 1) {
+      if (g.full && g.nt <= 128) return launch_accel_spt<CL, true, false, false, true, true, float>(s, A, g.nt, g.spt);
+    }
+    if (g.full) return launch_accel_spt<CL, true, false, false, false, true, float>(s, A, g.nt, g.spt);
+    return launch_accel_spt<CL, false, false, false, false, true, float>(s, A, g.nt, g.spt);
+  }
   if (traj) return launch_accel_spt<CL, false, true, false>(s, A, g.nt, g.spt);
   if (g.smem) {
     if (g.full) return launch_accel_spt<CL, true, false, true>(s, A, g.nt, g.spt);

@@ -84,6 +84,9 @@ struct rcscm_gpu_ctx {
   // device buffers
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
+  // complex64 (FP32) mode copies of the slot arrays
+  DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef;
+  bool f32_params_current = false;  // session: FP32 r_h / r_u hold the latest iterate
   // session geometry
   bool s_loaded = false, s_setup = false, s_pre = false;
   int64_t sB = 0, sI = 0, sJ = 0;
@@ -227,6 +230,38 @@ void alloc_problem(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M) {
   c->err.get<unsigned long long>(1);
 }
 
+bool f32(const rcscm_gpu_ctx* c) { return c->precision == RCSCM_C64; }
+
+// complex64 mode: single-precision copies of x and of the parameters
+void alloc_f32(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M) {
+  const size_t S = static_cast<size_t>(nb * J);
+  c->Xf.get<float2>(S * M);
+  c->sbxf.get<float2>(S);
+  c->taxf.get<float2>(S);
+  c->txxf.get<float>(S);
+  c->rhf.get<float>(S);
+  c->ruf.get<float>(S);
+}
+void x_to_f32(rcscm_gpu_ctx* c, size_t S, int M) {
+  c->launched(launch_d2f(c->stream, c->X.as<double>(), c->Xf.as<float>(), static_cast<int64_t>(2 * S * M)));
+}
+void params_to_f32(rcscm_gpu_ctx* c, size_t S, const double* rh, const double* ru) {
+  c->launched(launch_d2f(c->stream, rh, c->rhf.as<float>(), static_cast<int64_t>(S)));
+  c->launched(launch_d2f(c->stream, ru, c->ruf.as<float>(), static_cast<int64_t>(S)));
+}
+void params_from_f32(rcscm_gpu_ctx* c, size_t S) {
+  c->launched(launch_f2d(c->stream, c->rhf.as<float>(), c->rh.as<double>(), static_cast<int64_t>(S)));
+  c->launched(launch_f2d(c->stream, c->ruf.as<float>(), c->ru.as<double>(), static_cast<int64_t>(S)));
+}
+// sigma / tau precompute in the context's precision
+void precompute(rcscm_gpu_ctx* c, const DevProblem& P, double eps) {
+  if (f32(c))
+    c->launched(launch_slots_pre_f32(c->stream, P, c->Xf.as<float2>(), c->sbxf.as<float2>(), c->taxf.as<float2>(),
+                                     c->txxf.as<float>()));
+  else
+    c->launched(launch_slots(c->stream, P, false, true, eps));
+}
+
 AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, const rcscm_hyper& h, double eps,
                      double gamma_fault) {
   AccelArgs A{};
@@ -246,12 +281,17 @@ AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, 
   A.r_h = c->rh.as<double>();
   A.r_u = c->ru.as<double>();
   A.lambda = c->lam.as<double>();
+  A.sigma_bx_f = c->sbxf.as<float2>();
+  A.tau_ax_f = c->taxf.as<float2>();
+  A.tau_xx_f = c->txxf.as<float>();
+  A.r_h_f = c->rhf.as<float>();
+  A.r_u_f = c->ruf.as<float>();
   return A;
 }
 
 void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A) {
   if (A.nb * A.J == 0) return;
-  const AccelCfg g = choose_accel_cfg(A.J);
+  const AccelCfg g = choose_accel_cfg(A.J, f32(c));
   if (!g.cl)
     fail(RCSCM_UNSUPPORTED,
          "frames = " + std::to_string(A.J) + " exceeds the on-chip accel kernel capacity (16 x 2048)");
@@ -506,7 +546,9 @@ void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcsc
   }
   if (I == 0) return;
   const bool traj = extra && opt->record_trajectory && (extra->traj_r_h || extra->traj_r_u || extra->traj_lambda);
-  if (accel && !opt->compute_objective && !traj) {
+  const bool fp = accel && f32(c);  // complex64 (FP32) accelerated solve
+  if (fp && traj) fail(RCSCM_UNSUPPORTED, "record_trajectory is not supported in the complex64 mode");
+  if (accel && !fp && !opt->compute_objective && !traj) {
     std::vector<double> secs;
     if (run_accel_pipelined(c, in, p0, hyper, X, opt, out, &secs)) {
       if (extra) {
@@ -518,8 +560,17 @@ void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcsc
   }
   upload_model(c, in, p0, X, !accel || opt->compute_objective, accel);
   reset_err(c);
-  if (accel) c->launched(launch_slots(c->stream, problem(c, 1, I, J, M), false, true, opt->eps_var));
   const size_t S = static_cast<size_t>(I * J);
+  if (fp) {
+    alloc_f32(c, I, J, M);
+    x_to_f32(c, S, M);
+    params_to_f32(c, S, c->rh.as<double>(), c->ru.as<double>());
+    precompute(c, problem(c, 1, I, J, M), opt->eps_var);
+    // the objective is evaluated in double from the double sigma / tau
+    if (opt->compute_objective) c->launched(launch_slots(c->stream, problem(c, 1, I, J, M), false, true, opt->eps_var));
+  } else if (accel) {
+    c->launched(launch_slots(c->stream, problem(c, 1, I, J, M), false, true, opt->eps_var));
+  }
   double* trh = traj ? c->traj_rh.get<double>(S * std::max(iters, 1)) : nullptr;
   double* tru = traj ? c->traj_ru.get<double>(S * std::max(iters, 1)) : nullptr;
   double* trl = traj ? c->traj_lam.get<double>(I * std::max(iters, 1)) : nullptr;
@@ -558,7 +609,10 @@ void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcsc
     // accel: the O(1)-per-slot objective (scalar expansion, needs log pdet R');
     // naive: the per-slot Cholesky form of model.hpp:129-157.
     if (accel) c->launched(launch_logpdet(c->stream, problem(c, 1, I, J, M)));
-    auto eval = [&] { return accel ? objective_fast(c, I, J, M, *hyper) : objective(c, I, J, M, *hyper); };
+    auto eval = [&] {
+      if (fp) params_from_f32(c, S);
+      return accel ? objective_fast(c, I, J, M, *hyper) : objective(c, I, J, M, *hyper);
+    };
     objv.push_back(eval());
     for (int it = 0; it < iters; ++it) {
       CK(cudaEventRecord(c->ev0, c->stream));
@@ -573,6 +627,7 @@ void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcsc
       if (opt->rel_obj_tol > 0.0 && std::abs(cur - prev) <= opt->rel_obj_tol * std::abs(prev)) break;
     }
   }
+  if (fp) params_from_f32(c, S);
   download_params(c, I, J, out);
   if (traj && iters_run > 0) {
     double* th = c->tmp.get<double>(S * iters_run);
@@ -604,6 +659,39 @@ void extract_impl(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* 
   if (I == 0) return;
   upload_model(c, in, p, X, false, true);
   const size_t S = static_cast<size_t>(I * J);
+  if (f32(c) && !noise) {
+    // complex64 mode: single-precision Wiener filter from the complex64 x
+    alloc_f32(c, I, J, M);
+    x_to_f32(c, S, M);
+    params_to_f32(c, S, c->rh.as<double>(), c->ru.as<double>());
+    WienerArgsF32 Wf{};
+    Wf.nb = I;
+    Wf.J = J;
+    Wf.X = c->Xf.as<float2>();
+    Wf.a = c->a.as<double2>();
+    Wf.b = c->b.as<double2>();
+    Wf.Rpp = c->Rpp.as<double2>();
+    Wf.r_h = c->rhf.as<float>();
+    Wf.r_u = c->ruf.as<float>();
+    Wf.lambda = c->lam.as<double>();
+    Wf.dry = dry ? c->dryf.get<float2>(S) : nullptr;
+    Wf.image = image ? c->imagef.get<float2>(S * M) : nullptr;
+    c->launched(launch_wiener_f32(c->stream, M, Wf, true));
+    if (dry) {
+      double2* dd = c->dry.get<double2>(S);
+      c->launched(launch_f2d(c->stream, c->dryf.as<float>(), reinterpret_cast<double*>(dd), 2 * S));
+      double2* t = c->tmp.get<double2>(S);
+      c->launched(launch_to_ij_c(c->stream, dd, t, 1, I, J));
+      d2h(c, dry, t, S * sizeof(double2));
+    }
+    if (image) {
+      double2* im = c->image.get<double2>(S * M);
+      c->launched(launch_f2d(c->stream, c->imagef.as<float>(), reinterpret_cast<double*>(im), 2 * S * M));
+      d2h(c, image, im, S * M * sizeof(double2));
+    }
+    sync(c);
+    return;
+  }
   WienerArgs Wa{};
   Wa.nb = I;
   Wa.J = J;
@@ -643,7 +731,7 @@ int rcscm_gpu_create(const rcscm_gpu_config* cfg, rcscm_gpu_ctx** out) {
     *out = nullptr;
     rcscm_gpu_config d{0, RCSCM_C128, nullptr};
     if (cfg) d = *cfg;
-    if (d.precision != RCSCM_C128) fail(RCSCM_UNSUPPORTED, "precision: only RCSCM_C128 is implemented in this build");
+    if (d.precision != RCSCM_C128 && d.precision != RCSCM_C64) fail(RCSCM_INVALID_INPUT, "precision must be RCSCM_C128 or RCSCM_C64");
     int n = 0;
     CK(cudaGetDeviceCount(&n));
     if (d.device < 0 || d.device >= n) fail(RCSCM_INVALID_INPUT, "device ordinal out of range");
@@ -674,7 +762,8 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
   for (DBuf* b : {&c->X, &c->W, &c->A, &c->T, &c->V, &c->a, &c->b, &c->Rp, &c->Rpp, &c->power, &c->sab, &c->taa,
                   &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->lpd, &c->rh0, &c->ru0, &c->lam0, &c->tmp,
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->dry, &c->image, &c->noise,
-                  &c->partial, &c->obj, &c->err})
+                  &c->partial, &c->obj, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
+                  &c->dryf, &c->imagef})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -821,6 +910,13 @@ int rcscm_gpu_session_load(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, in
     h2d(c, c->A.p, A, nb * M * M * sizeof(double2));
     h2d(c, c->T.p, T, B * I * K * sizeof(double));
     h2d(c, c->V.p, V, B * K * J * sizeof(double));
+    if (f32(c)) {
+      alloc_f32(c, nb, J, M);
+      c->dryf.get<float2>(S);
+      c->imagef.get<float2>(S * M);
+      x_to_f32(c, S, M);
+    }
+    c->f32_params_current = false;
     c->sB = B;
     c->sI = I;
     c->sJ = J;
@@ -847,9 +943,13 @@ int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_h
     bool pre_done = false;
     if (stages & RCSCM_STAGE_SETUP) {
       c->launched(launch_setup(c->stream, P, 1e-10, eps_var), 2);
-      const bool pre = (stages & RCSCM_STAGE_PRECOMPUTE) != 0;
+      const bool pre = (stages & RCSCM_STAGE_PRECOMPUTE) != 0 && !f32(c);
       c->launched(launch_slots(c->stream, P, true, pre, eps_var));
       pre_done = pre;
+      if (f32(c)) {
+        params_to_f32(c, S, c->rh.as<double>(), c->ru.as<double>());
+        c->f32_params_current = true;
+      }
       d2d(c, c->rh0.p, c->rh.p, S * sizeof(double));
       d2d(c, c->ru0.p, c->ru.p, S * sizeof(double));
       d2d(c, c->lam0.p, c->lam.p, nb * sizeof(double));
@@ -861,16 +961,26 @@ int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_h
       d2d(c, c->rh.p, c->rh0.p, S * sizeof(double));
       d2d(c, c->ru.p, c->ru0.p, S * sizeof(double));
       d2d(c, c->lam.p, c->lam0.p, nb * sizeof(double));
+      if (f32(c)) {
+        params_to_f32(c, S, c->rh0.as<double>(), c->ru0.as<double>());
+        c->f32_params_current = true;
+      }
     }
     if ((stages & RCSCM_STAGE_PRECOMPUTE) && !pre_done) {
-      c->launched(launch_slots(c->stream, P, false, true, eps_var));
+      precompute(c, P, eps_var);
       c->s_pre = true;
     }
     if (stages & RCSCM_STAGE_ACCEL) {
       if (!c->s_pre) fail(RCSCM_INVALID_INPUT, "session_run: ACCEL needs PRECOMPUTE");
       run_accel(c, accel_args(c, nb, J, M, iters, h, eps_var, 0.0));
+      if (f32(c)) c->f32_params_current = true;
     }
-    if (stages & RCSCM_STAGE_NAIVE) c->launched(launch_naive(c->stream, M, naive_args(c, nb, J, iters, h, eps_var)));
+    if (stages & RCSCM_STAGE_NAIVE) {
+      // the naive comparison rule runs in complex128 in both modes
+      if (f32(c) && c->f32_params_current) params_from_f32(c, S);
+      c->launched(launch_naive(c->stream, M, naive_args(c, nb, J, iters, h, eps_var)));
+      c->f32_params_current = false;
+    }
     if (stages & RCSCM_STAGE_WIENER) {
       if (!c->s_pre) fail(RCSCM_INVALID_INPUT, "session_run: WIENER needs PRECOMPUTE");
       WienerArgs Wa{};
@@ -886,7 +996,27 @@ int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_h
       Wa.lambda = c->lam.as<double>();
       Wa.dry = c->dry.as<double2>();
       Wa.image = c->image.as<double2>();
-      c->launched(launch_wiener(c->stream, M, Wa, false, false));
+      if (f32(c)) {
+        if (!c->f32_params_current) params_to_f32(c, S, c->rh.as<double>(), c->ru.as<double>());
+        WienerArgsF32 Wf{};
+        Wf.nb = nb;
+        Wf.J = J;
+        Wf.a = Wa.a;
+        Wf.sigma_ab = Wa.sigma_ab;
+        Wf.tau_aa = Wa.tau_aa;
+        Wf.sigma_bx = c->sbxf.as<float2>();
+        Wf.tau_ax = c->taxf.as<float2>();
+        Wf.r_h = c->rhf.as<float>();
+        Wf.r_u = c->ruf.as<float>();
+        Wf.lambda = Wa.lambda;
+        Wf.dry = c->dryf.as<float2>();
+        Wf.image = c->imagef.as<float2>();
+        c->launched(launch_wiener_f32(c->stream, M, Wf, false));
+        c->launched(launch_f2d(c->stream, c->dryf.as<float>(), c->dry.as<double>(), 2 * S));
+        c->launched(launch_f2d(c->stream, c->imagef.as<float>(), c->image.as<double>(), 2 * S * M));
+      } else {
+        c->launched(launch_wiener(c->stream, M, Wa, false, false));
+      }
     }
   });
 }
@@ -897,6 +1027,7 @@ int rcscm_gpu_session_fetch(rcscm_gpu_ctx* c, double* r_h, double* r_u, double* 
     if (!c || !c->s_loaded) fail(RCSCM_INVALID_INPUT, "session_fetch: no session loaded");
     const int64_t nb = c->sB * c->sI, J = c->sJ;
     const size_t S = static_cast<size_t>(nb * J);
+    if (f32(c) && c->f32_params_current) params_from_f32(c, S);
     d2h(c, r_h, c->rh.p, S * sizeof(double));
     d2h(c, r_u, c->ru.p, S * sizeof(double));
     d2h(c, lambda, c->lam.p, nb * sizeof(double));

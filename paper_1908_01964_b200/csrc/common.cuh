@@ -40,6 +40,39 @@ __device__ __forceinline__ double rcp_pos(double x) {
   return fma(r, fma(e, e, e), r);
 }
 
+// ---- complex64 (FP32 mode) counterparts ----------------------------------------
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.x, b.y, -a.y * b.x));
+}
+__device__ __forceinline__ float2 cfmac(float2 a, float2 b, float2 acc) {
+  return make_float2(fmaf(a.x, b.x, fmaf(a.y, b.y, acc.x)), fmaf(a.x, b.y, fmaf(-a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 acc) {
+  return make_float2(fmaf(a.x, b.x, fmaf(-a.y, b.y, acc.x)), fmaf(a.x, b.y, fmaf(a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ float cnorm(float2 a) { return fmaf(a.x, a.x, a.y * a.y); }
+// MUFU.RCP seed + one Newton step (~1 ulp in FP32) for strictly positive x.
+__device__ __forceinline__ float rcp_pos(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return fmaf(r, fmaf(-x, r, 1.0f), r);
+}
+__device__ __forceinline__ float2 to_c(double2 v, float) { return make_float2(static_cast<float>(v.x), static_cast<float>(v.y)); }
+__device__ __forceinline__ double2 to_c(double2 v, double) { return v; }
+template <class T>
+struct CplxOf;
+template <>
+struct CplxOf<double> {
+  using type = double2;
+};
+template <>
+struct CplxOf<float> {
+  using type = float2;
+};
+
 // Device error word: the lowest failing (slot << 8 | code) wins (atomicMin),
 // so the reported failure is the first in the reference's (bin, frame) order.
 enum ErrCode : unsigned {

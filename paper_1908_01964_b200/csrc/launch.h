@@ -31,10 +31,11 @@ struct AccelCfg {
   bool smem;  // phase-B constants in shared memory (k_accel SMEMC)
   bool lb3;   // 128-thread x 3-CTA launch bounds (k_accel LB3), CL == 1 and nt <= 128 only
   bool direct;  // r_u from rho(lambda_new) after the reduction (k_accel DIRECT), LB3 path only
+  bool f32;     // complex64 / FP32 per-slot arithmetic
 };
 // Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL /
 // RCSCM_ACCEL_SMEM force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
-AccelCfg choose_accel_cfg(int64_t J);
+AccelCfg choose_accel_cfg(int64_t J, bool f32 = false);
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg);
 
 cudaError_t launch_naive(cudaStream_t s, int M, const NaiveArgs& N);
@@ -55,5 +56,12 @@ cudaError_t launch_to_ij(cudaStream_t s, const double* src, double* dst, int64_t
                          int64_t ld = 0);
 cudaError_t launch_to_ij_c(cudaStream_t s, const double2* src, double2* dst, int64_t B, int64_t I, int64_t J);
 cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out);
+
+// complex64 (FP32) mode
+cudaError_t launch_slots_pre_f32(cudaStream_t s, const DevProblem& P, const float2* Xf, float2* sbx, float2* tax,
+                                 float* txx);
+cudaError_t launch_wiener_f32(cudaStream_t s, int M, const WienerArgsF32& W, bool from_x);
+cudaError_t launch_d2f(cudaStream_t s, const double* src, float* dst, int64_t n);
+cudaError_t launch_f2d(cudaStream_t s, const float* src, double* dst, int64_t n);
 
 }  // namespace rcscm

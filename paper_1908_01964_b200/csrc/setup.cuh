@@ -378,3 +378,72 @@ __global__ void __launch_bounds__(NT) k_slots(DevProblem P, double eps) {
 }
 
 }  // namespace rcscm
+
+namespace rcscm {
+
+// K1 in the complex64 (FP32) mode: sigma_bx, tau_ax, tau_xx in single precision
+// from the complex64 copy of x (solver_accel.hpp:33-64); the per-bin sigma_ab
+// and tau_aa stay in double (computed from the double a, b, R'^+ exactly as
+// k_slots does). Half the HBM bytes of the complex128 pass.
+template <int M, int NT>
+__global__ void __launch_bounds__(NT) k_slots_pre_f32(DevProblem P, const float2* __restrict__ Xf, float2* sbx_f,
+                                                      float2* tax_f, float* txx_f) {
+  __shared__ float2 sRpp[M * M];
+  __shared__ float2 sb[M];
+  __shared__ float2 sp[M];
+  __shared__ double2 dp[M];
+  const int64_t bin = blockIdx.x;
+  const int tid = threadIdx.x;
+  for (int k = tid; k < M * M; k += NT) sRpp[k] = to_c(P.Rpp[bin * M * M + k], 0.0f);
+  if (tid < M) {
+    sb[tid] = to_c(P.b[bin * M + tid], 0.0f);
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = 0; k < M; ++k) s = cfma(P.Rpp[bin * M * M + tid + k * M], P.a[bin * M + k], s);
+    dp[tid] = s;
+    sp[tid] = to_c(s, 0.0f);
+  }
+  __syncthreads();
+  if (blockIdx.y == 0 && tid == 0) {
+    double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);
+    for (int k = 0; k < M; ++k) {
+      const double2 ak = P.a[bin * M + k];
+      ab = cfmac(ak, P.b[bin * M + k], ab);
+      aa = cfmac(ak, dp[k], aa);
+    }
+    P.sigma_ab[bin] = ab;
+    P.tau_aa[bin] = fmax(aa.x, 0.0);
+  }
+  const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + tid;
+  if (t >= P.J) return;
+  const int64_t slot = bin * P.J + t;
+  float2 x[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) x[m] = Xf[slot * M + m];
+  float2 sbx = make_float2(0.f, 0.f), tax = make_float2(0.f, 0.f), xx = make_float2(0.f, 0.f);
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    sbx = cfmac(sb[r], x[r], sbx);
+    tax = cfmac(sp[r], x[r], tax);
+    float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < M; ++k) acc = cfma(sRpp[r + k * M], x[k], acc);
+    xx = cfmac(x[r], acc, xx);
+  }
+  sbx_f[slot] = sbx;
+  tax_f[slot] = tax;
+  txx_f[slot] = fmaxf(xx.x, 0.f);
+}
+
+// double <-> float element conversions (complex arrays pass 2 * count).
+static __global__ void k_d2f(const double* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[k] = static_cast<float>(src[k]);
+}
+static __global__ void k_f2d(const float* __restrict__ src, double* __restrict__ dst, int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[k] = static_cast<double>(src[k]);
+}
+
+}  // namespace rcscm

@@ -1,4 +1,6 @@
 // setup_launch.cu -- launchers of K1a / K1b / K1 (setup.cuh).
+#include <algorithm>
+
 #include "dispatch.cuh"
 #include "launch.h"
 
@@ -51,6 +53,30 @@ cudaError_t launch_slots(cudaStream_t s, const DevProblem& P, bool init, bool pr
       k_slots<MM, kSlotNT, false, true><<<grid, kSlotNT, 0, s>>>(P, eps);
     return cudaGetLastError();
   });
+}
+
+cudaError_t launch_slots_pre_f32(cudaStream_t s, const DevProblem& P, const float2* Xf, float2* sbx, float2* tax,
+                                 float* txx) {
+  if (P.nb * P.J == 0) return cudaSuccess;
+  return dispatch_mics(P.M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    dim3 grid(P.nb, (P.J + kSlotNT - 1) / kSlotNT);
+    k_slots_pre_f32<MM, kSlotNT><<<grid, kSlotNT, 0, s>>>(P, Xf, sbx, tax, txx);
+    return cudaGetLastError();
+  });
+}
+
+static int conv_blocks(int64_t n) { return static_cast<int>(std::min<int64_t>((n + 255) / 256, 148 * 16)); }
+
+cudaError_t launch_d2f(cudaStream_t s, const double* src, float* dst, int64_t n) {
+  if (n == 0) return cudaSuccess;
+  k_d2f<<<conv_blocks(n), 256, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_f2d(cudaStream_t s, const float* src, double* dst, int64_t n) {
+  if (n == 0) return cudaSuccess;
+  k_f2d<<<conv_blocks(n), 256, 0, s>>>(src, dst, n);
+  return cudaGetLastError();
 }
 
 }  // namespace rcscm

@@ -331,3 +331,103 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double seed, int iters, doub
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
 }  // namespace rcscm
+
+namespace rcscm {
+
+// K4 in the complex64 (FP32) mode (wiener.hpp:19-43): the resident FP32
+// sigma_bx / tau_ax / r_h / r_u (or, FROM_X, sigma/tau recomputed from the
+// complex64 x) give s^ and image = a s^ in single precision; per-bin rho_aa and
+// 1/lambda are formed in double.
+struct WienerArgsF32 {
+  int64_t nb, J;
+  const float2* X;          // FROM_X
+  const double2* a;
+  const double2* b;         // FROM_X
+  const double2* Rpp;       // FROM_X
+  const double2* sigma_ab;  // !FROM_X
+  const double* tau_aa;     // !FROM_X
+  const float2* sigma_bx;   // !FROM_X
+  const float2* tau_ax;     // !FROM_X
+  const float* r_h;
+  const float* r_u;
+  const double* lambda;
+  float2* dry;
+  float2* image;
+};
+
+template <int M, int NT, bool FROM_X>
+__global__ void __launch_bounds__(NT) k_wiener_f32(WienerArgsF32 P) {
+  __shared__ float2 sa[M];
+  __shared__ float2 sb[M];
+  __shared__ float2 sp[M];
+  __shared__ double2 dpa[M];
+  __shared__ float sbin[4];
+  const int64_t bin = blockIdx.x;
+  const int tid = threadIdx.x;
+  if (tid < M) {
+    sa[tid] = to_c(P.a[bin * M + tid], 0.0f);
+    if (FROM_X) {
+      sb[tid] = to_c(P.b[bin * M + tid], 0.0f);
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = 0; k < M; ++k) s = cfma(P.Rpp[bin * M * M + tid + k * M], P.a[bin * M + k], s);
+      dpa[tid] = s;
+      sp[tid] = to_c(s, 0.0f);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double2 sab;
+    double taa;
+    if (FROM_X) {
+      double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);
+      for (int k = 0; k < M; ++k) {
+        const double2 ak = P.a[bin * M + k];
+        ab = cfmac(ak, P.b[bin * M + k], ab);
+        aa = cfmac(ak, dpa[k], aa);
+      }
+      sab = ab;
+      taa = fmax(aa.x, 0.0);
+    } else {
+      sab = P.sigma_ab[bin];
+      taa = P.tau_aa[bin];
+    }
+    const double inv_lam = 1.0 / P.lambda[bin];
+    sbin[0] = static_cast<float>(taa + cnorm(sab) * inv_lam);
+    sbin[1] = static_cast<float>(sab.x);
+    sbin[2] = static_cast<float>(sab.y);
+    sbin[3] = static_cast<float>(inv_lam);
+  }
+  __syncthreads();
+  const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + tid;
+  if (t >= P.J) return;
+  const int64_t slot = bin * P.J + t;
+  const float raa = sbin[0];
+  const float2 sab = make_float2(sbin[1], sbin[2]);
+  const float inv_lam = sbin[3];
+  float2 sbx, tax;
+  if (FROM_X) {
+    sbx = make_float2(0.f, 0.f);
+    tax = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const float2 xm = P.X[slot * M + m];
+      sbx = cfmac(sb[m], xm, sbx);
+      tax = cfmac(sp[m], xm, tax);
+    }
+  } else {
+    sbx = P.sigma_bx[slot];
+    tax = P.tau_ax[slot];
+  }
+  const float2 c = cmul(sab, sbx);
+  const float2 rax = make_float2(fmaf(c.x, inv_lam, tax.x), fmaf(c.y, inv_lam, tax.y));
+  const float rh = P.r_h[slot], ru = P.r_u[slot];
+  const float gamma = rh / fmaf(rh, raa, ru);
+  const float2 s = make_float2(rax.x * gamma, rax.y * gamma);
+  if (P.dry) P.dry[slot] = s;
+  if (P.image) {
+#pragma unroll
+    for (int m = 0; m < M; ++m) P.image[slot * M + m] = cmul(sa[m], s);
+  }
+}
+
+}  // namespace rcscm

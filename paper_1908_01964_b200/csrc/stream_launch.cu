@@ -73,4 +73,17 @@ cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out
   return cudaGetLastError();
 }
 
+cudaError_t launch_wiener_f32(cudaStream_t s, int M, const WienerArgsF32& W, bool from_x) {
+  if (W.nb * W.J == 0) return cudaSuccess;
+  return dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    dim3 grid(W.nb, (W.J + kWienerNT - 1) / kWienerNT);
+    if (from_x)
+      k_wiener_f32<MM, kWienerNT, true><<<grid, kWienerNT, 0, s>>>(W);
+    else
+      k_wiener_f32<MM, kWienerNT, false><<<grid, kWienerNT, 0, s>>>(W);
+    return cudaGetLastError();
+  });
+}
+
 }  // namespace rcscm

@@ -305,3 +305,48 @@ def test_pipelined_entry_point_bitwise(O, gpu, monkeypatch):
     assert np.array_equal(single.r_h, piped.r_h)
     assert np.array_equal(single.r_u, piped.r_u)
     assert np.array_equal(single.lam, piped.lam)
+
+
+# ---- complex64 (FP32) mode: relative-L2 <= 1e-4 on the output ----------------------
+def _rel_l2(got, ref):
+    got = np.asarray(got)
+    ref = np.asarray(ref)
+    return float(np.linalg.norm(got - ref) / max(np.linalg.norm(ref), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def gpu64():
+    from paper_1908_01964_b200 import GpuContext
+
+    return GpuContext(0, precision="c64")
+
+
+@pytest.mark.parametrize("cfg,I,J,iters", [(0, 64, 320, 100), (1, 32, 640, 100), (4, 8, 4096, 100), (2, 4, 20000, 50)])
+def test_c64_output_rel_l2(O, gpu64, cfg, I, J, iters):
+    u, inp, p0 = _synthetic(O, cfg, I, J)
+    g = gpu64.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=iters)).params
+    o = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=iters)).params
+    ge = gpu64.extract_target(inp, g, u.X)
+    oimg, odry = O.extract_target(inp, o, u.X)
+    assert _rel_l2(ge.dry, odry) <= 1e-4, _rel_l2(ge.dry, odry)
+    assert _rel_l2(ge.image, oimg) <= 1e-4
+    assert _rel_l2(g.lam, o.lam) <= 1e-4
+
+
+def test_c64_session_pipeline(O, gpu64):
+    from paper_1908_01964_b200 import synth
+    import paper_1908_01964_b200._capi as C
+
+    utts = synth.make_config(4, utterances=2, I=8, J=4096)
+    X, W, A, T, V = synth.stack(utts)
+    gpu64.session_load(X, W, A, T, V, 0)
+    gpu64.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL | C.STAGE_WIENER, 100)
+    gpu64.session_check()
+    out = gpu64.session_fetch(want_image=True)
+    for k, u in enumerate(utts):
+        inp = O.build_noise_scm(u.W, u.A, u.X, 0)
+        p0 = O.init_params(inp, u.T, u.V, u.W, u.A, u.X)
+        o = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=100)).params
+        oimg, odry = O.extract_target(inp, o, u.X)
+        assert _rel_l2(out["dry"][k], odry) <= 1e-4
+        assert _rel_l2(out["image"][k], oimg) <= 1e-4

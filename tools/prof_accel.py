@@ -13,12 +13,13 @@ ap.add_argument("--naive", action="store_true")
 ap.add_argument("--I", type=int, default=None)
 ap.add_argument("--J", type=int, default=None)
 ap.add_argument("--B", type=int, default=1)
+ap.add_argument("--c64", action="store_true")
 a = ap.parse_args()
 c = synth.CONFIGS[a.cfg]
 utts = synth.make_config(a.cfg, utterances=a.B, I=a.I, J=a.J)
 X, W, A, T, V = synth.stack(utts)
 s = torch.cuda.Stream()
-ctx = GpuContext(0, stream=s.cuda_stream)
+ctx = GpuContext(0, precision="c64" if a.c64 else "c128", stream=s.cuda_stream)
 ctx.session_load(X, W, A, T, V, 0)
 ctx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
 h = Hyperparams()
@@ -38,6 +39,6 @@ ctx.session_check()
 ms = min(e0.elapsed_time(e1) for e0, e1 in ev)
 B, I, J, M = X.shape
 it = c["naive_iters"] if a.naive else c["iters"]
-print(f"cfg{a.cfg} B={B} I={I} J={J} {'naive' if a.naive else 'accel'} spt={os.environ.get('RCSCM_ACCEL_SPT','auto')} "
+print(f"{'c64' if a.c64 else 'c128'} cfg{a.cfg} B={B} I={I} J={J} {'naive' if a.naive else 'accel'} spt={os.environ.get('RCSCM_ACCEL_SPT','auto')} "
       f"cl={os.environ.get('RCSCM_ACCEL_CL','auto')}: {ms:.4f} ms  {B*I*J*it/(ms*1e-3)/1e9:.1f} G slot-it/s  "
       f"{47*B*I*J*it/(ms*1e-3)/1e12:.2f} TF(47)")

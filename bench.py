@@ -36,8 +36,10 @@ sys.path.insert(0, ROOT)
 CFG = 1
 FLOPS_ACCEL = 47.0  # canonical flops per slot-iteration
 FLOPS_NAIVE = {2: 341.0, 4: 1804.0, 8: 11052.0}
-# K1 / K4 algorithmic bytes per slot (complex128): SURVEY 8(d)
-BYTES_PRE = {2: 88.0, 4: 120.0, 8: 184.0}
+# K1 / K4 algorithmic bytes per slot (complex128): SURVEY 8(d). The timed step's
+# K1 is the sigma/tau pass only: read x (16 M) + write sigma_bx, tau_ax, tau_xx (40);
+# SURVEY's 88/120/184 also count the r_h0 / r_u0 writes of the setup pass.
+BYTES_PRE = {2: 72.0, 4: 104.0, 8: 168.0}
 BYTES_WIENER = {2: 96.0, 4: 128.0, 8: 192.0}
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # HGX B200 spec class
 
@@ -357,6 +359,9 @@ def run_gpu(args):
              "canonical_flops_per_slot_iter": FLOPS_NAIVE.get(M),
              "accel_over_naive_per_iteration": (naive_ms / naive_iters) / (k2_avg / iters)}
 
+    # complex64 (FP32) mode of the same step, against the measured FP32 peak
+    c64 = c64_measure(local, tstream, X, W, A, T, V, iters, hyper, S, args, torch, C)
+
     # e2e through the C ABI with pinned host buffers (reference layout)
     e2e = e2e_measure(ctx, u, iters, hyper, args, torch)
 
@@ -386,6 +391,7 @@ def run_gpu(args):
             "roofline": roofline,
             "stream_kernels": stream_kernels,
             "naive": naive,
+            "c64": c64,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clocks,
@@ -395,6 +401,40 @@ def run_gpu(args):
         dist.barrier()
         dist.destroy_process_group()
     ctx.close()
+
+
+def c64_measure(local, tstream, X, W, A, T, V, iters, hyper, S, args, torch, C):
+    """The same device step in the complex64 / FP32 mode (output within
+    relative-L2 1e-4 of complex128, tests/test_gpu_parity.py)."""
+    from paper_1908_01964_b200 import GpuContext
+
+    ctx = GpuContext(local, precision="c64", stream=tstream.cuda_stream)
+    ctx.session_load(X, W, A, T, V, 0)
+    ctx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
+    for _ in range(max(args.warmup, 1)):
+        ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE, 0, hyper)
+        ctx.session_run(C.STAGE_ACCEL, iters, hyper)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for e0, e1, e2 in ev:
+        e0.record(tstream)
+        ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE, 0, hyper)
+        e1.record(tstream)
+        ctx.session_run(C.STAGE_ACCEL, iters, hyper)
+        e2.record(tstream)
+    torch.cuda.synchronize()
+    ctx.session_check()
+    step = sum(a.elapsed_time(c) for a, _, c in ev) / len(ev)
+    k2 = sum(b.elapsed_time(c) for _, b, c in ev) / len(ev)
+    tf = ctypes.c_double()
+    rc = C.load().rcscm_gpu_probe_fp32(ctx.handle, ctypes.byref(tf), None)
+    peak = tf.value if rc == 0 else None
+    achieved = FLOPS_ACCEL * S * iters / (k2 * 1e-3) / 1e12
+    ctx.close()
+    return {"value": S * iters / (step * 1e-3), "unit": "TF-slot updates/s", "ms_per_step": step,
+            "accel_k2_ms": k2, "achieved_tflops": achieved, "fp32_peak_tflops": peak,
+            "frac": achieved / peak if peak else None,
+            "note": "same step with x, sigma/tau and the slot arithmetic in single precision; lambda in double"}
 
 
 def e2e_measure(ctx, u, iters, hyper, args, torch):

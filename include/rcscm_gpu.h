@@ -182,6 +182,8 @@ void* rcscm_gpu_stream(rcscm_gpu_ctx* ctx);
  * Measured FP64 FMA-pipe throughput of this device (independent DFMA chains on
  * every SM), the denominator of the accel kernel's roofline fraction. */
 int rcscm_gpu_probe_fp64(rcscm_gpu_ctx* ctx, double* tflops, double* ms);
+/* Same for the FP32 FMA pipe (denominator of the complex64 mode). */
+int rcscm_gpu_probe_fp32(rcscm_gpu_ctx* ctx, double* tflops, double* ms);
 
 #ifdef __cplusplus
 }

@@ -111,6 +111,7 @@ SIGNATURES = {
     "rcscm_gpu_session_check": (ctypes.c_int, [_vp]),
     "rcscm_gpu_stream": (_vp, [_vp]),
     "rcscm_gpu_probe_fp64": (ctypes.c_int, [_vp, _dp, _dp]),
+    "rcscm_gpu_probe_fp32": (ctypes.c_int, [_vp, _dp, _dp]),
 }
 
 _lib = None

@@ -1044,17 +1044,18 @@ int rcscm_gpu_session_check(rcscm_gpu_ctx* c) {
   });
 }
 
-int rcscm_gpu_probe_fp64(rcscm_gpu_ctx* c, double* tflops, double* ms) {
+static int probe(rcscm_gpu_ctx* c, bool fp32, double* tflops, double* ms) {
   return guarded([&] {
-    if (!c || !tflops) fail(RCSCM_INVALID_INPUT, "probe_fp64: NULL argument");
+    if (!c || !tflops) fail(RCSCM_INVALID_INPUT, "probe: NULL argument");
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
     constexpr int kNacc = 8, kNt = 256;
-    const int blocks = sms * 8, iters = 20000;
+    const int blocks = sms * 8, iters = fp32 ? 40000 : 20000;
     double* out = c->obj.get<double>(1);
-    c->launched(launch_fp64_probe(c->stream, blocks, iters / 10, out));  // warm-up
+    auto run = [&](int n) { return fp32 ? launch_fp32_probe(c->stream, blocks, n, out) : launch_fp64_probe(c->stream, blocks, n, out); };
+    c->launched(run(iters / 10));  // warm-up
     CK(cudaEventRecord(c->ev0, c->stream));
-    c->launched(launch_fp64_probe(c->stream, blocks, iters, out));
+    c->launched(run(iters));
     CK(cudaEventRecord(c->ev1, c->stream));
     CK(cudaEventSynchronize(c->ev1));
     float t = 0.f;
@@ -1064,5 +1065,8 @@ int rcscm_gpu_probe_fp64(rcscm_gpu_ctx* c, double* tflops, double* ms) {
     if (ms) *ms = t;
   });
 }
+
+int rcscm_gpu_probe_fp64(rcscm_gpu_ctx* c, double* tflops, double* ms) { return probe(c, false, tflops, ms); }
+int rcscm_gpu_probe_fp32(rcscm_gpu_ctx* c, double* tflops, double* ms) { return probe(c, true, tflops, ms); }
 
 }  // extern "C"

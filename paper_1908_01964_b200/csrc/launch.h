@@ -56,6 +56,7 @@ cudaError_t launch_to_ij(cudaStream_t s, const double* src, double* dst, int64_t
                          int64_t ld = 0);
 cudaError_t launch_to_ij_c(cudaStream_t s, const double2* src, double2* dst, int64_t B, int64_t I, int64_t J);
 cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out);
+cudaError_t launch_fp32_probe(cudaStream_t s, int blocks, int iters, double* out);
 
 // complex64 (FP32) mode
 cudaError_t launch_slots_pre_f32(cudaStream_t s, const DevProblem& P, const float2* Xf, float2* sbx, float2* tax,

@@ -330,6 +330,23 @@ __global__ void __launch_bounds__(256) k_fp64_probe(double seed, int iters, doub
   for (int k = 0; k < NACC; ++k) s += acc[k];
   if (s == 12345.678) out[0] = s;  // keep the chains alive
 }
+// FP32 counterpart of k_fp64_probe (FFMA chains) for the complex64-mode roofline.
+template <int NACC>
+__global__ void __launch_bounds__(256) k_fp32_probe(float seed, int iters, double* out) {
+  float acc[NACC];
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) acc[k] = seed + 1e-3f * (threadIdx.x + k);
+  const float m = 0.9999999f, a = 1e-7f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < NACC; ++k) acc[k] = fmaf(acc[k], m, a);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NACC; ++k) s += acc[k];
+  if (s == 12345.678f) out[0] = s;
+}
+
 }  // namespace rcscm
 
 namespace rcscm {

@@ -72,6 +72,10 @@ cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out
   k_fp64_probe<8><<<blocks, 256, 0, s>>>(1.0, iters, out);
   return cudaGetLastError();
 }
+cudaError_t launch_fp32_probe(cudaStream_t s, int blocks, int iters, double* out) {
+  k_fp32_probe<8><<<blocks, 256, 0, s>>>(1.0f, iters, out);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_wiener_f32(cudaStream_t s, int M, const WienerArgsF32& W, bool from_x) {
   if (W.nb * W.J == 0) return cudaSuccess;

@@ -53,9 +53,12 @@ struct AccelArgs {
   const double2* sigma_bx;  // [bin][t]
   const double2* tau_ax;    // [bin][t]
   const double* tau_xx;     // [bin][t]
-  double* r_h;              // [bin][t] in/out
-  double* r_u;              // [bin][t] in/out
-  double* lambda;           // [bin]    in/out
+  double* r_h;              // [bin][t] out
+  double* r_u;              // [bin][t] out
+  double* lambda;           // [bin]    out
+  const double* r_h_in;     // [bin][t] initial iterate (may alias r_h)
+  const double* r_u_in;
+  const double* lambda_in;  // [bin]
   double* traj_r_h;         // optional [it][bin][t]
   double* traj_r_u;
   double* traj_lambda;      // optional [it][bin]
@@ -65,6 +68,8 @@ struct AccelArgs {
   const float* tau_xx_f;
   float* r_h_f;
   float* r_u_f;
+  const float* r_h_f_in;  // initial iterate (may alias r_h_f)
+  const float* r_u_f_in;
 };
 
 // std::max(v, eps) of the reference (returns v unless v < eps) for eps > 0,
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   const double2 sab = P.sigma_ab[bin];
   const double s2 = cnorm(sab);  // |sigma_ab|^2
   const double taa = P.tau_aa[bin];
-  double lam = P.lambda[bin];
+  double lam = P.lambda_in[bin];
   double il = 1.0 / lam;
   double raa = fma(s2, il, taa);  // rho_aa (solver_accel.hpp:122)
   const CT sabT = to_c(sab, T());
@@ -191,14 +196,14 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     CT tk;
     T xk;
     if constexpr (F32) {
-      rh[k] = P.r_h_f[s];
-      ru[k] = P.r_u_f[s];
+      rh[k] = P.r_h_f_in[s];
+      ru[k] = P.r_u_f_in[s];
       sbx[k] = P.sigma_bx_f[s];
       tk = P.tau_ax_f[s];
       xk = P.tau_xx_f[s] * invMT;
     } else {
-      rh[k] = P.r_h[s];
-      ru[k] = P.r_u[s];
+      rh[k] = P.r_h_in[s];
+      ru[k] = P.r_u_in[s];
       sbx[k] = P.sigma_bx[s];
       tk = P.tau_ax[s];
       xk = P.tau_xx[s] * invMT;

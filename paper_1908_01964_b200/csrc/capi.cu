@@ -85,10 +85,13 @@ struct rcscm_gpu_ctx {
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
   // complex64 (FP32) mode copies of the slot arrays
-  DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef;
+  DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef, rh0f, ru0f;
   bool f32_params_current = false;  // session: FP32 r_h / r_u hold the latest iterate
   // session geometry
   bool s_loaded = false, s_setup = false, s_pre = false;
+  // RESET is applied lazily: the next ACCEL reads params0 directly (no copy
+  // pass); any other consumer of the iterate materialises it first.
+  bool s_reset_pending = false;
   int64_t sB = 0, sI = 0, sJ = 0;
   int sM = 0, sK = 0, sn_h = 0;
 
@@ -286,6 +289,11 @@ AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, 
   A.tau_xx_f = c->txxf.as<float>();
   A.r_h_f = c->rhf.as<float>();
   A.r_u_f = c->ruf.as<float>();
+  A.r_h_in = A.r_h;
+  A.r_u_in = A.r_u;
+  A.lambda_in = A.lambda;
+  A.r_h_f_in = A.r_h_f;
+  A.r_u_f_in = A.r_u_f;
   return A;
 }
 
@@ -510,6 +518,9 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
     A.r_h += off;
     A.r_u += off;
     A.lambda += i0;
+    A.r_h_in += off;
+    A.r_u_in += off;
+    A.lambda_in += i0;
     if (opt->iters > 0) c->launched(launch_accel(cs, A, g));
     c->launched(launch_to_ij(cs, c->rh.as<double>() + off, t1 + i0, 1, Ic, J, I));
     c->launched(launch_to_ij(cs, c->ru.as<double>() + off, t2 + i0, 1, Ic, J, I));
@@ -763,7 +774,7 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
                   &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->lpd, &c->rh0, &c->ru0, &c->lam0, &c->tmp,
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
-                  &c->dryf, &c->imagef})
+                  &c->dryf, &c->imagef, &c->rh0f, &c->ru0f})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -926,9 +937,24 @@ int rcscm_gpu_session_load(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, in
     c->s_loaded = true;
     c->s_setup = false;
     c->s_pre = false;
+    c->s_reset_pending = false;
     reset_err(c);
     sync(c);
   });
+}
+
+// Applies a pending RESET to the working iterate (rh, ru, lam and the FP32 copies).
+static void materialize_reset(rcscm_gpu_ctx* c, size_t S, int64_t nb) {
+  if (!c->s_reset_pending) return;
+  d2d(c, c->rh.p, c->rh0.p, S * sizeof(double));
+  d2d(c, c->ru.p, c->ru0.p, S * sizeof(double));
+  d2d(c, c->lam.p, c->lam0.p, nb * sizeof(double));
+  if (f32(c)) {
+    d2d(c, c->rhf.p, c->rh0f.p, S * sizeof(float));
+    d2d(c, c->ruf.p, c->ru0f.p, S * sizeof(float));
+    c->f32_params_current = true;
+  }
+  c->s_reset_pending = false;
 }
 
 int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_hyper* hyper, double eps_var) {
@@ -949,32 +975,37 @@ int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_h
       if (f32(c)) {
         params_to_f32(c, S, c->rh.as<double>(), c->ru.as<double>());
         c->f32_params_current = true;
+        d2d(c, c->rh0f.get<float>(S), c->rhf.p, S * sizeof(float));
+        d2d(c, c->ru0f.get<float>(S), c->ruf.p, S * sizeof(float));
       }
       d2d(c, c->rh0.p, c->rh.p, S * sizeof(double));
       d2d(c, c->ru0.p, c->ru.p, S * sizeof(double));
       d2d(c, c->lam0.p, c->lam.p, nb * sizeof(double));
       c->s_setup = true;
+      c->s_reset_pending = false;
       if (pre) c->s_pre = true;
     }
     if (!c->s_setup) fail(RCSCM_INVALID_INPUT, "session_run: run RCSCM_STAGE_SETUP first");
-    if (stages & RCSCM_STAGE_RESET) {
-      d2d(c, c->rh.p, c->rh0.p, S * sizeof(double));
-      d2d(c, c->ru.p, c->ru0.p, S * sizeof(double));
-      d2d(c, c->lam.p, c->lam0.p, nb * sizeof(double));
-      if (f32(c)) {
-        params_to_f32(c, S, c->rh0.as<double>(), c->ru0.as<double>());
-        c->f32_params_current = true;
-      }
-    }
+    if (stages & RCSCM_STAGE_RESET) c->s_reset_pending = true;
     if ((stages & RCSCM_STAGE_PRECOMPUTE) && !pre_done) {
       precompute(c, P, eps_var);
       c->s_pre = true;
     }
     if (stages & RCSCM_STAGE_ACCEL) {
       if (!c->s_pre) fail(RCSCM_INVALID_INPUT, "session_run: ACCEL needs PRECOMPUTE");
-      run_accel(c, accel_args(c, nb, J, M, iters, h, eps_var, 0.0));
+      AccelArgs A = accel_args(c, nb, J, M, iters, h, eps_var, 0.0);
+      if (c->s_reset_pending) {
+        A.r_h_in = c->rh0.as<double>();
+        A.r_u_in = c->ru0.as<double>();
+        A.lambda_in = c->lam0.as<double>();
+        A.r_h_f_in = c->rh0f.as<float>();
+        A.r_u_f_in = c->ru0f.as<float>();
+        c->s_reset_pending = false;
+      }
+      run_accel(c, A);
       if (f32(c)) c->f32_params_current = true;
     }
+    if (stages & (RCSCM_STAGE_NAIVE | RCSCM_STAGE_WIENER)) materialize_reset(c, S, nb);
     if (stages & RCSCM_STAGE_NAIVE) {
       // the naive comparison rule runs in complex128 in both modes
       if (f32(c) && c->f32_params_current) params_from_f32(c, S);
@@ -1027,6 +1058,7 @@ int rcscm_gpu_session_fetch(rcscm_gpu_ctx* c, double* r_h, double* r_u, double* 
     if (!c || !c->s_loaded) fail(RCSCM_INVALID_INPUT, "session_fetch: no session loaded");
     const int64_t nb = c->sB * c->sI, J = c->sJ;
     const size_t S = static_cast<size_t>(nb * J);
+    materialize_reset(c, S, nb);
     if (f32(c) && c->f32_params_current) params_from_f32(c, S);
     d2h(c, r_h, c->rh.p, S * sizeof(double));
     d2h(c, r_u, c->ru.p, S * sizeof(double));

@@ -350,3 +350,40 @@ def test_c64_session_pipeline(O, gpu64):
         oimg, odry = O.extract_target(inp, o, u.X)
         assert _rel_l2(out["dry"][k], odry) <= 1e-4
         assert _rel_l2(out["image"][k], oimg) <= 1e-4
+
+
+@pytest.mark.parametrize("prec", ["c128", "c64"])
+def test_session_reset_replays(O, gpu, gpu64, prec):
+    """RESET restores params0 lazily: RESET+ACCEL replays the first run bitwise,
+    RESET followed by a fetch returns params0, and RESET+NAIVE starts from params0."""
+    from paper_1908_01964_b200 import synth
+    import paper_1908_01964_b200._capi as C
+
+    g = gpu if prec == "c128" else gpu64
+    utts = synth.make_config(1, utterances=2, I=24, J=640)
+    X, W, A, T, V = synth.stack(utts)
+    g.session_load(X, W, A, T, V, 0)
+    g.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
+    p0 = g.session_fetch()
+    g.session_run(C.STAGE_ACCEL, 7)
+    first = g.session_fetch()
+    g.session_run(C.STAGE_ACCEL, 3)  # moves the iterate on
+    g.session_run(C.STAGE_RESET | C.STAGE_ACCEL, 7)
+    again = g.session_fetch()
+    for k in ("r_h", "r_u", "lam"):
+        assert np.array_equal(first[k], again[k]), k
+        assert not np.array_equal(first[k], p0[k]), k
+    g.session_run(C.STAGE_RESET)
+    back = g.session_fetch()
+    for k in ("r_h", "r_u", "lam"):
+        assert np.array_equal(back[k], p0[k]), k
+    g.session_run(C.STAGE_ACCEL, 3)
+    g.session_run(C.STAGE_RESET | C.STAGE_NAIVE, 2)
+    nv = g.session_fetch()
+    u = utts[1]
+    inp = O.build_noise_scm(u.W, u.A, u.X, 0)
+    o0 = O.init_params(inp, u.T, u.V, u.W, u.A, u.X)
+    if prec == "c128":
+        o = O.run("naive", inp, o0, u.X, O.SolverOptions(iters=2)).params
+        assert np.allclose(nv["lam"][1], o.lam, rtol=1e-8, atol=0)
+    g.session_check()

@@ -1,8 +1,10 @@
 """Summarise ncu captures into profiles/ncu_summary.json (+ .md).
 
-usage: python tools/ncu_summary.py KEY=path.ncu-rep [KEY=path ...] [--launches launches.csv]
+usage: python tools/ncu_summary.py KEY=path.ncu-rep[@name-substring] [KEY=path ...]
 
-KEY names the kernel family (k_accel, k_slots, k_naive, k_wiener); bench.py
+KEY names the kernel family (k_accel, k_slots, k_naive, k_wiener); the capture's
+first launch whose name contains the substring (default: KEY) is summarised.
+bench.py
 reads profiles/ncu_summary.json[KEY].dram_bytes_per_launch for roofline.traffic.
 """
 import csv
@@ -74,8 +76,11 @@ def main(argv):
         if "=" not in arg:
             continue
         key, rep = arg.split("=", 1)
-        kernels = raw(rep)
+        rep, _, pat = rep.partition("@")
+        pat = pat or key
+        kernels = [k for k in raw(rep) if pat in k.get("Kernel Name", "")]
         if not kernels:
+            print(f"{key}: no launch matching {pat!r} in {rep}", file=sys.stderr)
             continue
         k = kernels[0]
         k["dram_bytes_per_launch"] = k.get("dram_read_bytes", 0.0) + k.get("dram_write_bytes", 0.0)

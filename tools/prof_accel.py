@@ -10,6 +10,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--cfg", type=int, default=1)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--naive", action="store_true")
+ap.add_argument("--wiener", action="store_true")
 ap.add_argument("--I", type=int, default=None)
 ap.add_argument("--J", type=int, default=None)
 ap.add_argument("--B", type=int, default=1)
@@ -28,7 +29,9 @@ for r in range(a.reps):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE, 0, h)
     e0.record(s)
-    if a.naive:
+    if a.wiener:
+        ctx.session_run(C.STAGE_WIENER, 0, h)
+    elif a.naive:
         ctx.session_run(C.STAGE_NAIVE, c["naive_iters"], h)
     else:
         ctx.session_run(C.STAGE_ACCEL, c["iters"], h)
@@ -38,7 +41,7 @@ torch.cuda.synchronize()
 ctx.session_check()
 ms = min(e0.elapsed_time(e1) for e0, e1 in ev)
 B, I, J, M = X.shape
-it = c["naive_iters"] if a.naive else c["iters"]
-print(f"{'c64' if a.c64 else 'c128'} cfg{a.cfg} B={B} I={I} J={J} {'naive' if a.naive else 'accel'} spt={os.environ.get('RCSCM_ACCEL_SPT','auto')} "
+it = 1 if a.wiener else (c["naive_iters"] if a.naive else c["iters"])
+print(f"{'c64' if a.c64 else 'c128'} cfg{a.cfg} B={B} I={I} J={J} {'wiener' if a.wiener else ('naive' if a.naive else 'accel')} spt={os.environ.get('RCSCM_ACCEL_SPT','auto')} "
       f"cl={os.environ.get('RCSCM_ACCEL_CL','auto')}: {ms:.4f} ms  {B*I*J*it/(ms*1e-3)/1e9:.1f} G slot-it/s  "
       f"{47*B*I*J*it/(ms*1e-3)/1e12:.2f} TF(47)")

@@ -131,7 +131,7 @@ __device__ __forceinline__ float tfma(float a, float b, float c) { return fmaf(a
 // FULL: every thread's SPT slots are inside the bin chunk (NT * SPT == chunk),
 // so no per-slot masks. TRAJ: record r_h / r_u / lambda after every iteration.
 // SMEMC: the four per-slot constants used only after the lambda reduction
-// (tau_ax, s_ab*s_bx, tau_xx/M, |s_bx|^2/M: 48 B/slot) live in dynamic shared
+// (tau_ax, u*s_bx, tau_xx/M, |s_bx|^2/M: 48 B/slot) live in dynamic shared
 // memory ([k][tid] planes, conflict-free) instead of registers, which roughly
 // halves the register footprint and doubles the resident warps per SM.
 // LB3: launch bounds of 128 threads x 3 CTAs/SM (<= 170 registers) instead of
@@ -177,7 +177,15 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   double lam = P.lambda_in[bin];
   double il = 1.0 / lam;
   double raa = fma(s2, il, taa);  // rho_aa (solver_accel.hpp:122)
-  const CT sabT = to_c(sab, T());
+  // Rotated residual: with u = s_ab / |s_ab| (1 when s_ab = 0) and the per-slot
+  // constant c = u s_bx,  |s_bx - g conj(s_ab) rho_ax| = |c - g |s_ab| rho_ax|
+  // (multiply by the unit phase u), and  s_ab s_bx / lambda = c (|s_ab| / lambda).
+  // s_bx itself then leaves the loop; 3 FP64 ops per slot-iteration fewer.
+  const double kap = sqrt(s2);
+  const double2 uph = kap > 0.0 ? make_double2(sab.x / kap, sab.y / kap) : make_double2(1.0, 0.0);
+  const CT uT = to_c(uph, T());
+  const T kapT = static_cast<T>(kap);
+  T ilcT = static_cast<T>(il * kap);
   const T s2T = static_cast<T>(s2);
   T ilT = static_cast<T>(il);
 
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   // txx and dd are pre-scaled by 1/M (exact for M = 2, 4, 8, 16).
   constexpr int SR = SMEMC ? 1 : SPT;  // register copies of the constants
   T rh[SPT], ru[SPT], txx[SR], dd[SR];
-  CT rax[SPT], tax[SR], cc[SR], sbx[SPT];
+  CT rax[SPT], tax[SR], cc[SR];
   bool valid[SPT];
   const T invMT = static_cast<T>(inv_M);
 #pragma unroll
@@ -193,25 +201,25 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
     valid[k] = FULL || t < t_end;
     const int64_t s = base + (valid[k] ? t : t0);
-    CT tk;
+    CT tk, sb;
     T xk;
     if constexpr (F32) {
       rh[k] = P.r_h_f_in[s];
       ru[k] = P.r_u_f_in[s];
-      sbx[k] = P.sigma_bx_f[s];
+      sb = P.sigma_bx_f[s];
       tk = P.tau_ax_f[s];
       xk = P.tau_xx_f[s] * invMT;
     } else {
       rh[k] = P.r_h_in[s];
       ru[k] = P.r_u_in[s];
-      sbx[k] = P.sigma_bx[s];
+      sb = P.sigma_bx[s];
       tk = P.tau_ax[s];
       xk = P.tau_xx[s] * invMT;
     }
-    const CT ck = cmul(sabT, sbx[k]);     // sigma_ab * sigma_bx
-    const T dk = cnorm(sbx[k]) * invMT;   // |sigma_bx|^2 / M
-    rax[k].x = tfma(ck.x, ilT, tk.x);
-    rax[k].y = tfma(ck.y, ilT, tk.y);
+    const CT ck = cmul(uT, sb);      // u sigma_bx
+    const T dk = cnorm(sb) * invMT;  // |sigma_bx|^2 / M
+    rax[k].x = tfma(ck.x, ilcT, tk.x);
+    rax[k].y = tfma(ck.y, ilcT, tk.y);
     if constexpr (SMEMC) {
       s_tax[k * NT + tid] = tk;
       s_cc[k * NT + tid] = ck;
@@ -254,9 +262,15 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
       const T gk = tfma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
       const T iru = D * inv;                          // 1 / r~_u
       // resid = s_bx - gamma conj(s_ab) rho~_ax
-      const CT e = cmulc(sabT, rax[k]);
-      const T rx = tfma(-gk, e.x, sbx[k].x);
-      const T ry = tfma(-gk, e.y, sbx[k].y);
+      CT ck;
+      if constexpr (SMEMC) {
+        ck = s_cc[k * NT + tid];
+      } else {
+        ck = cc[k];
+      }
+      const T gs = gk * kapT;
+      const T rx = tfma(-gs, rax[k].x, ck.x);
+      const T ry = tfma(-gs, rax[k].y, ck.y);
       const T rr = tfma(rx, rx, ry * ry);
       // per-slot lambda term, independent across slots (no serial accumulator)
       term[k] = (FULL || valid[k]) ? tfma(gk, s2T, rr * iru) : T(0);
@@ -307,9 +321,9 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
       rh[k] = floor_eps(tfma(gq, k1, k2), epsT);
       const T m2g = g[k] * m2M;                                 // -2 gamma / M
       const T re0 = tfma(rax[k].x, tk.x, rax[k].y * tk.y);      // Re(rho~_ax conj tau_ax)
-      const T re1 = tfma(rax[k].x, ck.x, rax[k].y * ck.y);      // Re(rho~_ax conj(s_ab s_bx))
+      const T re1 = tfma(rax[k].x, ck.x, rax[k].y * ck.y);      // Re(rho~_ax conj(u s_bx))
       p0[k] = tfma(m2g, re0, tfma(gq, taaM, xk));
-      p1[k] = tfma(m2g, re1, tfma(gq, s2M, dk));
+      p1[k] = tfma(m2g * kapT, re1, tfma(gq, s2M, dk));         // s_ab s_bx = |s_ab| u s_bx
     }
     __syncthreads();
     double total = 0.0;
@@ -361,6 +375,7 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     il = rcp_pos(lam);
     raa = fma(s2, il, taa);
     ilT = static_cast<T>(il);
+    ilcT = static_cast<T>(il * kap);
     const T raaM = static_cast<T>(raa * inv_M);
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
@@ -382,8 +397,8 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
         }
       }
       CT nax;  // rho_ax with lambda_new
-      nax.x = tfma(ck.x, ilT, tk.x);
-      nax.y = tfma(ck.y, ilT, tk.y);
+      nax.x = tfma(ck.x, ilcT, tk.x);
+      nax.y = tfma(ck.y, ilcT, tk.y);
       if constexpr (DIRECT) {
         // solver_accel.hpp:167-173 with rho_xx / M = tau_xx/M + |s_bx|^2/M / lambda
         const T rxx = tfma(dk, ilT, xk);

@@ -130,21 +130,23 @@ __device__ __forceinline__ float tfma(float a, float b, float c) { return fmaf(a
 
 // FULL: every thread's SPT slots are inside the bin chunk (NT * SPT == chunk),
 // so no per-slot masks. TRAJ: record r_h / r_u / lambda after every iteration.
-// SMEMC: the four per-slot constants used only after the lambda reduction
+// SMEMC 1: the four per-slot constants used only after the lambda reduction
 // (tau_ax, u*s_bx, tau_xx/M, |s_bx|^2/M: 48 B/slot) live in dynamic shared
 // memory ([k][tid] planes, conflict-free) instead of registers, which roughly
 // halves the register footprint and doubles the resident warps per SM.
-// LB3: launch bounds of 128 threads x 3 CTAs/SM (<= 170 registers) instead of
-// one 256-thread CTA's worth, trading a little ILP for resident warps.
 // DIRECT: form r_u after the reduction from rho with the new lambda (8 FP64 ops
 // per slot, the reference's own order) instead of the affine P0 + P1/lambda
 // split (10 ops, but all but 3 of them overlap the reduction).
 // T: the per-slot arithmetic type -- double (complex128, reference-exact) or
 // float (the complex64 / FP32 mode); lambda, its reduction and the per-bin
 // scalars stay in double in both.
-template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false,
+// SMEMC 2: only tau_ax and (tau_xx, |s_bx|^2)/M in shared memory (32 B/slot);
+// u s_bx, read in both halves of the iteration, stays in registers.
+// MINB: launch bounds of 128 threads x MINB CTAs/SM (MINB = 3: <= 168
+// registers) instead of one 256-thread CTA's worth (0).
+template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
           typename T = double>
-__global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_accel(AccelArgs P) {
+__global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1)) k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
   using CT = typename CplxOf<T>::type;
   constexpr bool F32 = sizeof(T) == 4;
@@ -165,11 +167,12 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   const int64_t t_end = min(J, t0 + Jc);
   const int64_t base = bin * J;
   const double inv_M = P.inv_M;
-  // shared planes (SMEMC): tax[k][tid], cc[k][tid] (complex), txx[k][tid], dd[k][tid] (real)
+  // shared planes ([k][tid], conflict-free): tax, (txx, dd) packed, and for
+  // SMEMC 1 also cc
+  constexpr bool TX_SM = SMEMC >= 1, CC_SM = SMEMC == 1;
   CT* s_tax = reinterpret_cast<CT*>(dyn_raw);
-  CT* s_cc = s_tax + SPT * NT;
-  T* s_txx = reinterpret_cast<T*>(s_cc + SPT * NT);
-  T* s_dd = s_txx + SPT * NT;
+  CT* s_xd = s_tax + SPT * NT;
+  CT* s_cc = s_xd + SPT * NT;
 
   const double2 sab = P.sigma_ab[bin];
   const double s2 = cnorm(sab);  // |sigma_ab|^2
@@ -191,9 +194,19 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
 
   // per-slot state: rh, ru evolve; rax = rho~_ax carried; the rest is constant.
   // txx and dd are pre-scaled by 1/M (exact for M = 2, 4, 8, 16).
-  constexpr int SR = SMEMC ? 1 : SPT;  // register copies of the constants
-  T rh[SPT], ru[SPT], txx[SR], dd[SR];
-  CT rax[SPT], tax[SR], cc[SR];
+  constexpr int SR = TX_SM ? 1 : SPT, SC = CC_SM ? 1 : SPT;  // register copies of the constants
+  T rh[SPT], ru[SPT], txx[SR] = {}, dd[SR] = {};
+  CT rax[SPT], tax[SR] = {}, cc[SC] = {};
+  // constant accessors (registers or the shared planes)
+  auto get_cc = [&](int k) -> CT {
+    if constexpr (CC_SM) return s_cc[k * NT + tid]; else return cc[k];
+  };
+  auto get_tax = [&](int k) -> CT {
+    if constexpr (TX_SM) return s_tax[k * NT + tid]; else return tax[k];
+  };
+  auto get_xd = [&](int k) -> CT {  // (tau_xx / M, |s_bx|^2 / M)
+    if constexpr (TX_SM) return s_xd[k * NT + tid]; else { CT v; v.x = txx[k]; v.y = dd[k]; return v; }
+  };
   bool valid[SPT];
   const T invMT = static_cast<T>(inv_M);
 #pragma unroll
@@ -220,17 +233,18 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     const T dk = cnorm(sb) * invMT;  // |sigma_bx|^2 / M
     rax[k].x = tfma(ck.x, ilcT, tk.x);
     rax[k].y = tfma(ck.y, ilcT, tk.y);
-    if constexpr (SMEMC) {
+    if constexpr (TX_SM) {
       s_tax[k * NT + tid] = tk;
-      s_cc[k * NT + tid] = ck;
-      s_txx[k * NT + tid] = xk;
-      s_dd[k * NT + tid] = dk;
+      CT v;
+      v.x = xk;
+      v.y = dk;
+      s_xd[k * NT + tid] = v;
     } else {
       tax[k] = tk;
-      cc[k] = ck;
       txx[k] = xk;
       dd[k] = dk;
     }
+    if constexpr (CC_SM) s_cc[k * NT + tid] = ck; else cc[k] = ck;
   }
 
   if (tid < 2 * kMaxWarps) (&red[0][0])[tid] = 0.0;
@@ -249,6 +263,7 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
   const T taaM = static_cast<T>(taa * inv_M), s2M = static_cast<T>(s2 * inv_M);
   const T fault = static_cast<T>(P.gamma_fault);
   const T k1 = static_cast<T>(P.k1), k2 = static_cast<T>(P.k2), epsT = static_cast<T>(P.eps);
+#pragma unroll 2
   for (int it = 0; it < P.iters; ++it) {
     const int buf = it & 1;
     const T raaT = static_cast<T>(raa);
@@ -262,12 +277,7 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
       const T gk = tfma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
       const T iru = D * inv;                          // 1 / r~_u
       // resid = s_bx - gamma conj(s_ab) rho~_ax
-      CT ck;
-      if constexpr (SMEMC) {
-        ck = s_cc[k * NT + tid];
-      } else {
-        ck = cc[k];
-      }
+      const CT ck = get_cc(k);
       const T gs = gk * kapT;
       const T rx = tfma(-gs, rax[k].x, ck.x);
       const T ry = tfma(-gs, rax[k].y, ck.y);
@@ -303,19 +313,8 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
         p1[k] = g[k] * m2M;  // -2 gamma / M
         continue;
       }
-      CT tk, ck;
-      T xk, dk;
-      if constexpr (SMEMC) {
-        tk = s_tax[k * NT + tid];
-        ck = s_cc[k * NT + tid];
-        xk = s_txx[k * NT + tid];
-        dk = s_dd[k * NT + tid];
-      } else {
-        tk = tax[k];
-        ck = cc[k];
-        xk = txx[k];
-        dk = dd[k];
-      }
+      const CT tk = get_tax(k), ck = get_cc(k), xd = get_xd(k);
+      const T xk = xd.x, dk = xd.y;
       const T q = tfma(g[k], cnorm(rax[k]), ru[k]);
       const T gq = g[k] * q;
       rh[k] = floor_eps(tfma(gq, k1, k2), epsT);
@@ -379,29 +378,14 @@ __global__ void __launch_bounds__(LB3 ? 128 : 256, LB3 ? 3 : (SMEMC ? 2 : 1)) k_
     const T raaM = static_cast<T>(raa * inv_M);
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      CT tk, ck;
-      T xk = T(0), dk = T(0);
-      if constexpr (SMEMC) {
-        tk = s_tax[k * NT + tid];
-        ck = s_cc[k * NT + tid];
-        if constexpr (DIRECT) {
-          xk = s_txx[k * NT + tid];
-          dk = s_dd[k * NT + tid];
-        }
-      } else {
-        tk = tax[k];
-        ck = cc[k];
-        if constexpr (DIRECT) {
-          xk = txx[k];
-          dk = dd[k];
-        }
-      }
+      const CT tk = get_tax(k), ck = get_cc(k);
       CT nax;  // rho_ax with lambda_new
       nax.x = tfma(ck.x, ilcT, tk.x);
       nax.y = tfma(ck.y, ilcT, tk.y);
       if constexpr (DIRECT) {
         // solver_accel.hpp:167-173 with rho_xx / M = tau_xx/M + |s_bx|^2/M / lambda
-        const T rxx = tfma(dk, ilT, xk);
+        const CT xd = get_xd(k);
+        const T rxx = tfma(xd.y, ilT, xd.x);
         const T re = tfma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
         ru[k] = floor_eps(tfma(p1[k], re, tfma(p0[k], raaM, rxx)), epsT);
       } else {

@@ -6,7 +6,7 @@
 namespace rcscm {
 
 AccelCfg choose_accel_cfg(int64_t J, bool f32) {
-  AccelCfg best{0, 0, 0, false, false, false, false, f32};
+  AccelCfg best{0, 0, 0, false, 0, 0, false, f32};
   const char* e_dir = std::getenv("RCSCM_ACCEL_DIRECT");
   const bool direct = e_dir ? std::atoi(e_dir) != 0 : true;  // measured faster (B200)
   const char* e_spt = std::getenv("RCSCM_ACCEL_SPT");
@@ -15,8 +15,10 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
   // -1: per-configuration default (shared-memory constants for clusters, where
   // the cluster barrier needs more resident CTAs to hide; measured on B200)
   const int smem_env = e_sm ? std::atoi(e_sm) : -1;
-  const char* e_lb = std::getenv("RCSCM_ACCEL_LB3");
-  const bool lb3 = e_lb ? std::atoi(e_lb) != 0 : true;  // measured faster (B200, configs 0/1/3)
+  // MINB: CTAs per SM the 128-thread launch bounds target (0 = 256-thread bounds);
+  // 3 measured fastest with register-resident constants (B200, configs 0/1/3)
+  const char* e_mb = std::getenv("RCSCM_ACCEL_MINB");
+  const int minb_env = e_mb ? std::atoi(e_mb) : -1;
   const int force_spt = e_spt ? std::atoi(e_spt) : 0;
   const int force_cl = e_cl ? std::atoi(e_cl) : 0;
   for (int cl : {1, 2, 4, 8, 16}) {
@@ -37,8 +39,9 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
         best_waste = waste;
         // FULL needs every CTA of the cluster to own exactly nt * spt frames
         const bool full = (waste == 0) && (jc * cl == J);
-        const bool smem = smem_env >= 0 ? smem_env != 0 : cl > 1;
-        best = AccelCfg{cl, static_cast<int>(nt), spt, full, f32 ? false : smem, lb3, direct, f32};
+        const int smem = smem_env >= 0 ? smem_env : (cl > 1 ? 1 : 0);
+        const int minb = minb_env >= 0 ? minb_env : (smem == 0 ? 3 : 4);
+        best = AccelCfg{cl, static_cast<int>(nt), spt, full, f32 ? 0 : smem, minb, direct, f32};
       }
     }
     if (best.cl) return best;

@@ -6,14 +6,15 @@
 
 namespace rcscm {
 
-template <int SPT, int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false,
+template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
           typename T = double>
 cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
-  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>;
+  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);
-  cfg.dynamicSmemBytes = SMEMC ? static_cast<size_t>(SPT) * nt * 6 * sizeof(T) : 0;
+  // shared planes: tax + (txx, dd) [+ cc for SMEMC 1], one complex each per slot
+  cfg.dynamicSmemBytes = SMEMC ? static_cast<size_t>(SPT) * nt * (SMEMC == 1 ? 6 : 4) * sizeof(T) : 0;
   if (SMEMC) {  // opt in to the full dynamic allowance (static + dynamic may pass 48 KB)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(cfg.dynamicSmemBytes));
@@ -37,16 +38,16 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
   return cudaLaunchKernelEx(&cfg, kern, A);
 }
 
-template <int CL, bool FULL, bool TRAJ, bool SMEMC, bool LB3 = false, bool DIRECT = false, typename T = double>
+template <int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false, typename T = double>
 cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt) {
   switch (spt) {
-    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
-    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
-    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
-    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
-    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
-    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
-    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, LB3, DIRECT, T>(s, A, nt);
+    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
+    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
+    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
+    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
+    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
+    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
+    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -56,24 +57,27 @@ cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& 
   const bool traj = A.traj_r_h != nullptr;
   if (g.f32) {  // complex64 mode: direct form, registers only
     if constexpr (CL == 1) {
-      if (g.full && g.nt <= 128) return launch_accel_spt<CL, true, false, false, true, true, float>(s, A, g.nt, g.spt);
+      if (g.full && g.minb && g.nt <= 128) return launch_accel_spt<CL, true, false, 0, 3, true, float>(s, A, g.nt, g.spt);
     }
-    if (g.full) return launch_accel_spt<CL, true, false, false, false, true, float>(s, A, g.nt, g.spt);
-    return launch_accel_spt<CL, false, false, false, false, true, float>(s, A, g.nt, g.spt);
+    if (g.full) return launch_accel_spt<CL, true, false, 0, 0, true, float>(s, A, g.nt, g.spt);
+    return launch_accel_spt<CL, false, false, 0, 0, true, float>(s, A, g.nt, g.spt);
   }
-  if (traj) return launch_accel_spt<CL, false, true, false>(s, A, g.nt, g.spt);
-  if (g.smem) {
-    if (g.full) return launch_accel_spt<CL, true, false, true>(s, A, g.nt, g.spt);
-    return launch_accel_spt<CL, false, false, true>(s, A, g.nt, g.spt);
-  }
+  if (traj) return launch_accel_spt<CL, false, true, 0>(s, A, g.nt, g.spt);
   if constexpr (CL == 1) {
-    if (g.full && g.lb3 && g.nt <= 128) {
-      if (g.direct) return launch_accel_spt<CL, true, false, false, true, true>(s, A, g.nt, g.spt);
-      return launch_accel_spt<CL, true, false, false, true>(s, A, g.nt, g.spt);
+    // 128-thread CTAs, several per SM: the tuned single-CTA-per-bin variants
+    if (g.full && g.minb && g.nt <= 128 && g.direct) {
+      if (g.smem == 2 && g.minb == 4) return launch_accel_spt<CL, true, false, 2, 4, true>(s, A, g.nt, g.spt);
+      if (g.smem == 1 && g.minb == 4) return launch_accel_spt<CL, true, false, 1, 4, true>(s, A, g.nt, g.spt);
+      if (g.smem == 2 && g.minb == 5) return launch_accel_spt<CL, true, false, 2, 5, true>(s, A, g.nt, g.spt);
+      if (g.smem == 0) return launch_accel_spt<CL, true, false, 0, 3, true>(s, A, g.nt, g.spt);
     }
   }
-  if (g.full) return launch_accel_spt<CL, true, false, false>(s, A, g.nt, g.spt);
-  return launch_accel_spt<CL, false, false, false>(s, A, g.nt, g.spt);
+  if (g.smem) {
+    if (g.full) return launch_accel_spt<CL, true, false, 1>(s, A, g.nt, g.spt);
+    return launch_accel_spt<CL, false, false, 1>(s, A, g.nt, g.spt);
+  }
+  if (g.full) return launch_accel_spt<CL, true, false, 0>(s, A, g.nt, g.spt);
+  return launch_accel_spt<CL, false, false, 0>(s, A, g.nt, g.spt);
 }
 
 #define RCSCM_DECLARE_ACCEL_CL(CL) \

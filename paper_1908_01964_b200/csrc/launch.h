@@ -28,13 +28,13 @@ cudaError_t launch_slots(cudaStream_t s, const DevProblem& P, bool init, bool pr
 struct AccelCfg {
   int cl, nt, spt;
   bool full;  // nt * spt == chunk: no per-slot masks
-  bool smem;  // phase-B constants in shared memory (k_accel SMEMC)
-  bool lb3;   // 128-thread x 3-CTA launch bounds (k_accel LB3), CL == 1 and nt <= 128 only
-  bool direct;  // r_u from rho(lambda_new) after the reduction (k_accel DIRECT), LB3 path only
+  int smem;   // per-slot constants in shared memory (k_accel SMEMC: 0 none, 1 all, 2 tax/txx/dd)
+  int minb;   // 128-thread x minb-CTA launch bounds (k_accel MINB), CL == 1 and nt <= 128 only
+  bool direct;  // r_u from rho(lambda_new) after the reduction (k_accel DIRECT), MINB path only
   bool f32;     // complex64 / FP32 per-slot arithmetic
 };
 // Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL /
-// RCSCM_ACCEL_SMEM force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
+// RCSCM_ACCEL_SMEM / RCSCM_ACCEL_MINB force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
 AccelCfg choose_accel_cfg(int64_t J, bool f32 = false);
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg);
 

@@ -35,6 +35,8 @@
 
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace rcscm {
@@ -180,18 +182,21 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
   double lam = P.lambda_in[bin];
   double il = 1.0 / lam;
   double raa = fma(s2, il, taa);  // rho_aa (solver_accel.hpp:122)
-  // Rotated residual: with u = s_ab / |s_ab| (1 when s_ab = 0) and the per-slot
-  // constant c = u s_bx,  |s_bx - g conj(s_ab) rho_ax| = |c - g |s_ab| rho_ax|
-  // (multiply by the unit phase u), and  s_ab s_bx / lambda = c (|s_ab| / lambda).
-  // s_bx itself then leaves the loop; 3 FP64 ops per slot-iteration fewer.
-  const double kap = sqrt(s2);
-  const double2 uph = kap > 0.0 ? make_double2(sab.x / kap, sab.y / kap) : make_double2(1.0, 0.0);
-  const CT uT = to_c(uph, T());
-  const T kapT = static_cast<T>(kap);
-  T ilcT = static_cast<T>(il * kap);
+  // Scaled residual: with the per-slot constant c = s_ab s_bx / |s_ab|^2 (s_bx
+  // itself when s_ab = 0),
+  //   |s_bx - g conj(s_ab) rho_ax|^2 = |s_ab|^2 |c - g rho_ax|^2   and
+  //   s_ab s_bx / lambda = c (|s_ab|^2 / lambda),
+  // so |s_ab|^2 leaves the per-slot lambda term and multiplies the bin total:
+  //   lambda = (|s_ab|^2 / J) sum_t [g + |c - g rho_ax|^2 / r~_u].
+  // Two FP64 ops per slot-iteration fewer than the literal form. Bins with
+  // s_ab = 0 (a orthogonal to b) take the literal form: residual s_bx, term
+  // |s_bx|^2 / r~_u (the branch is uniform per CTA).
+  const bool scaled = s2 > 0.0;
+  const double cs = scaled ? 1.0 / s2 : 0.0;
+  const CT sabT = to_c(scaled ? make_double2(sab.x * cs, sab.y * cs) : make_double2(1.0, 0.0), T());
+  T ilcT = static_cast<T>(il * s2);  // |s_ab|^2 / lambda
   const T s2T = static_cast<T>(s2);
   T ilT = static_cast<T>(il);
-
   // per-slot state: rh, ru evolve; rax = rho~_ax carried; the rest is constant.
   // txx and dd are pre-scaled by 1/M (exact for M = 2, 4, 8, 16).
   constexpr int SR = TX_SM ? 1 : SPT, SC = CC_SM ? 1 : SPT;  // register copies of the constants
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
       tk = P.tau_ax[s];
       xk = P.tau_xx[s] * invMT;
     }
-    const CT ck = cmul(uT, sb);      // u sigma_bx
+    const CT ck = cmul(sabT, sb);    // c = s_ab s_bx / |s_ab|^2
     const T dk = cnorm(sb) * invMT;  // |sigma_bx|^2 / M
     rax[k].x = tfma(ck.x, ilcT, tk.x);
     rax[k].y = tfma(ck.y, ilcT, tk.y);
@@ -263,149 +268,163 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
   const T taaM = static_cast<T>(taa * inv_M), s2M = static_cast<T>(s2 * inv_M);
   const T fault = static_cast<T>(P.gamma_fault);
   const T k1 = static_cast<T>(P.k1), k2 = static_cast<T>(P.k2), epsT = static_cast<T>(P.eps);
-#pragma unroll 2
-  for (int it = 0; it < P.iters; ++it) {
-    const int buf = it & 1;
-    const T raaT = static_cast<T>(raa);
-    // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
-    //     (solver_accel.hpp:67-76, :143-158).
-    T g[SPT], term[SPT];
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const T D = tfma(rh[k], raaT, ru[k]);  // r~_u + r~_h rho~_aa
-      const T inv = rcp_pos(D * ru[k]);
-      const T gk = tfma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
-      const T iru = D * inv;                          // 1 / r~_u
-      // resid = s_bx - gamma conj(s_ab) rho~_ax
-      const CT ck = get_cc(k);
-      const T gs = gk * kapT;
-      const T rx = tfma(-gs, rax[k].x, ck.x);
-      const T ry = tfma(-gs, rax[k].y, ck.y);
-      const T rr = tfma(rx, rx, ry * ry);
-      // per-slot lambda term, independent across slots (no serial accumulator)
-      term[k] = (FULL || valid[k]) ? tfma(gk, s2T, rr * iru) : T(0);
-      g[k] = gk;
-    }
-    // fixed pairwise tree over the thread's slots, then the warp total (FP64)
-#pragma unroll
-    for (int w = 1; w < SPT; w <<= 1) {
-#pragma unroll
-      for (int k = 0; k + w < SPT; k += 2 * w) term[k] += term[k + w];
-    }
-    const double part = warp_total_mma(static_cast<double>(term[0]), lane);
-    if (lane == 0) red[buf][warp] = part;
-    // (2) everything that does not need the new lambda, overlapping the
-    //     reduction: r_h (solver_accel.hpp:134-141) and (non-DIRECT) the two
-    //     halves of the r_u update, which is affine in 1/lambda_new
-    //     (:160-176 with :121-127):
-    //       M r_u = P0 + P1 / lambda_new,
-    //       P0 = g q tau_aa + tau_xx - 2 g Re(rho~_ax conj tau_ax)
-    //       P1 = g q |s_ab|^2 + |s_bx|^2 - 2 g Re(rho~_ax conj(s_ab s_bx))
-    //     (stored pre-scaled by 1/M; q = r~_u + g |rho~_ax|^2).
-    T p0[SPT], p1[SPT];
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      if constexpr (DIRECT) {
+  // Lambda's scale: |s_ab|^2 / J on the scaled path, 1 / J on the literal one.
+  const double il_eps = rcp_pos(P.eps);
+  const double s2_M = s2 * inv_M, taa_M = taa * inv_M;
+  auto run = [&](auto sc_tag) {
+    constexpr bool SCL = decltype(sc_tag)::value;
+    const double lsc = SCL ? s2 * invJ : invJ;
+  #pragma unroll 2
+    for (int it = 0; it < P.iters; ++it) {
+      const int buf = it & 1;
+      const T raaT = static_cast<T>(raa);
+      // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
+      //     (solver_accel.hpp:67-76, :143-158).
+      T g[SPT], term[SPT];
+  #pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        const T D = tfma(rh[k], raaT, ru[k]);  // r~_u + r~_h rho~_aa
+        const T inv = rcp_pos(D * ru[k]);
+        const T gk = tfma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
+        const T iru = D * inv;                          // 1 / r~_u
+        // resid = s_bx - gamma conj(s_ab) rho~_ax
+        // scaled residual c - g rho~_ax (s_bx itself when s_ab = 0)
+        const CT ck = get_cc(k);
+        const T rx = SCL ? tfma(-gk, rax[k].x, ck.x) : ck.x;
+        const T ry = SCL ? tfma(-gk, rax[k].y, ck.y) : ck.y;
+        const T rr = tfma(rx, rx, ry * ry);
+        // per-slot lambda term, independent across slots (no serial accumulator)
+        term[k] = (FULL || valid[k]) ? (SCL ? tfma(rr, iru, gk) : rr * iru) : T(0);
+        g[k] = gk;
+      }
+      // fixed pairwise tree over the thread's slots, then the warp total (FP64)
+  #pragma unroll
+      for (int w = 1; w < SPT; w <<= 1) {
+  #pragma unroll
+        for (int k = 0; k + w < SPT; k += 2 * w) term[k] += term[k + w];
+      }
+      const double part = warp_total_mma(static_cast<double>(term[0]), lane);
+      if (lane == 0) red[buf][warp] = part;
+      // (2) everything that does not need the new lambda, overlapping the
+      //     reduction: r_h (solver_accel.hpp:134-141) and (non-DIRECT) the two
+      //     halves of the r_u update, which is affine in 1/lambda_new
+      //     (:160-176 with :121-127):
+      //       M r_u = P0 + P1 / lambda_new,
+      //       P0 = g q tau_aa + tau_xx - 2 g Re(rho~_ax conj tau_ax)
+      //       P1 = g q |s_ab|^2 + |s_bx|^2 - 2 g Re(rho~_ax conj(s_ab s_bx))
+      //     (stored pre-scaled by 1/M; q = r~_u + g |rho~_ax|^2).
+      T p0[SPT], p1[SPT];
+  #pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        if constexpr (DIRECT) {
+          const T q = tfma(g[k], cnorm(rax[k]), ru[k]);
+          const T gq = g[k] * q;
+          rh[k] = floor_eps(tfma(gq, k1, k2), epsT);
+          p0[k] = gq;          // gamma q
+          p1[k] = g[k] * m2M;  // -2 gamma / M
+          continue;
+        }
+        const CT tk = get_tax(k), ck = get_cc(k), xd = get_xd(k);
+        const T xk = xd.x, dk = xd.y;
         const T q = tfma(g[k], cnorm(rax[k]), ru[k]);
         const T gq = g[k] * q;
         rh[k] = floor_eps(tfma(gq, k1, k2), epsT);
-        p0[k] = gq;          // gamma q
-        p1[k] = g[k] * m2M;  // -2 gamma / M
-        continue;
+        const T m2g = g[k] * m2M;                                 // -2 gamma / M
+        const T re0 = tfma(rax[k].x, tk.x, rax[k].y * tk.y);      // Re(rho~_ax conj tau_ax)
+        const T re1 = tfma(rax[k].x, ck.x, rax[k].y * ck.y);      // Re(rho~_ax conj c)
+        p0[k] = tfma(m2g, re0, tfma(gq, taaM, xk));
+        p1[k] = tfma(m2g * s2T, re1, tfma(gq, s2M, dk));          // s_ab s_bx = |s_ab|^2 c
       }
-      const CT tk = get_tax(k), ck = get_cc(k), xd = get_xd(k);
-      const T xk = xd.x, dk = xd.y;
-      const T q = tfma(g[k], cnorm(rax[k]), ru[k]);
-      const T gq = g[k] * q;
-      rh[k] = floor_eps(tfma(gq, k1, k2), epsT);
-      const T m2g = g[k] * m2M;                                 // -2 gamma / M
-      const T re0 = tfma(rax[k].x, tk.x, rax[k].y * tk.y);      // Re(rho~_ax conj tau_ax)
-      const T re1 = tfma(rax[k].x, ck.x, rax[k].y * ck.y);      // Re(rho~_ax conj(u s_bx))
-      p0[k] = tfma(m2g, re0, tfma(gq, taaM, xk));
-      p1[k] = tfma(m2g * kapT, re1, tfma(gq, s2M, dk));         // s_ab s_bx = |s_ab| u s_bx
-    }
-    __syncthreads();
-    double total = 0.0;
-    if constexpr (CL == 1) {
-      total = NT <= 128 ? block_total4(red[buf]) : block_total8(red[buf]);
-    } else {
-      // CTA partial -> cluster: lanes r < CL of warp 0 store this CTA's partial
-      // into cl_vals[buf][rank] of CTA r (st.shared::cluster) and arrive on its
-      // cl_bar[buf] with release semantics; every thread then waits on the local
-      // barrier (acquire) and sums the CL partials in rank order -- the same
-      // fixed tree in every CTA. One DSMEM write latency instead of a
-      // cluster-wide barrier plus a remote read.
-      const double c = block_total8(red[buf]);
-      if (warp == 0 && lane < CL) {
-        const unsigned lv = static_cast<unsigned>(__cvta_generic_to_shared(&cl_vals[buf][rank]));
-        const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
-        unsigned rv, rb;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rv) : "r"(lv), "r"(lane));
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(lane));
-        asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rv), "d"(c) : "memory");
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
-      }
-      {
-        const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
-        const unsigned parity = static_cast<unsigned>((it >> 1) & 1);
-        unsigned done = 0;
-        while (!done) {
-          asm volatile(
-              "{\n .reg .pred p;\n"
-              " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-              " selp.u32 %0, 1, 0, p;\n}"
-              : "=r"(done)
-              : "r"(lb), "r"(parity)
-              : "memory");
-        }
-      }
-      double v[CL];
-#pragma unroll
-      for (int r = 0; r < CL; ++r) v[r] = cl_vals[buf][r];
-#pragma unroll
-      for (int w = 1; w < CL; w <<= 1) {
-#pragma unroll
-        for (int r = 0; r + w < CL; r += 2 * w) v[r] += v[r + w];
-      }
-      total = v[0];
-    }
-    // (3) the short tail that needs lambda_new
-    lam = floor_eps(total * invJ, P.eps);
-    il = rcp_pos(lam);
-    raa = fma(s2, il, taa);
-    ilT = static_cast<T>(il);
-    ilcT = static_cast<T>(il * kap);
-    const T raaM = static_cast<T>(raa * inv_M);
-#pragma unroll
-    for (int k = 0; k < SPT; ++k) {
-      const CT tk = get_tax(k), ck = get_cc(k);
-      CT nax;  // rho_ax with lambda_new
-      nax.x = tfma(ck.x, ilcT, tk.x);
-      nax.y = tfma(ck.y, ilcT, tk.y);
-      if constexpr (DIRECT) {
-        // solver_accel.hpp:167-173 with rho_xx / M = tau_xx/M + |s_bx|^2/M / lambda
-        const CT xd = get_xd(k);
-        const T rxx = tfma(xd.y, ilT, xd.x);
-        const T re = tfma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
-        ru[k] = floor_eps(tfma(p1[k], re, tfma(p0[k], raaM, rxx)), epsT);
+      __syncthreads();
+      double total = 0.0;
+      if constexpr (CL == 1) {
+        total = NT <= 128 ? block_total4(red[buf]) : block_total8(red[buf]);
       } else {
-        ru[k] = floor_eps(tfma(p1[k], ilT, p0[k]), epsT);
-      }
-      rax[k] = nax;
-    }
-    if constexpr (TRAJ) {
-#pragma unroll
-      for (int k = 0; k < SPT; ++k) {
-        if (valid[k]) {
-          const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
-          const int64_t o = static_cast<int64_t>(it) * P.nb * J + base + t;
-          P.traj_r_h[o] = rh[k];
-          P.traj_r_u[o] = ru[k];
+        // CTA partial -> cluster: lanes r < CL of warp 0 store this CTA's partial
+        // into cl_vals[buf][rank] of CTA r (st.shared::cluster) and arrive on its
+        // cl_bar[buf] with release semantics; every thread then waits on the local
+        // barrier (acquire) and sums the CL partials in rank order -- the same
+        // fixed tree in every CTA. One DSMEM write latency instead of a
+        // cluster-wide barrier plus a remote read.
+        const double c = block_total8(red[buf]);
+        if (warp == 0 && lane < CL) {
+          const unsigned lv = static_cast<unsigned>(__cvta_generic_to_shared(&cl_vals[buf][rank]));
+          const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
+          unsigned rv, rb;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rv) : "r"(lv), "r"(lane));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(lane));
+          asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rv), "d"(c) : "memory");
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
         }
+        {
+          const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
+          const unsigned parity = static_cast<unsigned>((it >> 1) & 1);
+          unsigned done = 0;
+          while (!done) {
+            asm volatile(
+                "{\n .reg .pred p;\n"
+                " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+                " selp.u32 %0, 1, 0, p;\n}"
+                : "=r"(done)
+                : "r"(lb), "r"(parity)
+                : "memory");
+          }
+        }
+        double v[CL];
+  #pragma unroll
+        for (int r = 0; r < CL; ++r) v[r] = cl_vals[buf][r];
+  #pragma unroll
+        for (int w = 1; w < CL; w <<= 1) {
+  #pragma unroll
+          for (int r = 0; r + w < CL; r += 2 * w) v[r] += v[r + w];
+        }
+        total = v[0];
       }
-      if (rank == 0 && tid == 0) P.traj_lambda[static_cast<int64_t>(it) * P.nb + bin] = lam;
+      // (3) the short tail that needs lambda_new
+      // lambda = max(total * scale, eps); its reciprocal is formed speculatively
+      // from the unfloored value and replaced by 1/eps when the floor applies,
+      // so the floor is off the critical path (same values as rcp(floor)).
+      const double lraw = total * lsc;
+      const double ilr = rcp_pos(lraw);
+      const bool fl = __double_as_longlong(lraw) < __double_as_longlong(P.eps);
+      lam = fl ? P.eps : lraw;
+      il = fl ? il_eps : ilr;
+      raa = fma(s2, il, taa);
+      ilT = static_cast<T>(il);
+      ilcT = static_cast<T>(il * s2);
+      const T raaM = static_cast<T>(fma(s2_M, il, taa_M));  // rho_aa / M (exact scaling for 2^k M)
+  #pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        const CT tk = get_tax(k), ck = get_cc(k);
+        CT nax;  // rho_ax with lambda_new
+        nax.x = tfma(ck.x, ilcT, tk.x);
+        nax.y = tfma(ck.y, ilcT, tk.y);
+        if constexpr (DIRECT) {
+          // solver_accel.hpp:167-173 with rho_xx / M = tau_xx/M + |s_bx|^2/M / lambda
+          const CT xd = get_xd(k);
+          const T rxx = tfma(xd.y, ilT, xd.x);
+          const T re = tfma(rax[k].x, nax.x, rax[k].y * nax.y);  // Re(rho~_ax conj(rho_ax))
+          ru[k] = floor_eps(tfma(p1[k], re, tfma(p0[k], raaM, rxx)), epsT);
+        } else {
+          ru[k] = floor_eps(tfma(p1[k], ilT, p0[k]), epsT);
+        }
+        rax[k] = nax;
+      }
+      if constexpr (TRAJ) {
+  #pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+          if (valid[k]) {
+            const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+            const int64_t o = static_cast<int64_t>(it) * P.nb * J + base + t;
+            P.traj_r_h[o] = rh[k];
+            P.traj_r_u[o] = ru[k];
+          }
+        }
+        if (rank == 0 && tid == 0) P.traj_lambda[static_cast<int64_t>(it) * P.nb + bin] = lam;
+      }
     }
-  }
+  };
+  if (scaled) run(std::integral_constant<bool, true>{}); else run(std::integral_constant<bool, false>{});
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
     if (valid[k]) {

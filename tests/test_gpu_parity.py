@@ -154,6 +154,30 @@ def test_iters_zero_passthrough(O, gpu):  # test_solver_accel.cpp:289-298, test_
         assert np.array_equal(r.r_h, p.r_h) and np.array_equal(r.r_u, p.r_u) and np.array_equal(r.lam, p.lam)
 
 
+@pytest.mark.parametrize("J", [16, 640])
+def test_sigma_ab_zero_bins(O, gpu, J):
+    """Bins whose b is orthogonal to a (sigma_ab = a^H b = 0) take K2's literal
+    lambda form (no |sigma_ab|^2 scaling); mixed with ordinary bins in one launch."""
+    import dataclasses
+
+    inp, p, X = O.make_verify_instance(6, J, 3, 4242 + J)
+    b = inp.b.copy()
+    for i in (1, 4):
+        a = inp.a[i]
+        v = b[i] - a * (np.vdot(a, b[i]) / np.vdot(a, a))  # remove the a component
+        b[i] = v / np.linalg.norm(v)
+    inp = dataclasses.replace(inp, b=b)
+    assert abs(np.vdot(inp.a[1], inp.b[1])) < 1e-15 and abs(np.vdot(inp.a[0], inp.b[0])) > 1e-3
+    for iters in (1, 20):
+        g = gpu.run_algorithm2(inp, p, _hyper(), X, _opts(iters=iters)).params
+        o = O.run("accel2", inp, p, X, O.SolverOptions(iters=iters)).params
+        if iters == 1:
+            r = check_params(g, o)
+            assert r["ok"], r
+        else:
+            assert O.trajectory_distance(g, o) <= 1e-8
+
+
 def test_rh_zero_collapse(O, gpu):  # test_solver_naive.cpp:60-65 / test_wiener.cpp:9-15
     inp, p, X = O.make_verify_instance(2, 6, 3, 1)
     p.r_h[:] = 0

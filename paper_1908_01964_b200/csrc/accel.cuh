@@ -84,13 +84,15 @@ __device__ __forceinline__ double floor_eps(double v, double eps) {
   return __longlong_as_double(iv < ie ? ie : iv);
 }
 
-// Sum of the 32 lanes' values, returned in every lane, on the FP64 tensor
-// core: DMMA m8n8k4 with B = 1 leaves in lane l the sum of its 4-lane group
-// g_{l/4}; one shuffle round transposes the 8 group sums into the k index and
-// two more DMMAs (B = 1) add them. ~90 cycles of latency on B200 against
-// ~180 for a 5-step shuffle butterfly (measured: DMMA 26, SHFL.f64+DADD 36).
-// Multiplications by 1 are exact and the DMMA's internal order is fixed, so
-// the result is deterministic and identical in every lane.
+// Sum of the 32 lanes' values, returned in every lane: one DMMA m8n8k4 with
+// B = 1 leaves in lane l the sum of its 4-lane group (fixed internal order;
+// multiplications by 1 are exact), then a 3-level xor butterfly over the 8
+// group sums. Every lane ends with the same bits: each butterfly level adds
+// the same two operands in both partner lanes and IEEE addition commutes.
+// Measured on B200 at 3 CTAs/SM (tools/k2_probe.cu): 4 % faster per launch
+// than the all-DMMA tree (DMMA, shuffle transpose, two DMMAs), whose three
+// tensor-pipe ops per warp-iteration contend under load, and than a 5-level
+// shuffle butterfly (longer latency).
 __device__ __forceinline__ double dmma_ones(double a) {
   double d0;
   [[maybe_unused]] double d1;
@@ -99,12 +101,11 @@ __device__ __forceinline__ double dmma_ones(double a) {
       : "d"(a), "d"(1.0), "d"(0.0), "d"(0.0));
   return d0;
 }
-__device__ __forceinline__ double warp_total_mma(double v, int lane) {
-  const double g = dmma_ones(v);  // lane l: sum of lanes 4*(l/4) .. +3
-  const int src = (lane & 3) << 2;
-  const double lo = __shfl_sync(0xffffffffu, g, src);       // g_{l%4}
-  const double hi = __shfl_sync(0xffffffffu, g, src + 16);  // g_{l%4 + 4}
-  return dmma_ones(lo) + dmma_ones(hi);
+__device__ __forceinline__ double warp_total(double v) {
+  double s = dmma_ones(v);  // lane l: sum of lanes 4*(l/4) .. +3
+#pragma unroll
+  for (int m = 4; m < 32; m <<= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  return s;
 }
 
 // Sum of the (zero-padded) first 4 per-warp partials (CTAs of <= 128 threads).
@@ -121,6 +122,21 @@ __device__ __forceinline__ double block_total8(const double* red) {
   const double2 a = r[0], b = r[1], c = r[2], d = r[3];
   return ((a.x + a.y) + (b.x + b.y)) + ((c.x + c.y) + (d.x + d.y));
 }
+
+// Development probe (tools/k2_probe.cu): per-phase clock64 stamps of lane 0 of
+// every warp for the first 16 iterations. Compiled out of the library.
+#ifdef RCSCM_K2_PROBE
+__device__ long long* g_k2_probe;
+#define K2_PROBE(idx, dep)                                                                              \
+  do {                                                                                                  \
+    asm volatile("" ::"d"(static_cast<double>(dep)));                                                  \
+    if (lane == 0 && it < 16) g_k2_probe[((blockIdx.x * 8 + warp) * 16 + it) * 8 + (idx)] = clock64(); \
+  } while (0)
+#else
+#define K2_PROBE(idx, dep) \
+  do {                     \
+  } while (0)
+#endif
 
 // FP32-mode counterpart of floor_eps (32-bit compare of the bit patterns).
 __device__ __forceinline__ float floor_eps(float v, float eps) {
@@ -268,20 +284,20 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
   const T taaM = static_cast<T>(taa * inv_M), s2M = static_cast<T>(s2 * inv_M);
   const T fault = static_cast<T>(P.gamma_fault);
   const T k1 = static_cast<T>(P.k1), k2 = static_cast<T>(P.k2), epsT = static_cast<T>(P.eps);
-  // Lambda's scale: |s_ab|^2 / J on the scaled path, 1 / J on the literal one.
+  // 1/lambda when the eps floor applies
   const double il_eps = rcp_pos(P.eps);
-  const double s2_M = s2 * inv_M, taa_M = taa * inv_M;
+  const double taa_M = taa * inv_M;
   auto run = [&](auto sc_tag) {
     constexpr bool SCL = decltype(sc_tag)::value;
-    const double lsc = SCL ? s2 * invJ : invJ;
-  #pragma unroll 2
+#pragma unroll 2
     for (int it = 0; it < P.iters; ++it) {
       const int buf = it & 1;
+      K2_PROBE(0, rh[0]);
       const T raaT = static_cast<T>(raa);
       // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
       //     (solver_accel.hpp:67-76, :143-158).
       T g[SPT], term[SPT];
-  #pragma unroll
+#pragma unroll
       for (int k = 0; k < SPT; ++k) {
         const T D = tfma(rh[k], raaT, ru[k]);  // r~_u + r~_h rho~_aa
         const T inv = rcp_pos(D * ru[k]);
@@ -298,12 +314,14 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
         g[k] = gk;
       }
       // fixed pairwise tree over the thread's slots, then the warp total (FP64)
-  #pragma unroll
+#pragma unroll
       for (int w = 1; w < SPT; w <<= 1) {
-  #pragma unroll
+#pragma unroll
         for (int k = 0; k + w < SPT; k += 2 * w) term[k] += term[k + w];
       }
-      const double part = warp_total_mma(static_cast<double>(term[0]), lane);
+      K2_PROBE(1, term[0]);
+      const double part = warp_total(static_cast<double>(term[0]));
+      K2_PROBE(2, part);
       if (lane == 0) red[buf][warp] = part;
       // (2) everything that does not need the new lambda, overlapping the
       //     reduction: r_h (solver_accel.hpp:134-141) and (non-DIRECT) the two
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
       //       P1 = g q |s_ab|^2 + |s_bx|^2 - 2 g Re(rho~_ax conj(s_ab s_bx))
       //     (stored pre-scaled by 1/M; q = r~_u + g |rho~_ax|^2).
       T p0[SPT], p1[SPT];
-  #pragma unroll
+#pragma unroll
       for (int k = 0; k < SPT; ++k) {
         if constexpr (DIRECT) {
           const T q = tfma(g[k], cnorm(rax[k]), ru[k]);
@@ -336,6 +354,7 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
         p1[k] = tfma(m2g * s2T, re1, tfma(gq, s2M, dk));          // s_ab s_bx = |s_ab|^2 c
       }
       __syncthreads();
+      K2_PROBE(3, 0.0);
       double total = 0.0;
       if constexpr (CL == 1) {
         total = NT <= 128 ? block_total4(red[buf]) : block_total8(red[buf]);
@@ -371,29 +390,33 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
           }
         }
         double v[CL];
-  #pragma unroll
+#pragma unroll
         for (int r = 0; r < CL; ++r) v[r] = cl_vals[buf][r];
-  #pragma unroll
+#pragma unroll
         for (int w = 1; w < CL; w <<= 1) {
-  #pragma unroll
+#pragma unroll
           for (int r = 0; r + w < CL; r += 2 * w) v[r] += v[r + w];
         }
         total = v[0];
       }
       // (3) the short tail that needs lambda_new
-      // lambda = max(total * scale, eps); its reciprocal is formed speculatively
-      // from the unfloored value and replaced by 1/eps when the floor applies,
-      // so the floor is off the critical path (same values as rcp(floor)).
-      const double lraw = total * lsc;
+      // lambda = max(total * scale, eps) (scale |s_ab|^2 / J, or 1 / J for
+      // s_ab = 0); its reciprocal is formed speculatively from the unfloored
+      // value and replaced by 1/eps when the floor applies, so the floor is off
+      // the critical path. (Taking |s_ab|^2/lambda = J/total directly from a
+      // reciprocal of total/J measured 1 % slower.)
+      const double lraw = total * (SCL ? s2 * invJ : invJ);
+      K2_PROBE(4, lraw);
       const double ilr = rcp_pos(lraw);
       const bool fl = __double_as_longlong(lraw) < __double_as_longlong(P.eps);
       lam = fl ? P.eps : lraw;
       il = fl ? il_eps : ilr;
-      raa = fma(s2, il, taa);
+      const double ilc = il * s2;
+      raa = taa + ilc;
       ilT = static_cast<T>(il);
-      ilcT = static_cast<T>(il * s2);
-      const T raaM = static_cast<T>(fma(s2_M, il, taa_M));  // rho_aa / M (exact scaling for 2^k M)
-  #pragma unroll
+      ilcT = static_cast<T>(ilc);
+      const T raaM = static_cast<T>(fma(ilc, inv_M, taa_M));  // rho_aa / M
+#pragma unroll
       for (int k = 0; k < SPT; ++k) {
         const CT tk = get_tax(k), ck = get_cc(k);
         CT nax;  // rho_ax with lambda_new
@@ -410,8 +433,9 @@ __global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1
         }
         rax[k] = nax;
       }
+      K2_PROBE(5, ru[0]);
       if constexpr (TRAJ) {
-  #pragma unroll
+#pragma unroll
         for (int k = 0; k < SPT; ++k) {
           if (valid[k]) {
             const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;

@@ -131,6 +131,11 @@ __device__ long long* g_k2_probe;
   do {                                                                                                  \
     asm volatile("" ::"d"(static_cast<double>(dep)));                                                  \
     if (lane == 0 && it < 16) g_k2_probe[((blockIdx.x * 8 + warp) * 16 + it) * 8 + (idx)] = clock64(); \
+    if ((idx) == 0 && lane == 0 && it == 0) {                                                           \
+      unsigned smid_;                                                                                   \
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid_));                                               \
+      g_k2_probe[((blockIdx.x * 8 + warp) * 16) * 8 + 7] = smid_;                                       \
+    }                                                                                                   \
   } while (0)
 #else
 #define K2_PROBE(idx, dep) \
@@ -164,7 +169,11 @@ __device__ __forceinline__ float tfma(float a, float b, float c) { return fmaf(a
 // registers) instead of one 256-thread CTA's worth (0).
 template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
           typename T = double>
-__global__ void __launch_bounds__(MINB ? 128 : 256, MINB ? MINB : (SMEMC ? 2 : 1)) k_accel(AccelArgs P) {
+#ifndef RCSCM_K2_LB_THREADS
+#define RCSCM_K2_LB_THREADS 128  // MINB launch-bounds CTA size (tools may override)
+#endif
+__global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB : (SMEMC ? 2 : 1))
+    k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
   using CT = typename CplxOf<T>::type;
   constexpr bool F32 = sizeof(T) == 4;

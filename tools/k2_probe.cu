@@ -56,18 +56,23 @@ int main(int argc, char** argv) {
 #ifdef RCSCM_K2_PROBE
     CK(cudaMemcpyToSymbol(g_k2_probe, &dprobe, sizeof(dprobe)));
 #endif
-    auto kern = k_accel<5, 1, true, false, 0, 3, true, double>;
+#ifndef K2_SPT
+#define K2_SPT 5
+#define K2_MINB 3
+#endif
+    const int nt = J / K2_SPT;
+    auto kern = k_accel<K2_SPT, 1, true, false, 0, K2_MINB, true, double>;
 #ifdef RCSCM_K2_STAGGER
     CK(cudaMemcpyToSymbol(g_k2_stagger, &st, sizeof(st)));
     std::vector<unsigned> zero(256, 0);
 #endif
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int r = 0; r < 3; ++r) kern<<<nb, 128>>>(A);
+    for (int r = 0; r < 3; ++r) kern<<<nb, nt>>>(A);
 #ifdef RCSCM_K2_STAGGER
     CK(cudaMemcpyToSymbol(g_k2_smcount, zero.data(), 256 * sizeof(unsigned)));
 #endif
     cudaEventRecord(e0);
-    kern<<<nb, 128>>>(A);
+    kern<<<nb, nt>>>(A);
     cudaEventRecord(e1);
     CK(cudaDeviceSynchronize());
     float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -83,6 +88,24 @@ int main(int argc, char** argv) {
           acc[5] += static_cast<double>(q[0] - p[5]);
           ++cnt;
         }
+    // phase relation of the CTAs sharing an SM: iteration-start stamps of warp 0
+    {
+      std::vector<std::vector<int>> by_sm(1024);
+      for (int b = 0; b < nb; ++b) by_sm[h[((static_cast<size_t>(b) * 8) * 16) * 8 + 7] & 1023].push_back(b);
+      int shown = 0;
+      for (int sm = 0; sm < 1024 && shown < 3; ++sm) {
+        if (by_sm[sm].size() < 2) continue;
+        ++shown;
+        printf("  sm %d:", sm);
+        const long long t00 = h[((static_cast<size_t>(by_sm[sm][0]) * 8) * 16 + 4) * 8];
+        for (int b : by_sm[sm]) {
+          printf(" [cta %d:", b);
+          for (int it = 4; it < 10; ++it) printf(" %lld", h[((static_cast<size_t>(b) * 8) * 16 + it) * 8] - t00);
+          printf("]");
+        }
+        printf("\n");
+      }
+    }
     double tot = 0;
     for (double& a : acc) { a /= cnt; tot += a; }
 #ifdef RCSCM_K2_STAGGER

@@ -9,7 +9,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librcscm_gpu.so")
+LIB_PATH = os.environ.get("RCSCM_GPU_LIB") or os.path.join(_HERE, "librcscm_gpu.so")  # env: A/B builds
 
 RCSCM_OK = 0
 RCSCM_INVALID_INPUT = 2

@@ -30,6 +30,23 @@ __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_dou
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cnorm(double2 a) { return fma(a.x, a.x, a.y * a.y); }
 
+// Launch shape of the slot-stream kernels (K1 precompute, K4 Wiener): each
+// thread owns SPT slots of one bin strided by the CTA size, a CTA covers one
+// chunk of a bin's frames. The chunk count is the fewest with <= 256 threads,
+// and the CTA size the smallest warp multiple covering the chunk, so a bin of
+// J frames wastes < 32 * SPT slots (J = 640, SPT = 4: one 160-thread CTA).
+struct SlotGrid {
+  int nt;
+  int64_t chunks;
+};
+inline SlotGrid slot_grid(int64_t J, int spt) {
+  const int64_t cap = static_cast<int64_t>(spt) * 256;
+  const int64_t chunks = J > 0 ? (J + cap - 1) / cap : 1;
+  const int64_t per = (J + chunks - 1) / chunks;
+  const int64_t nt = ((per + spt - 1) / spt + 31) / 32 * 32;
+  return SlotGrid{static_cast<int>(nt > 0 ? nt : 32), chunks};
+}
+
 // Reciprocal for strictly positive, normal x: MUFU.RCP64H seed refined by one
 // Newton step plus the cubic term (error ~ e0^3, far below 1 ulp for the
 // ~2^-22 seed). Replaces the IEEE division slow path in the on-chip loop.

@@ -381,6 +381,78 @@ __global__ void __launch_bounds__(NT) k_slots(DevProblem P, double eps) {
 
 namespace rcscm {
 
+// K1 (PRE): the per-slot quadratic forms of solver_accel.hpp:33-64 --
+// sigma_bx = b^H x, tau_ax = (R'^+ a)^H x, tau_xx = max(Re x^H R'^+ x, 0) -- and
+// the per-bin sigma_ab = a^H b, tau_aa = max(Re a^H R'^+ a, 0). One pass over x
+// (16 M B/slot read, 40 B/slot written). Each thread owns SPT slots (strided by
+// the CTA size, slot_grid) and issues all of its x loads before the per-bin
+// prologue (R'^+, b, R'^+ a into shared memory), so the prologue's dependent
+// loads and barrier overlap the stream instead of preceding it. Arithmetic order
+// is that of k_slots (bitwise-identical results).
+template <int M, int SPT>
+__global__ void __launch_bounds__(256) k_pre(DevProblem P) {
+  __shared__ double2 sRpp[M * M];
+  __shared__ double2 sb[M];
+  __shared__ double2 sp[M];  // R'^+ a
+  const int64_t bin = blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t J = P.J;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.y) * nt * SPT + tid;
+  double2 x[SPT][M];
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    const int64_t t = t0 + static_cast<int64_t>(k) * nt;
+    if (t < J) {
+      const double2* xp = P.X + (bin * J + t) * M;
+#pragma unroll
+      for (int m = 0; m < M; ++m) x[k][m] = __ldg(xp + m);
+    }
+  }
+  for (int k = tid; k < M * M; k += nt) sRpp[k] = P.Rpp[bin * M * M + k];
+  if (tid < M) {
+    sb[tid] = P.b[bin * M + tid];
+    double2 s = make_double2(0.0, 0.0);
+    for (int k = 0; k < M; ++k) s = cfma(P.Rpp[bin * M * M + tid + k * M], P.a[bin * M + k], s);
+    sp[tid] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    const int64_t t = t0 + static_cast<int64_t>(k) * nt;
+    if (t >= J) continue;
+    const int64_t slot = bin * J + t;
+    double2 sbx = make_double2(0.0, 0.0), tax = make_double2(0.0, 0.0);
+    double2 xx = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      sbx = cfmac(sb[r], x[k][r], sbx);
+      tax = cfmac(sp[r], x[k][r], tax);
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int q = 0; q < M; ++q) acc = cfma(sRpp[r + q * M], x[k][q], acc);
+      xx = cfmac(x[k][r], acc, xx);
+    }
+    P.sigma_bx[slot] = sbx;
+    P.tau_ax[slot] = tax;
+    P.tau_xx[slot] = fmax(xx.x, 0.0);
+  }
+  if (blockIdx.y == 0 && tid == 0) {
+    double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);
+    for (int k = 0; k < M; ++k) {
+      const double2 ak = P.a[bin * M + k];
+      ab = cfmac(ak, sb[k], ab);
+      aa = cfmac(ak, sp[k], aa);
+    }
+    P.sigma_ab[bin] = ab;
+    P.tau_aa[bin] = fmax(aa.x, 0.0);
+  }
+}
+// slots per thread of k_pre: 16 complex x values in registers
+template <int M>
+constexpr int pre_spt() {
+  return M >= 16 ? 1 : 16 / M;
+}
+
 // K1 in the complex64 (FP32) mode: sigma_bx, tau_ax, tau_xx in single precision
 // from the complex64 copy of x (solver_accel.hpp:33-64); the per-bin sigma_ab
 // and tau_aa stay in double (computed from the double a, b, R'^+ exactly as

@@ -44,13 +44,17 @@ cudaError_t launch_slots(cudaStream_t s, const DevProblem& P, bool init, bool pr
   if (P.nb * P.J == 0 || !(init || pre)) return cudaSuccess;
   return dispatch_mics(P.M, [&](auto mm) {
     constexpr int MM = decltype(mm)::value;
+    if (!init) {  // the precompute pass alone (every solve): k_pre
+      constexpr int SPT = pre_spt<MM>();
+      const SlotGrid g = slot_grid(P.J, SPT);
+      k_pre<MM, SPT><<<dim3(P.nb, g.chunks), g.nt, 0, s>>>(P);
+      return cudaGetLastError();
+    }
     dim3 grid(P.nb, (P.J + kSlotNT - 1) / kSlotNT);
     if (init && pre)
       k_slots<MM, kSlotNT, true, true><<<grid, kSlotNT, 0, s>>>(P, eps);
-    else if (init)
-      k_slots<MM, kSlotNT, true, false><<<grid, kSlotNT, 0, s>>>(P, eps);
     else
-      k_slots<MM, kSlotNT, false, true><<<grid, kSlotNT, 0, s>>>(P, eps);
+      k_slots<MM, kSlotNT, true, false><<<grid, kSlotNT, 0, s>>>(P, eps);
     return cudaGetLastError();
   });
 }

@@ -28,15 +28,40 @@ struct WienerArgs {
 // (wiener.hpp:19-43): gamma = r_h / (r_u + r_h rho_aa), s^ = gamma rho_ax,
 // image = a s^; noise = x - image (wiener.hpp:46-53). FROM_X recomputes
 // sigma_bx / tau_ax from x on the fly (the standalone API, wiener.hpp:24-26);
-// otherwise the solve's resident precompute is reused. HBM-bound.
-template <int M, int NT, bool FROM_X, bool NOISE>
-__global__ void __launch_bounds__(NT) k_wiener(WienerArgs P) {
+// otherwise the solve's resident precompute is reused. HBM-bound: each thread
+// owns SPT slots of one bin (strided by the CTA size, slot_grid) and issues all
+// of its slot loads before the per-bin prologue (a, b, R'^+ a to shared memory,
+// one barrier), which then overlaps the stream.
+template <int M, int SPT, bool FROM_X, bool NOISE>
+__global__ void __launch_bounds__(256) k_wiener(WienerArgs P) {
   __shared__ double2 sa[M];
   __shared__ double2 sb[M];
   __shared__ double2 sp[M];
-  __shared__ double sbin[4];  // rho_aa, Re/Im(sigma_ab * inv_lam) ... see below
   const int64_t bin = blockIdx.x;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t J = P.J;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.y) * nt * SPT + tid;
+  constexpr bool XIN = FROM_X || NOISE;
+  double2 x[XIN ? SPT : 1][XIN ? M : 1];
+  double2 sbx[SPT], tax[SPT];
+  double rh[SPT], ru[SPT];
+#pragma unroll
+  for (int k = 0; k < SPT; ++k) {
+    const int64_t t = t0 + static_cast<int64_t>(k) * nt;
+    if (t < J) {
+      const int64_t slot = bin * J + t;
+      if constexpr (XIN) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) x[k][m] = __ldg(P.X + slot * M + m);
+      }
+      if constexpr (!FROM_X) {
+        sbx[k] = __ldg(P.sigma_bx + slot);
+        tax[k] = __ldg(P.tau_ax + slot);
+      }
+      rh[k] = __ldg(P.r_h + slot);
+      ru[k] = __ldg(P.r_u + slot);
+    }
+  }
   if (tid < M) {
     sa[tid] = P.a[bin * M + tid];
     if (FROM_X) {
@@ -46,67 +71,59 @@ __global__ void __launch_bounds__(NT) k_wiener(WienerArgs P) {
       sp[tid] = s;
     }
   }
-  __syncthreads();
-  if (tid == 0) {
-    double2 sab;
-    double taa;
-    if (FROM_X) {
-      double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);
-      for (int k = 0; k < M; ++k) {
-        ab = cfmac(sa[k], sb[k], ab);
-        aa = cfmac(sa[k], sp[k], aa);
-      }
-      sab = ab;
-      taa = fmax(aa.x, 0.0);
-    } else {
-      sab = P.sigma_ab[bin];
-      taa = P.tau_aa[bin];
-    }
-    const double inv_lam = 1.0 / P.lambda[bin];
-    sbin[0] = taa + cnorm(sab) * inv_lam;
-    sbin[1] = sab.x;
-    sbin[2] = sab.y;
-    sbin[3] = inv_lam;
+  double2 sab;
+  double taa;
+  if (!FROM_X) {
+    sab = P.sigma_ab[bin];
+    taa = P.tau_aa[bin];
   }
+  const double inv_lam = 1.0 / P.lambda[bin];
   __syncthreads();
-  const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + tid;
-  if (t >= P.J) return;
-  const int64_t slot = bin * P.J + t;
-  const double raa = sbin[0];
-  const double2 sab = make_double2(sbin[1], sbin[2]);
-  const double inv_lam = sbin[3];
-  double2 x[M];
-  double2 sbx, tax;
-  if (FROM_X || NOISE) {
-#pragma unroll
-    for (int m = 0; m < M; ++m) x[m] = P.X[slot * M + m];
-  }
   if (FROM_X) {
-    sbx = make_double2(0.0, 0.0);
-    tax = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int m = 0; m < M; ++m) {
-      sbx = cfmac(sb[m], x[m], sbx);
-      tax = cfmac(sp[m], x[m], tax);
+    double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);
+    for (int k = 0; k < M; ++k) {
+      ab = cfmac(sa[k], sb[k], ab);
+      aa = cfmac(sa[k], sp[k], aa);
     }
-  } else {
-    sbx = P.sigma_bx[slot];
-    tax = P.tau_ax[slot];
+    sab = ab;
+    taa = fmax(aa.x, 0.0);
   }
-  const double2 c = cmul(sab, sbx);
-  const double2 rax = make_double2(fma(c.x, inv_lam, tax.x), fma(c.y, inv_lam, tax.y));
-  const double rh = P.r_h[slot], ru = P.r_u[slot];
-  const double gamma = rh / fma(rh, raa, ru);
-  const double2 s = cscale(rax, gamma);
-  if (P.dry) P.dry[slot] = s;
-  if (P.image || NOISE) {
+  const double raa = taa + cnorm(sab) * inv_lam;
 #pragma unroll
-    for (int m = 0; m < M; ++m) {
-      const double2 img = cmul(sa[m], s);
-      if (P.image) P.image[slot * M + m] = img;
-      if (NOISE) P.noise[slot * M + m] = csub(x[m], img);
+  for (int k = 0; k < SPT; ++k) {
+    const int64_t t = t0 + static_cast<int64_t>(k) * nt;
+    if (t >= J) continue;
+    const int64_t slot = bin * J + t;
+    double2 bx = make_double2(0.0, 0.0), ax = make_double2(0.0, 0.0);
+    if constexpr (FROM_X) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        bx = cfmac(sb[m], x[k][m], bx);
+        ax = cfmac(sp[m], x[k][m], ax);
+      }
+    } else {
+      bx = sbx[k];
+      ax = tax[k];
+    }
+    const double2 c = cmul(sab, bx);
+    const double2 rax = make_double2(fma(c.x, inv_lam, ax.x), fma(c.y, inv_lam, ax.y));
+    const double gamma = rh[k] / fma(rh[k], raa, ru[k]);
+    const double2 sh = cscale(rax, gamma);
+    if (P.dry) P.dry[slot] = sh;
+    if (P.image || NOISE) {
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const double2 img = cmul(sa[m], sh);
+        if (P.image) P.image[slot * M + m] = img;
+        if constexpr (NOISE) P.noise[slot * M + m] = csub(x[k][m], img);
+      }
     }
   }
+}
+// slots per thread of k_wiener: 4 without x, else 8 complex x values in registers
+template <int M, bool XIN>
+constexpr int wiener_spt() {
+  return XIN ? (M >= 8 ? 1 : 8 / M) : 4;
 }
 
 // K5: MAP objective (model.hpp:129-157), one thread per slot with an in-register

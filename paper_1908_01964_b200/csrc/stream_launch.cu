@@ -12,14 +12,14 @@ cudaError_t launch_wiener(cudaStream_t s, int M, const WienerArgs& W, bool from_
   if (W.nb * W.J == 0) return cudaSuccess;
   return dispatch_mics(M, [&](auto mm) {
     constexpr int MM = decltype(mm)::value;
-    dim3 grid(W.nb, (W.J + kWienerNT - 1) / kWienerNT);
-    if (from_x && noise)
-      k_wiener<MM, kWienerNT, true, true><<<grid, kWienerNT, 0, s>>>(W);
-    else if (from_x)
-      k_wiener<MM, kWienerNT, true, false><<<grid, kWienerNT, 0, s>>>(W);
-    else
-      k_wiener<MM, kWienerNT, false, false><<<grid, kWienerNT, 0, s>>>(W);
-    return cudaGetLastError();
+    auto go = [&](auto kern, int spt) {
+      const SlotGrid g = slot_grid(W.J, spt);
+      kern<<<dim3(W.nb, g.chunks), g.nt, 0, s>>>(W);
+      return cudaGetLastError();
+    };
+    if (from_x && noise) return go(k_wiener<MM, wiener_spt<MM, true>(), true, true>, wiener_spt<MM, true>());
+    if (from_x) return go(k_wiener<MM, wiener_spt<MM, true>(), true, false>, wiener_spt<MM, true>());
+    return go(k_wiener<MM, wiener_spt<MM, false>(), false, false>, wiener_spt<MM, false>());
   });
 }
 

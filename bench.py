@@ -7,8 +7,9 @@ the accelerated rule (Algorithm 2, solver_accel.hpp:254), complex128. Synthetic
 inputs from the BASELINE recipe (paper_1908_01964_b200/synth.py), seed
 1000 * 1 + rank, generated once on the host.
 
-A step = run_algorithm2 on the device with its inputs resident in HBM:
-restore params0 -> sigma/tau precompute (K1) -> 100 on-chip iterations (K2).
+A step = run_algorithm2 on the device with its inputs resident in HBM: one
+fused K2 launch (restore params0, the sigma/tau precompute in its prologue,
+100 on-chip iterations). K1 and K4 are timed alone (cold L2) as extras.
 value  = B * I * J * iters * n_gpus / (max-over-ranks device time per step).
 e2e    = the same metric through the C ABI entry point rcscm_gpu_run_algorithm2
          with pinned host buffers in the reference layout (H2D of X, inputs and
@@ -265,18 +266,17 @@ def run_gpu(args):
         with torch.cuda.stream(tstream):
             l2_flush.fill_(1.0)
 
-    step_stages_a = C.STAGE_RESET | C.STAGE_PRECOMPUTE
-    step_stages_b = C.STAGE_ACCEL
+    # one step = run_algorithm2 on resident inputs: restore params0, sigma / tau
+    # precompute, 100 iterations -- one fused K2 launch (precompute in its prologue)
+    step_stages = C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL
 
     # warm-up
     for _ in range(args.warmup):
-        ctx.session_run(step_stages_a, 0, hyper)
-        ctx.session_run(step_stages_b, iters, hyper)
+        ctx.session_run(step_stages, iters, hyper)
     torch.cuda.synchronize(dev)
     ctx.session_check()
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     launches0 = ctx.launch_count
     if world > 1:
         dist.barrier()
@@ -284,19 +284,16 @@ def run_gpu(args):
     with ClockSampler(local) as clk:
         for k in range(args.steps):
             flush()  # L2 flush between steps (outside the events)
-            e0, e1, e2 = ev[k]
+            e0, e1 = ev[k]
             e0.record(tstream)
-            ctx.session_run(step_stages_a, 0, hyper)
+            ctx.session_run(step_stages, iters, hyper)
             e1.record(tstream)
-            ctx.session_run(step_stages_b, iters, hyper)
-            e2.record(tstream)
         torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     launches = (ctx.launch_count - launches0) / args.steps
-    step_ms = [e0.elapsed_time(e2) for e0, _, e2 in ev]
-    k2_ms = [e1.elapsed_time(e2) for _, e1, e2 in ev]
-    k1_ms = [e0.elapsed_time(e1) for e0, e1, _ in ev]
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    k2_ms = step_ms  # the step is the single fused K2 launch
     tot_ms = sum(step_ms)
     if world > 1:
         t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
@@ -312,11 +309,17 @@ def run_gpu(args):
     rc = C.load().rcscm_gpu_probe_fp64(ctx.handle, ctypes.byref(tf), ctypes.byref(pm))
     fp64_peak = tf.value if rc == 0 else NOMINAL_FP64_TFLOPS
     k2_avg = sum(k2_ms) / len(k2_ms)
-    achieved = FLOPS_ACCEL * slot_iters / (k2_avg * 1e-3) / 1e12
+    # algorithmic flops of the fused launch: the sigma / tau forms once per slot
+    # (8 M^2 + 24 M) plus 47 per slot-iteration
+    pre_flops = 8.0 * M * M + 24.0 * M
+    launch_flops = FLOPS_ACCEL * slot_iters + pre_flops * B * I * J
+    achieved = launch_flops / (k2_avg * 1e-3) / 1e12
     roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "traffic": ncu_traffic("k_accel"),
-                "kernel": "k_accel (K2, on-chip Algorithm 2 iterations)",
+                "kernel": "k_accel<PREM=M> (K2 with the sigma/tau precompute fused into its prologue, then the "
+                          "on-chip Algorithm 2 iterations)",
                 "flops_per_slot_iter": FLOPS_ACCEL, "slot_iters_per_launch": slot_iters,
+                "precompute_flops_per_slot": pre_flops, "flops_per_launch": launch_flops,
                 "avg_launch_ms": k2_avg,
                 "peak_source": "measured live: DFMA probe (rcscm_gpu_probe_fp64) on this GPU; MEASURED_PEAKS.json "
                                "has no FP64 figure",
@@ -339,20 +342,10 @@ def run_gpu(args):
         e1.synchronize()
         return e0.elapsed_time(e1) / reps
 
-    pre_ms = timed(C.STAGE_PRECOMPUTE, 0)
-    wie_ms = timed(C.STAGE_WIENER, 0)
     naive_iters = c["naive_iters"]
     naive_ms = timed(C.STAGE_RESET | C.STAGE_NAIVE, naive_iters, reps=3)
     ctx.session_check()
-    stream_kernels = {
-        "k_slots_precompute": {"ms": pre_ms, "bytes_per_slot": BYTES_PRE.get(M), "achieved_gbs":
-                               BYTES_PRE.get(M, 0) * S / (pre_ms * 1e-3) / 1e9, "peak_gbs": hbm,
-                               "frac": BYTES_PRE.get(M, 0) * S / (pre_ms * 1e-3) / 1e9 / hbm,
-                               "note": "inputs smaller than L2 on this config; timed back-to-back after one flush"},
-        "k_wiener": {"ms": wie_ms, "bytes_per_slot": BYTES_WIENER.get(M), "achieved_gbs":
-                     BYTES_WIENER.get(M, 0) * S / (wie_ms * 1e-3) / 1e9, "peak_gbs": hbm,
-                     "frac": BYTES_WIENER.get(M, 0) * S / (wie_ms * 1e-3) / 1e9 / hbm},
-    }
+    stream_kernels = stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, torch, C)
     naive = {"value": S * naive_iters / (naive_ms * 1e-3), "unit": "TF-slot updates/s", "iters": naive_iters,
              "ms_per_run": naive_ms,
              "achieved_tflops_canonical": FLOPS_NAIVE.get(M, 0) * S * naive_iters / (naive_ms * 1e-3) / 1e12,
@@ -383,11 +376,12 @@ def run_gpu(args):
             "dtype": "f64",
             "data": "synthetic (BASELINE recipe: sinc-coherent diffuse noise + NMF-variance target, 0 dB; seed 1001+rank)",
             "config": {"workload": c["name"], "M": M, "I": I, "J": J, "utterances_per_gpu": B, "iters": iters,
-                       "step": "reset params0 + sigma/tau precompute (K1) + 100 on-chip iterations (K2)",
+                       "step": "run_algorithm2 on resident inputs: params0, sigma/tau precompute fused into the "
+                               "prologue of K2, 100 on-chip iterations (one kernel)",
                        "l2": "flushed between steps (256 MiB write, outside the timed events)",
                        "parallelism": f"bins sharded by utterance, {world} GPU(s), no collective in the loop"},
             "gpu_launches": launches,
-            "breakdown_ms": {"precompute_k1": sum(k1_ms) / len(k1_ms), "accel_k2": k2_avg},
+            "breakdown_ms": {"fused_k2": k2_avg},
             "roofline": roofline,
             "stream_kernels": stream_kernels,
             "naive": naive,
@@ -401,6 +395,49 @@ def run_gpu(args):
         dist.barrier()
         dist.destroy_process_group()
     ctx.close()
+
+
+def stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, torch, C):
+    """K1 (standalone precompute) and K4 (Wiener) against the HBM peak: each
+    launch timed alone after an L2 flush (cold L2, median of 7), on the bench
+    utterance (68 / 84 MB: launch-latency bound) and on a batch of 8 copies of
+    it (0.5 / 0.7 GB: the streaming regime the batched configs run in)."""
+    from paper_1908_01964_b200 import GpuContext
+    import numpy as np
+
+    def cold(cx, stages, reps=7):
+        ts = []
+        for r in range(reps + 1):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(tstream)
+            cx.session_run(stages, 0, hyper)
+            e1.record(tstream)
+            e1.synchronize()
+            if r:
+                ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    def entry(ms, bps, n):
+        gbs = bps * n / (ms * 1e-3) / 1e9
+        return {"ms": ms, "bytes_per_slot": bps, "slots": n, "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm}
+
+    ctx.session_run(C.STAGE_PRECOMPUTE, 0, hyper)
+    out = {"k_pre": entry(cold(ctx, C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S),
+           "k_wiener": entry(cold(ctx, C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S)}
+    nb = 8
+    big = GpuContext(local, stream=tstream.cuda_stream)
+    rep = lambda v: np.concatenate([v] * nb, axis=0)
+    big.session_load(rep(X), rep(W), rep(A), rep(T), rep(V), 0)
+    big.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
+    big.session_run(C.STAGE_ACCEL, 3, hyper)
+    out["k_pre_batch8"] = entry(cold(big, C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S * nb)
+    out["k_wiener_batch8"] = entry(cold(big, C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S * nb)
+    big.session_check()
+    big.close()
+    out["note"] = ("each launch alone after an L2 flush; algorithmic bytes (K1: read x, write sigma_bx, tau_ax, "
+                   "tau_xx; K4: read sigma_bx, tau_ax, r_h, r_u, write dry + image)")
+    return out
 
 
 def c64_measure(local, tstream, X, W, A, T, V, iters, hyper, S, args, torch, C):

@@ -72,6 +72,18 @@ struct AccelArgs {
   float* r_u_f;
   const float* r_h_f_in;  // initial iterate (may alias r_h_f)
   const float* r_u_f_in;
+  // fused precompute (k_accel PREM > 0): the sigma / tau forms are formed from
+  // x in the kernel's prologue instead of read from K1's arrays; the *_w
+  // outputs (each may be null) keep them for later stages (Wiener)
+  const double2* X;       // [bin][t][m]
+  const double2* a_in;    // [bin][M]
+  const double2* b_in;    // [bin][M]
+  const double2* Rpp_in;  // [bin][M*M]
+  double2* sigma_ab_w;
+  double* tau_aa_w;
+  double2* sigma_bx_w;
+  double2* tau_ax_w;
+  double* tau_xx_w;
 };
 
 // std::max(v, eps) of the reference (returns v unless v < eps) for eps > 0,
@@ -167,8 +179,9 @@ __device__ __forceinline__ float tfma(float a, float b, float c) { return fmaf(a
 // u s_bx, read in both halves of the iteration, stays in registers.
 // MINB: launch bounds of 128 threads x MINB CTAs/SM (MINB = 3: <= 168
 // registers) instead of one 256-thread CTA's worth (0).
+// PREM: fused precompute for M = PREM mics (0: read K1's sigma / tau arrays).
 template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
-          typename T = double>
+          typename T = double, int PREM = 0>
 #ifndef RCSCM_K2_LB_THREADS
 #define RCSCM_K2_LB_THREADS 128  // MINB launch-bounds CTA size (tools may override)
 #endif
@@ -201,9 +214,51 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
   CT* s_xd = s_tax + SPT * NT;
   CT* s_cc = s_xd + SPT * NT;
 
-  const double2 sab = P.sigma_ab[bin];
+  double2 sab;
+  double taa;
+  constexpr int PM = PREM > 0 ? PREM : 1;
+  __shared__ double2 pR[PM * PM], pb[PM], pp[PM];  // fused precompute: R'^+, b, R'^+ a
+  // fused precompute: this thread's x is requested before the per-bin prologue
+  // (whose dependent loads and barrier then overlap it) when it fits registers
+  constexpr bool XPRE = PREM > 0 && SPT * PREM <= 20;
+  double2 xpre[XPRE ? SPT : 1][XPRE ? PREM : 1];
+  if constexpr (XPRE) {
+#pragma unroll
+    for (int k = 0; k < SPT; ++k) {
+      const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+      const int64_t s = base + ((FULL || t < t_end) ? t : t0);
+#pragma unroll
+      for (int m = 0; m < PREM; ++m) xpre[k][m] = __ldg(P.X + s * PREM + m);
+    }
+  }
+  if constexpr (PREM > 0) {
+    // per-bin prologue of K1 (k_pre): R'^+, b and R'^+ a in shared memory;
+    // sigma_ab = a^H b and tau_aa = max(Re a^H R'^+ a, 0) in every thread
+    for (int k = tid; k < PREM * PREM; k += NT) pR[k] = P.Rpp_in[bin * PREM * PREM + k];
+    if (tid < PREM) {
+      pb[tid] = P.b_in[bin * PREM + tid];
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = 0; k < PREM; ++k) s = cfma(P.Rpp_in[bin * PREM * PREM + tid + k * PREM], P.a_in[bin * PREM + k], s);
+      pp[tid] = s;
+    }
+    __syncthreads();
+    double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);
+    for (int k = 0; k < PREM; ++k) {
+      const double2 ak = P.a_in[bin * PREM + k];
+      ab = cfmac(ak, pb[k], ab);
+      aa = cfmac(ak, pp[k], aa);
+    }
+    sab = ab;
+    taa = fmax(aa.x, 0.0);
+    if (rank == 0 && tid == 0 && P.sigma_ab_w) {
+      P.sigma_ab_w[bin] = sab;
+      P.tau_aa_w[bin] = taa;
+    }
+  } else {
+    sab = P.sigma_ab[bin];
+    taa = P.tau_aa[bin];
+  }
   const double s2 = cnorm(sab);  // |sigma_ab|^2
-  const double taa = P.tau_aa[bin];
   double lam = P.lambda_in[bin];
   double il = 1.0 / lam;
   double raa = fma(s2, il, taa);  // rho_aa (solver_accel.hpp:122)
@@ -252,6 +307,22 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       sb = P.sigma_bx_f[s];
       tk = P.tau_ax_f[s];
       xk = P.tau_xx_f[s] * invMT;
+    } else if constexpr (PREM > 0) {
+      rh[k] = P.r_h_in[s];
+      ru[k] = P.r_u_in[s];
+      double2 xv[PREM];
+#pragma unroll
+      for (int m = 0; m < PREM; ++m) {
+        if constexpr (XPRE) xv[m] = xpre[k][m]; else xv[m] = __ldg(P.X + s * PREM + m);
+      }
+      double txx;
+      slot_forms<PREM>(xv, pb, pp, pR, sb, tk, txx);
+      if (P.sigma_bx_w && valid[k]) {
+        P.sigma_bx_w[s] = sb;
+        P.tau_ax_w[s] = tk;
+        P.tau_xx_w[s] = txx;
+      }
+      xk = txx * invMT;
     } else {
       rh[k] = P.r_h_in[s];
       ru[k] = P.r_u_in[s];

@@ -49,8 +49,16 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
   return best;
 }
 
+bool accel_fusable(const AccelCfg& g, int M) {
+  const char* e = std::getenv("RCSCM_FUSE_PRE");
+  if (e && std::atoi(e) == 0) return false;
+  return (M == 2 || M == 4 || M == 8) && g.cl == 1 && g.full && !g.f32 && g.smem == 0 && g.minb == 3 && g.direct &&
+         g.nt <= 128;
+}
+
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
   if (A.nb * A.J == 0) return cudaSuccess;
+  if (g.prem) return launch_accel_fused(s, A, g);
   switch (g.cl) {
     case 1: return launch_accel_cl1(s, A, g);
     case 2: return launch_accel_cl2(s, A, g);

@@ -7,9 +7,9 @@
 namespace rcscm {
 
 template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
-          typename T = double>
+          typename T = double, int PREM = 0>
 cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
-  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>;
+  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);
@@ -38,16 +38,17 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
   return cudaLaunchKernelEx(&cfg, kern, A);
 }
 
-template <int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false, typename T = double>
+template <int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false, typename T = double,
+          int PREM = 0>
 cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt) {
   switch (spt) {
-    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
-    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
-    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
-    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
-    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
-    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
-    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T>(s, A, nt);
+    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
+    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
+    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
+    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
+    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
+    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
+    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -87,5 +88,7 @@ RCSCM_DECLARE_ACCEL_CL(2)
 RCSCM_DECLARE_ACCEL_CL(4)
 RCSCM_DECLARE_ACCEL_CL(8)
 RCSCM_DECLARE_ACCEL_CL(16)
+// the fused-precompute instances (accel_fused.cu)
+cudaError_t launch_accel_fused(cudaStream_t s, const AccelArgs& A, const AccelCfg& g);
 
 }  // namespace rcscm

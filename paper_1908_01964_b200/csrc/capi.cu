@@ -297,9 +297,28 @@ AccelArgs accel_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, int iters, 
   return A;
 }
 
-void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A) {
+// K2 reads x and forms sigma / tau itself (fused precompute) for the bins
+// [b0, b0 + A.nb) of the context's arrays; keep_forms also stores the forms
+// (and sigma_ab, tau_aa) for later stages.
+void set_fused(rcscm_gpu_ctx* c, AccelArgs& A, int64_t b0, int64_t J, int M, bool keep_forms) {
+  const size_t off = static_cast<size_t>(b0 * J);
+  A.X = c->X.as<double2>() + off * M;
+  A.a_in = c->a.as<double2>() + b0 * M;
+  A.b_in = c->b.as<double2>() + b0 * M;
+  A.Rpp_in = c->Rpp.as<double2>() + b0 * M * M;
+  if (keep_forms) {
+    A.sigma_ab_w = c->sab.as<double2>() + b0;
+    A.tau_aa_w = c->taa.as<double>() + b0;
+    A.sigma_bx_w = c->sbx.as<double2>() + off;
+    A.tau_ax_w = c->tax.as<double2>() + off;
+    A.tau_xx_w = c->txx.as<double>() + off;
+  }
+}
+
+void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A, int prem = 0) {
   if (A.nb * A.J == 0) return;
-  const AccelCfg g = choose_accel_cfg(A.J, f32(c));
+  AccelCfg g = choose_accel_cfg(A.J, f32(c));
+  g.prem = prem;
   if (!g.cl)
     fail(RCSCM_UNSUPPORTED,
          "frames = " + std::to_string(A.J) + " exceeds the on-chip accel kernel capacity (16 x 2048)");
@@ -454,8 +473,9 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   int nch = e_ch ? std::atoi(e_ch) : static_cast<int>(std::min<int64_t>(8, I / 128));
   nch = std::min(nch, kMaxChunks);
   if (nch < 2) return false;
-  const AccelCfg g = choose_accel_cfg(J);
+  AccelCfg g = choose_accel_cfg(J);
   if (!g.cl) return false;
+  if (accel_fusable(g, M) && opt->iters > 0) g.prem = M;  // one kernel per chunk: precompute fused into K2
   for (int k = 0; k < 2; ++k)
     if (!c->aux[k]) CK(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
   for (int k = 0; k < kMaxChunks + 3; ++k)
@@ -507,8 +527,10 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
     P.sigma_bx += off;
     P.tau_ax += off;
     P.tau_xx += off;
-    c->launched(launch_slots(cs, P, false, true, opt->eps_var));
+    const bool fuse = g.prem != 0;
+    if (!fuse) c->launched(launch_slots(cs, P, false, true, opt->eps_var));
     AccelArgs A = afull;
+    if (fuse) set_fused(c, A, i0, J, M, false);
     A.nb = Ic;
     A.sigma_ab += i0;
     A.tau_aa += i0;
@@ -967,6 +989,10 @@ int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_h
     const size_t S = static_cast<size_t>(nb * J);
     DevProblem P = problem(c, c->sB, c->sI, J, M);
     bool pre_done = false;
+    // PRECOMPUTE + ACCEL in one call (complex128, tuned K2 shape): one fused kernel
+    // forms sigma / tau from x in K2's prologue (and keeps them for WIENER)
+    const bool fuse_pre = (stages & RCSCM_STAGE_PRECOMPUTE) && (stages & RCSCM_STAGE_ACCEL) &&
+                          !(stages & RCSCM_STAGE_SETUP) && !f32(c) && accel_fusable(choose_accel_cfg(J), M);
     if (stages & RCSCM_STAGE_SETUP) {
       c->launched(launch_setup(c->stream, P, 1e-10, eps_var), 2);
       const bool pre = (stages & RCSCM_STAGE_PRECOMPUTE) != 0 && !f32(c);
@@ -987,13 +1013,16 @@ int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_h
     }
     if (!c->s_setup) fail(RCSCM_INVALID_INPUT, "session_run: run RCSCM_STAGE_SETUP first");
     if (stages & RCSCM_STAGE_RESET) c->s_reset_pending = true;
-    if ((stages & RCSCM_STAGE_PRECOMPUTE) && !pre_done) {
+    if ((stages & RCSCM_STAGE_PRECOMPUTE) && !pre_done && !fuse_pre) {
       precompute(c, P, eps_var);
       c->s_pre = true;
     }
     if (stages & RCSCM_STAGE_ACCEL) {
-      if (!c->s_pre) fail(RCSCM_INVALID_INPUT, "session_run: ACCEL needs PRECOMPUTE");
+      if (!c->s_pre && !fuse_pre) fail(RCSCM_INVALID_INPUT, "session_run: ACCEL needs PRECOMPUTE");
       AccelArgs A = accel_args(c, nb, J, M, iters, h, eps_var, 0.0);
+      // the forms depend only on the session's setup outputs: store them only
+      // if no earlier precompute has (WIENER reads them)
+      if (fuse_pre) set_fused(c, A, 0, J, M, !c->s_pre);
       if (c->s_reset_pending) {
         A.r_h_in = c->rh0.as<double>();
         A.r_u_in = c->ru0.as<double>();
@@ -1002,7 +1031,8 @@ int rcscm_gpu_session_run(rcscm_gpu_ctx* c, int stages, int iters, const rcscm_h
         A.r_u_f_in = c->ru0f.as<float>();
         c->s_reset_pending = false;
       }
-      run_accel(c, A);
+      run_accel(c, A, fuse_pre ? M : 0);
+      if (fuse_pre) c->s_pre = true;
       if (f32(c)) c->f32_params_current = true;
     }
     if (stages & (RCSCM_STAGE_NAIVE | RCSCM_STAGE_WIENER)) materialize_reset(c, S, nb);

@@ -30,6 +30,29 @@ __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_dou
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cnorm(double2 a) { return fma(a.x, a.x, a.y * a.y); }
 
+// The per-slot quadratic forms of solver_accel.hpp:33-64 for one x (M complex):
+// sigma_bx = b^H x, tau_ax = (R'^+ a)^H x, tau_xx = max(Re x^H R'^+ x, 0), in
+// the one arithmetic order shared by K1 (k_pre, k_slots) and K2's fused
+// precompute, so both produce the same bits. sb = b, sp = R'^+ a, sR = R'^+
+// (column-major M x M).
+template <int M>
+__device__ __forceinline__ void slot_forms(const double2 (&x)[M], const double2* sb, const double2* sp,
+                                           const double2* sR, double2& sbx, double2& tax, double& txx) {
+  sbx = make_double2(0.0, 0.0);
+  tax = make_double2(0.0, 0.0);
+  double2 xx = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    sbx = cfmac(sb[r], x[r], sbx);
+    tax = cfmac(sp[r], x[r], tax);
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < M; ++q) acc = cfma(sR[r + q * M], x[q], acc);
+    xx = cfmac(x[r], acc, xx);
+  }
+  txx = fmax(xx.x, 0.0);
+}
+
 // Launch shape of the slot-stream kernels (K1 precompute, K4 Wiener): each
 // thread owns SPT slots of one bin strided by the CTA size, a CTA covers one
 // chunk of a bin's frames. The chunk count is the fewest with <= 256 threads,

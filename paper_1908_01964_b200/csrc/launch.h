@@ -32,11 +32,16 @@ struct AccelCfg {
   int minb;   // 128-thread x minb-CTA launch bounds (k_accel MINB), CL == 1 and nt <= 128 only
   bool direct;  // r_u from rho(lambda_new) after the reduction (k_accel DIRECT), MINB path only
   bool f32;     // complex64 / FP32 per-slot arithmetic
+  int prem = 0;  // fused precompute for M = prem mics (k_accel PREM; 0 = read K1's arrays)
 };
 // Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL /
 // RCSCM_ACCEL_SMEM / RCSCM_ACCEL_MINB force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
 AccelCfg choose_accel_cfg(int64_t J, bool f32 = false);
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg);
+// true if K2 can fuse the sigma / tau precompute for this configuration (the
+// tuned single-CTA complex128 variant, M in {2, 4, 8}); env RCSCM_FUSE_PRE=0
+// disables it
+bool accel_fusable(const AccelCfg& cfg, int M);
 
 cudaError_t launch_naive(cudaStream_t s, int M, const NaiveArgs& N);
 

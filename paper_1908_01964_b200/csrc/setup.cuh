@@ -327,20 +327,12 @@ __global__ void __launch_bounds__(NT) k_slots(DevProblem P, double eps) {
 #pragma unroll
   for (int m = 0; m < M; ++m) x[m] = xp[m];
   if (PRE) {
-    double2 sbx = make_double2(0.0, 0.0), tax = make_double2(0.0, 0.0);
-    double2 xx = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-      sbx = cfmac(sb[r], x[r], sbx);
-      tax = cfmac(sp[r], x[r], tax);
-      double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int k = 0; k < M; ++k) acc = cfma(sRpp[r + k * M], x[k], acc);
-      xx = cfmac(x[r], acc, xx);
-    }
+    double2 sbx, tax;
+    double txx;
+    slot_forms<M>(x, sb, sp, sRpp, sbx, tax, txx);
     P.sigma_bx[slot] = sbx;
     P.tau_ax[slot] = tax;
-    P.tau_xx[slot] = fmax(xx.x, 0.0);
+    P.tau_xx[slot] = txx;
   }
   if (INIT) {
     double2 y[M];
@@ -421,20 +413,12 @@ __global__ void __launch_bounds__(256) k_pre(DevProblem P) {
     const int64_t t = t0 + static_cast<int64_t>(k) * nt;
     if (t >= J) continue;
     const int64_t slot = bin * J + t;
-    double2 sbx = make_double2(0.0, 0.0), tax = make_double2(0.0, 0.0);
-    double2 xx = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int r = 0; r < M; ++r) {
-      sbx = cfmac(sb[r], x[k][r], sbx);
-      tax = cfmac(sp[r], x[k][r], tax);
-      double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int q = 0; q < M; ++q) acc = cfma(sRpp[r + q * M], x[k][q], acc);
-      xx = cfmac(x[k][r], acc, xx);
-    }
+    double2 sbx, tax;
+    double txx;
+    slot_forms<M>(x[k], sb, sp, sRpp, sbx, tax, txx);
     P.sigma_bx[slot] = sbx;
     P.tau_ax[slot] = tax;
-    P.tau_xx[slot] = fmax(xx.x, 0.0);
+    P.tau_xx[slot] = txx;
   }
   if (blockIdx.y == 0 && tid == 0) {
     double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);

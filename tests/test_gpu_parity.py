@@ -316,6 +316,32 @@ def test_session_pipeline_matches_entry_points(O, gpu):
         assert output_rel_err(out["image"][k], oimg) <= 1e-6
 
 
+@pytest.mark.parametrize("cfg,I,J", [(0, 24, 320), (1, 16, 640), (4, 6, 640)])
+def test_fused_precompute_bitwise(O, gpu, monkeypatch, cfg, I, J):
+    """K2 with the sigma / tau precompute fused into its prologue (one kernel for
+    PRECOMPUTE | ACCEL) equals K1 + K2 bitwise, including the forms it keeps for
+    the Wiener stage; M = 2, 4, 8."""
+    from paper_1908_01964_b200 import synth
+    import paper_1908_01964_b200._capi as C
+
+    X, W, A, T, V = synth.stack(synth.make_config(cfg, utterances=2, I=I, J=J))
+    outs = []
+    for fuse in ("1", "0"):
+        monkeypatch.setenv("RCSCM_FUSE_PRE", fuse)
+        gpu.session_load(X, W, A, T, V, 0)
+        gpu.session_run(C.STAGE_SETUP)
+        n0 = gpu.launch_count
+        gpu.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL, 12)
+        launches = gpu.launch_count - n0
+        gpu.session_run(C.STAGE_WIENER)
+        gpu.session_check()
+        outs.append((gpu.session_fetch(want_image=True), launches))
+    (f, nf), (u, nu) = outs
+    assert nf == 1 and nu == 2, (nf, nu)
+    for k in ("r_h", "r_u", "lam", "dry", "image"):
+        assert np.array_equal(f[k], u[k]), k
+
+
 def test_pipelined_entry_point_bitwise(O, gpu, monkeypatch):
     """The copy/compute-pipelined run_algorithm2 (bins in chunks on two
     streams) equals the single-shot path bitwise."""

@@ -15,6 +15,7 @@ ap.add_argument("--I", type=int, default=None)
 ap.add_argument("--J", type=int, default=None)
 ap.add_argument("--B", type=int, default=1)
 ap.add_argument("--c64", action="store_true")
+ap.add_argument("--unfused", action="store_true", help="K2 alone (forms from K1's arrays)")
 a = ap.parse_args()
 c = synth.CONFIGS[a.cfg]
 utts = synth.make_config(a.cfg, utterances=a.B, I=a.I, J=a.J)
@@ -33,8 +34,10 @@ for r in range(a.reps):
         ctx.session_run(C.STAGE_WIENER, 0, h)
     elif a.naive:
         ctx.session_run(C.STAGE_NAIVE, c["naive_iters"], h)
-    else:
+    elif a.unfused:
         ctx.session_run(C.STAGE_ACCEL, c["iters"], h)
+    else:  # the bench step: precompute fused into K2
+        ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL, c["iters"], h)
     e1.record(s)
     ev.append((e0, e1))
 torch.cuda.synchronize()

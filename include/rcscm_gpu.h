@@ -8,6 +8,7 @@
  *   rcscm_gpu_init_params       replaces  init_params           model.hpp:95-124
  *   rcscm_gpu_map_objective     replaces  map_objective         model.hpp:129-157
  *   rcscm_gpu_run_naive         replaces  run_naive             solver_naive.hpp:412-450
+ *   rcscm_gpu_run_algorithm1    replaces  run_algorithm1        solver_accel.hpp:245-250
  *   rcscm_gpu_run_algorithm2    replaces  run_algorithm2        solver_accel.hpp:254-258
  *   rcscm_gpu_extract_target    replaces  extract_target        wiener.hpp:19-43
  *   rcscm_gpu_extract_noise     replaces  extract_noise         wiener.hpp:46-53
@@ -136,6 +137,12 @@ int rcscm_gpu_run_naive(rcscm_gpu_ctx* ctx, const rcscm_inputs* in,
                         const rcscm_params* params0, const rcscm_hyper* hyper,
                         const double* X, const rcscm_solver_opts* opt,
                         rcscm_params* out, rcscm_result* extra);
+/* solver_accel.hpp:245-250 (Algorithm 1: per-bin M x M inverse each iteration;
+ * needs in->R_prime, not R_prime_pinv; complex128 in both context precisions) */
+int rcscm_gpu_run_algorithm1(rcscm_gpu_ctx* ctx, const rcscm_inputs* in,
+                             const rcscm_params* params0, const rcscm_hyper* hyper,
+                             const double* X, const rcscm_solver_opts* opt,
+                             rcscm_params* out, rcscm_result* extra);
 /* solver_accel.hpp:254-258 */
 int rcscm_gpu_run_algorithm2(rcscm_gpu_ctx* ctx, const rcscm_inputs* in,
                              const rcscm_params* params0, const rcscm_hyper* hyper,

@@ -5,6 +5,7 @@
 //   rcscm::gpu::init_params       <- rcscm::init_params       model.hpp:95-124
 //   rcscm::gpu::map_objective     <- rcscm::map_objective     model.hpp:129-157
 //   rcscm::gpu::run_naive         <- rcscm::run_naive         solver_naive.hpp:412-450
+//   rcscm::gpu::run_algorithm1    <- rcscm::run_algorithm1    solver_accel.hpp:245-250
 //   rcscm::gpu::run_algorithm2    <- rcscm::run_algorithm2    solver_accel.hpp:254-258
 //   rcscm::gpu::extract_target    <- rcscm::extract_target    wiener.hpp:19-43
 //   rcscm::gpu::extract_noise     <- rcscm::extract_noise     wiener.hpp:46-53
@@ -135,7 +136,8 @@ inline RcscmParams alloc_params(int64_t I, int64_t J) {
   p.lambda.assign(I, 0.0);
   return p;
 }
-inline SolverResult run(Context& ctx, bool accel, const RcscmInputs& in, const RcscmParams& p0,
+// backend: 0 = run_naive, 1 = run_algorithm1, 2 = run_algorithm2
+inline SolverResult run(Context& ctx, int backend, const RcscmInputs& in, const RcscmParams& p0,
                         const Hyperparams& hyper, const Spectrogram& X, const SolverOptions& opt) {
   const int64_t I = in.bins, J = X.frames;
   const rcscm_inputs v = view(in, J);
@@ -160,8 +162,9 @@ inline SolverResult run(Context& ctx, bool accel, const RcscmInputs& in, const R
   rcscm_result extra{res.objective.data(), &n_obj, res.iter_seconds.data(), &n_it,
                      opt.record_trajectory ? th.data() : nullptr, opt.record_trajectory ? tu.data() : nullptr,
                      opt.record_trajectory ? tl.data() : nullptr};
-  check(accel ? rcscm_gpu_run_algorithm2(ctx.get(), &v, &pin, &h, X.ptr(), &o, &pout, &extra)
-              : rcscm_gpu_run_naive(ctx.get(), &v, &pin, &h, X.ptr(), &o, &pout, &extra));
+  check(backend == 2   ? rcscm_gpu_run_algorithm2(ctx.get(), &v, &pin, &h, X.ptr(), &o, &pout, &extra)
+        : backend == 1 ? rcscm_gpu_run_algorithm1(ctx.get(), &v, &pin, &h, X.ptr(), &o, &pout, &extra)
+                       : rcscm_gpu_run_naive(ctx.get(), &v, &pin, &h, X.ptr(), &o, &pout, &extra));
   res.objective.resize(n_obj);
   res.iter_seconds.resize(n_it);
   for (int k = 0; opt.record_trajectory && k < n_it; ++k) {
@@ -220,12 +223,17 @@ inline double map_objective(Context& ctx, const RcscmInputs& in, const RcscmPara
 
 inline SolverResult run_naive(Context& ctx, const RcscmInputs& in, const RcscmParams& params0,
                               const Hyperparams& hyper, const Spectrogram& X, const SolverOptions& opt) {
-  return detail::run(ctx, false, in, params0, hyper, X, opt);
+  return detail::run(ctx, 0, in, params0, hyper, X, opt);
+}
+
+inline SolverResult run_algorithm1(Context& ctx, const RcscmInputs& in, const RcscmParams& params0,
+                                   const Hyperparams& hyper, const Spectrogram& X, const SolverOptions& opt) {
+  return detail::run(ctx, 1, in, params0, hyper, X, opt);
 }
 
 inline SolverResult run_algorithm2(Context& ctx, const RcscmInputs& in, const RcscmParams& params0,
                                    const Hyperparams& hyper, const Spectrogram& X, const SolverOptions& opt) {
-  return detail::run(ctx, true, in, params0, hyper, X, opt);
+  return detail::run(ctx, 2, in, params0, hyper, X, opt);
 }
 
 inline ExtractionResult extract_target(Context& ctx, const RcscmInputs& in, const RcscmParams& p,

@@ -21,6 +21,7 @@ from .api import (  # noqa: F401
     extract_target,
     init_params,
     map_objective,
+    run_algorithm1,
     run_algorithm2,
     run_naive,
 )

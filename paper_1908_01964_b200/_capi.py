@@ -97,6 +97,9 @@ SIGNATURES = {
     "rcscm_gpu_run_naive": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams),
                                            ctypes.POINTER(CHyper), _dp, ctypes.POINTER(COpts),
                                            ctypes.POINTER(CParams), ctypes.POINTER(CResult)]),
+    "rcscm_gpu_run_algorithm1": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams),
+                                                ctypes.POINTER(CHyper), _dp, ctypes.POINTER(COpts),
+                                                ctypes.POINTER(CParams), ctypes.POINTER(CResult)]),
     "rcscm_gpu_run_algorithm2": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams),
                                                 ctypes.POINTER(CHyper), _dp, ctypes.POINTER(COpts),
                                                 ctypes.POINTER(CParams), ctypes.POINTER(CResult)]),

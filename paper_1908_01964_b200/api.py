@@ -7,6 +7,7 @@ Same names, argument meaning and error behaviour as
   init_params(inputs, T, V, demix_W, demix_A, X)         model.hpp:95-124
   map_objective(inputs, params, hyper, X)                model.hpp:129-157
   run_naive(inputs, params0, hyper, X, opt)              solver_naive.hpp:412-450
+  run_algorithm1(inputs, params0, hyper, X, opt)         solver_accel.hpp:245-250
   run_algorithm2(inputs, params0, hyper, X, opt)         solver_accel.hpp:254-258
   extract_target(inputs, params, X)                      wiener.hpp:19-43
   extract_noise(inputs, params, X)                       wiener.hpp:46-53
@@ -277,6 +278,9 @@ class GpuContext:
     def run_naive(self, inputs, params0, hyper, X, opt=None) -> SolverResult:
         return self._run(self._lib.rcscm_gpu_run_naive, inputs, params0, hyper, X, opt)
 
+    def run_algorithm1(self, inputs, params0, hyper, X, opt=None) -> SolverResult:
+        return self._run(self._lib.rcscm_gpu_run_algorithm1, inputs, params0, hyper, X, opt)
+
     def run_algorithm2(self, inputs, params0, hyper, X, opt=None) -> SolverResult:
         return self._run(self._lib.rcscm_gpu_run_algorithm2, inputs, params0, hyper, X, opt)
 
@@ -360,6 +364,10 @@ def map_objective(inputs, params, hyper, X):
 
 def run_naive(inputs, params0, hyper, X, opt=None):
     return default_context().run_naive(inputs, params0, hyper, X, opt)
+
+
+def run_algorithm1(inputs, params0, hyper, X, opt=None):
+    return default_context().run_algorithm1(inputs, params0, hyper, X, opt)
 
 
 def run_algorithm2(inputs, params0, hyper, X, opt=None):

@@ -84,6 +84,7 @@ struct rcscm_gpu_ctx {
   // device buffers
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
+  DBuf gam;  // Algorithm 1 scratch (gamma per slot)
   // complex64 (FP32) mode copies of the slot arrays
   DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef, rh0f, ru0f;
   bool f32_params_current = false;  // session: FP32 r_h / r_u hold the latest iterate
@@ -165,6 +166,12 @@ int decode_err(unsigned long long key, int64_t J, std::string* msg) {
       return RCSCM_NUMERICAL;
     case kErrEigNoConverge:
       *msg = "hermitian_eig: eigensolver failed to converge (bin " + bs + ")";
+      return RCSCM_NUMERICAL;
+    case kErrFirstStageLambda:
+      *msg = "rho_first_stage: nonpositive lambda at bin " + bs;
+      return RCSCM_NUMERICAL;
+    case kErrFirstStageSingular:
+      *msg = "rho_first_stage: singular R^(u) at bin " + bs;
       return RCSCM_NUMERICAL;
     default:
       *msg = "device error code " + std::to_string(code);
@@ -323,6 +330,31 @@ void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A, int prem = 0) {
     fail(RCSCM_UNSUPPORTED,
          "frames = " + std::to_string(A.J) + " exceeds the on-chip accel kernel capacity (16 x 2048)");
   c->launched(launch_accel(c->stream, A, g));
+}
+
+Accel1Args accel1_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int iters, const rcscm_hyper& h, double eps,
+                       double gamma_fault) {
+  Accel1Args A{};
+  A.nb = nb;
+  A.J = J;
+  A.iters = iters;
+  A.alpha2 = h.alpha + 2.0;
+  A.beta = h.beta;
+  A.eps = eps;
+  A.gamma_fault = gamma_fault;
+  A.X = c->X.as<double2>();
+  A.a = c->a.as<double2>();
+  A.b = c->b.as<double2>();
+  A.Rp = c->Rp.as<double2>();
+  A.r_h = c->rh.as<double>();
+  A.r_u = c->ru.as<double>();
+  A.lambda = c->lam.as<double>();
+  const size_t S = static_cast<size_t>(nb * J);
+  A.rho_ax = c->scratch.get<double2>(S);
+  A.sigma_bx = c->sbx.get<double2>(S);
+  A.gamma = c->gam.get<double>(S);
+  A.err = c->err.as<unsigned long long>();
+  return A;
 }
 
 NaiveArgs naive_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int iters, const rcscm_hyper& h, double eps) {
@@ -563,10 +595,13 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
 
 // Shared driver of run_naive / run_algorithm2 (solver_naive.hpp:412-450,
 // solver_accel.hpp:183-240).
-void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcscm_params* p0,
+enum Backend { kNaive = 0, kAccel1 = 1, kAccel2 = 2 };
+
+void run_solver(rcscm_gpu_ctx* c, Backend backend, const rcscm_inputs* in, const rcscm_params* p0,
                 const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt, rcscm_params* out,
                 rcscm_result* extra) {
-  const char* who = accel ? "run_accelerated" : "run_naive";
+  const bool accel = backend == kAccel2;  // Algorithm 2: sigma / tau precompute, K2
+  const char* who = backend == kNaive ? "run_naive" : "run_accelerated";
   validate_opts(opt, who);
   validate_inputs(in, !accel || opt->compute_objective, accel);
   if (!p0 || !out || !hyper) fail(RCSCM_INVALID_INPUT, std::string(who) + ": params / hyper must not be NULL");
@@ -610,7 +645,15 @@ void run_solver(rcscm_gpu_ctx* c, bool accel, const rcscm_inputs* in, const rcsc
   std::vector<double> objv, secs;
   int iters_run = 0;
   auto launch = [&](int first, int count) {
-    if (accel) {
+    if (backend == kAccel1) {
+      Accel1Args A = accel1_args(c, I, J, count, *hyper, opt->eps_var, opt->gamma_fault);
+      if (traj) {
+        A.traj_r_h = trh + static_cast<size_t>(first) * S;
+        A.traj_r_u = tru + static_cast<size_t>(first) * S;
+        A.traj_lambda = trl + static_cast<size_t>(first) * I;
+      }
+      c->launched(launch_accel1(c->stream, M, A));
+    } else if (accel) {
       AccelArgs A = accel_args(c, I, J, M, count, *hyper, opt->eps_var, opt->gamma_fault);
       if (traj) {
         A.traj_r_h = trh + static_cast<size_t>(first) * S;
@@ -794,7 +837,7 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->X, &c->W, &c->A, &c->T, &c->V, &c->a, &c->b, &c->Rp, &c->Rpp, &c->power, &c->sab, &c->taa,
                   &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->lpd, &c->rh0, &c->ru0, &c->lam0, &c->tmp,
-                  &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->dry, &c->image, &c->noise,
+                  &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->gam, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
                   &c->dryf, &c->imagef, &c->rh0f, &c->ru0f})
     b->release();
@@ -891,7 +934,7 @@ int rcscm_gpu_run_naive(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_pa
                         rcscm_result* extra) {
   return guarded([&] {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
-    run_solver(c, false, in, params0, hyper, X, opt, out, extra);
+    run_solver(c, kNaive, in, params0, hyper, X, opt, out, extra);
   });
 }
 
@@ -900,7 +943,16 @@ int rcscm_gpu_run_algorithm2(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcs
                              rcscm_params* out, rcscm_result* extra) {
   return guarded([&] {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
-    run_solver(c, true, in, params0, hyper, X, opt, out, extra);
+    run_solver(c, kAccel2, in, params0, hyper, X, opt, out, extra);
+  });
+}
+
+int rcscm_gpu_run_algorithm1(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* params0,
+                             const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt,
+                             rcscm_params* out, rcscm_result* extra) {
+  return guarded([&] {
+    if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
+    run_solver(c, kAccel1, in, params0, hyper, X, opt, out, extra);
   });
 }
 

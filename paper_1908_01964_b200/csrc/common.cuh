@@ -124,6 +124,8 @@ enum ErrCode : unsigned {
   kErrObjectiveNotPd = 5,  // model.hpp:141-143
   kErrObjectiveNonFinite = 6,  // model.hpp:151-153
   kErrEigNoConverge = 7,   // linalg.hpp:31-32
+  kErrFirstStageLambda = 8,    // solver_accel.hpp:90-92
+  kErrFirstStageSingular = 9,  // solver_accel.hpp:95-97
 };
 __device__ __forceinline__ void report_error(unsigned long long* err, long long slot, unsigned code) {
   atomicMin(err, (static_cast<unsigned long long>(slot) << 8) | code);

@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include "accel.cuh"
+#include "accel1.cuh"
 #include "naive.cuh"
 #include "setup.cuh"
 #include "stream.cuh"
@@ -44,6 +45,8 @@ cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg
 bool accel_fusable(const AccelCfg& cfg, int M);
 
 cudaError_t launch_naive(cudaStream_t s, int M, const NaiveArgs& N);
+// K6: Algorithm 1 (first-stage acceleration), every iteration in one launch
+cudaError_t launch_accel1(cudaStream_t s, int M, const Accel1Args& A);
 
 cudaError_t launch_wiener(cudaStream_t s, int M, const WienerArgs& W, bool from_x, bool noise);
 // K1b MODE 2: log pseudo-determinant of each bin's R' (P.logpdet)

@@ -41,7 +41,7 @@ def _synthetic(O, cfg, I, J):
 @pytest.mark.parametrize("I,J,M", [(8, 16, 2), (8, 16, 3), (8, 128, 4), (64, 16, 8), (64, 128, 2), (8, 16, 1)])
 def test_verify_instances_one_iteration(O, gpu, I, J, M):
     inp, p, X = O.make_verify_instance(I, J, M, 1000 * I + 10 * J + M)
-    for backend, fn in (("accel2", gpu.run_algorithm2), ("naive", gpu.run_naive)):
+    for backend, fn in (("accel2", gpu.run_algorithm2), ("naive", gpu.run_naive), ("accel1", gpu.run_algorithm1)):
         g = fn(inp, p, _hyper(), X, _opts(iters=1)).params
         o = O.run(backend, inp, p, X, O.SolverOptions(iters=1)).params
         r = check_params(g, o)
@@ -56,12 +56,14 @@ def test_verify_grid_trajectories(O, gpu, I, J, M):
     opt = _opts(iters=50, record_trajectory=True)
     ga = gpu.run_algorithm2(inp, p, _hyper(), X, opt)
     gn = gpu.run_naive(inp, p, _hyper(), X, opt)
+    g1 = gpu.run_algorithm1(inp, p, _hyper(), X, opt)
     on = O.run("naive", inp, p, X, O.SolverOptions(iters=50, record_trajectory=True))
-    assert len(ga.trajectory) == len(gn.trajectory) == 50
+    assert len(ga.trajectory) == len(gn.trajectory) == len(g1.trajectory) == 50
     worst = 0.0
     for k in range(50):
         worst = max(worst, O.trajectory_distance(ga.trajectory[k], on.trajectory[k]),
                     O.trajectory_distance(gn.trajectory[k], on.trajectory[k]),
+                    O.trajectory_distance(g1.trajectory[k], on.trajectory[k]),
                     O.trajectory_distance(ga.trajectory[k], gn.trajectory[k]))
     assert worst <= 1e-8, worst
 
@@ -149,9 +151,77 @@ def test_naive_scalar_known_answer(gpu):
 
 def test_iters_zero_passthrough(O, gpu):  # test_solver_accel.cpp:289-298, test_solver_naive.cpp:147-156
     inp, p, X = O.make_verify_instance(2, 4, 3, 12)
-    for fn in (gpu.run_algorithm2, gpu.run_naive):
+    for fn in (gpu.run_algorithm2, gpu.run_naive, gpu.run_algorithm1):
         r = fn(inp, p, _hyper(), X, _opts(iters=0)).params
         assert np.array_equal(r.r_h, p.r_h) and np.array_equal(r.r_u, p.r_u) and np.array_equal(r.lam, p.lam)
+
+
+# ---- Algorithm 1 (first-stage acceleration, K6) -------------------------------------
+@pytest.mark.parametrize("cfg,I,J", [(0, 16, 320), (1, 8, 640), (4, 4, 1024), (1, 5, 17)])
+def test_algorithm1_synthetic(O, gpu, cfg, I, J):
+    """run_algorithm1 vs the oracle's Algorithm 1: one iteration (r_u
+    condition-aware as for Algorithm 2), and 30-iteration trajectories against
+    GPU Algorithm 2 within the reference's cross-backend bar."""
+    u, inp, p0 = _synthetic(O, cfg, I, J)
+    S = ru_condition_scale(O, inp, p0, u.X)
+    g = gpu.run_algorithm1(inp, p0, _hyper(), u.X, _opts(iters=1)).params
+    o = O.run("accel1", inp, p0, u.X, O.SolverOptions(iters=1)).params
+    r = check_params(g, o, S)
+    assert r["ok"], r
+    g1 = gpu.run_algorithm1(inp, p0, _hyper(), u.X, _opts(iters=30)).params
+    o1 = O.run("accel1", inp, p0, u.X, O.SolverOptions(iters=30)).params
+    assert output_rel_err(gpu.extract_target(inp, g1, u.X).dry, O.extract_target(inp, o1, u.X)[1]) <= 1e-6
+
+
+def test_algorithm1_scalar_rho_first_stage(gpu):
+    """test_solver_accel.cpp:112-128: R' = 0, a = b = 1, lambda = 2, x = 0 ->
+    rho_aa = 1/2, rho_ax = rho_xx = 0; one iteration from r_h = r_u = 1 then
+    gives gamma = 1/(1 + 1/2), r_h = (gamma + beta)/(alpha + 2), lambda = gamma
+    (|s_ab|^2 = 1, s_bx = 0) and r_u = max(gamma rho_aa(lambda) / 1, eps)."""
+    from paper_1908_01964_b200 import RcscmInputs, RcscmParams
+
+    inp = RcscmInputs(np.ones((1, 1), complex), np.zeros((1, 1, 1), complex), np.zeros((1, 1, 1), complex),
+                      np.ones((1, 1), complex), 0)
+    p = RcscmParams(np.ones((1, 3)), np.ones((1, 3)), np.array([2.0]))
+    r = gpu.run_algorithm1(inp, p, _hyper(), np.zeros((1, 3, 1), complex), _opts(iters=1)).params
+    g = 1.0 / 1.5
+    assert r.r_h[0, 0] == pytest.approx((g * (1 + g * 0) + 1e-16) / 3.1, rel=1e-13)
+    assert r.lam[0] == pytest.approx(g, rel=1e-13)
+    assert r.r_u[0, 0] == pytest.approx(g * (1.0 / g) * 1.0, rel=1e-13)
+
+
+def test_algorithm1_objective_monotone_and_threads(O, gpu):
+    """test_solver_accel.cpp:320-332 (monotone objective over 100 iterations) and
+    :351-368 (results independent of the threads option), for Algorithm 1."""
+    inp, p, X = O.make_verify_instance(4, 12, 3, 14)
+    res = gpu.run_algorithm1(inp, p, _hyper(), X, _opts(iters=100, compute_objective=True))
+    obj = np.asarray(res.objective)
+    assert len(obj) == 101
+    assert np.all(obj[1:] >= obj[:-1] - 1e-7 * np.abs(obj[:-1]))
+    oo = O.run("accel1", inp, p, X, O.SolverOptions(iters=100, compute_objective=True))
+    assert np.allclose(obj, oo.objective, rtol=1e-9, atol=0)
+    inp, p, X = O.make_verify_instance(7, 10, 3, 16)
+    a = gpu.run_algorithm1(inp, p, _hyper(), X, _opts(iters=25)).params
+    b = gpu.run_algorithm1(inp, p, _hyper(), X, _opts(iters=25, threads=4)).params
+    assert np.array_equal(a.r_h, b.r_h) and np.array_equal(a.r_u, b.r_u) and np.array_equal(a.lam, b.lam)
+
+
+def test_algorithm1_errors(O, gpu):
+    """solver_accel.hpp:90-97: a nonpositive lambda / singular R^(u) raise
+    NumericalError naming the bin."""
+    from paper_1908_01964_b200 import NumericalError, RcscmParams
+
+    inp, p, X = O.make_verify_instance(3, 4, 2, 21)
+    lam = p.lam.copy()
+    lam[1] = -1.0
+    with pytest.raises(NumericalError, match="rho_first_stage: nonpositive lambda at bin 1"):
+        gpu.run_algorithm1(inp, RcscmParams(p.r_h, p.r_u, lam), _hyper(), X, _opts(iters=1))
+    Rp = inp.R_prime.copy()
+    Rp[2] = -np.eye(2)
+    import dataclasses
+
+    with pytest.raises(NumericalError, match="rho_first_stage: singular R\\^\\(u\\) at bin 2"):
+        gpu.run_algorithm1(dataclasses.replace(inp, R_prime=Rp), p, _hyper(), X, _opts(iters=1))
 
 
 @pytest.mark.parametrize("J", [16, 640])

@@ -369,7 +369,11 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
   const double taa_M = taa * inv_M;
   auto run = [&](auto sc_tag) {
     constexpr bool SCL = decltype(sc_tag)::value;
-#pragma unroll 2
+#ifndef RCSCM_K2_UNROLL
+#define RCSCM_K2_UNROLL 2  // iteration-loop unroll (tools may override)
+#endif
+    constexpr int kUnroll = RCSCM_K2_UNROLL;
+#pragma unroll kUnroll
     for (int it = 0; it < P.iters; ++it) {
       const int buf = it & 1;
       K2_PROBE(0, rh[0]);

@@ -12,6 +12,8 @@
  *   rcscm_gpu_run_algorithm2    replaces  run_algorithm2        solver_accel.hpp:254-258
  *   rcscm_gpu_extract_target    replaces  extract_target        wiener.hpp:19-43
  *   rcscm_gpu_extract_noise     replaces  extract_noise         wiener.hpp:46-53
+ *   rcscm_gpu_stft_analyze      replaces  stft_analyze          stft.hpp:50-88
+ *   rcscm_gpu_stft_synthesize   replaces  stft_synthesize       stft.hpp:92-129
  *
  * Plain pointers and sizes only; no CUDA or Eigen types cross the boundary.
  * Host buffers use the reference's Eigen column-major complex128 layouts:
@@ -22,6 +24,7 @@
  *   dry              : element (i, t) at i + t*I, complex
  *   lambda           : [i]
  *   T (NmfModel::T[n_h], I x K) : i + k*I ;  V (NmfModel::V[n_h], K x J) : k + t*K
+ *   waveform samples : (ch, p) at ch + p*M             (Waveform::samples, M x len col-major)
  *
  * Error contract (types.hpp:20-30, tools/rcscm.cpp:22-25): functions return
  *   RCSCM_OK (0), RCSCM_INVALID_INPUT (2, InvalidInputError),
@@ -155,6 +158,24 @@ int rcscm_gpu_extract_target(rcscm_gpu_ctx* ctx, const rcscm_inputs* in,
 /* wiener.hpp:46-53 */
 int rcscm_gpu_extract_noise(rcscm_gpu_ctx* ctx, const rcscm_inputs* in,
                             const rcscm_params* p, const double* X, double* noise);
+
+/* ---- STFT / ISTFT (the steps before and after the path) ------------------ */
+/* stft.hpp:37-46 + :58-60: window / hop in samples, frame count
+ * J = ceil((len + win - hop) / hop) and bin count win/2 + 1 (any output may be NULL) */
+int rcscm_gpu_stft_shape(int64_t num_samples, double sample_rate, double win_ms,
+                         double hop_ms, int* win, int* hop, int64_t* frames,
+                         int64_t* bins);
+/* stft.hpp:50-88: samples (M x len) -> X [i][t][m] (bins x frames x M) */
+int rcscm_gpu_stft_analyze(rcscm_gpu_ctx* ctx, const double* samples,
+                           int64_t num_samples, int M, double sample_rate,
+                           double win_ms, double hop_ms, double* X);
+/* stft.hpp:92-129: X [i][t][m] with the Spectrogram's win_samples / hop_samples /
+ * source_samples -> samples (M x len), len = source_samples if > 0 else
+ * J*hop - (win - hop) */
+int rcscm_gpu_stft_synthesize(rcscm_gpu_ctx* ctx, const double* X, int64_t I,
+                              int64_t J, int M, double sample_rate, int spec_win,
+                              int spec_hop, int64_t source_samples, double win_ms,
+                              double hop_ms, double* samples);
 
 /* ---- device-resident session (bench / pipelines) -------------------------
  * A session keeps one problem (B utterances x I bins x J frames x M mics,

@@ -449,6 +449,80 @@ def extract_noise(inputs: Inputs, p: Params, X):
     return noise
 
 
+# ---- stft.hpp (numpy restatement; the DFT is numpy's pocketfft) --------------
+def hamming_window(n: int) -> np.ndarray:
+    """stft.hpp:12-17: periodic Hamming, 0.54 - 0.46 cos(2 pi k / n)."""
+    return np.array([0.54 - 0.46 * np.cos(2.0 * np.pi * k / n) for k in range(n)])
+
+
+def wola_dual_window(win: np.ndarray, hop: int) -> np.ndarray:
+    """stft.hpp:22-29: d[k] = w[k] / sum of w^2 hitting k modulo hop."""
+    n = len(win)
+    denom = np.zeros(hop)
+    for k in range(n):
+        denom[k % hop] += win[k] * win[k]
+    return np.array([win[k] / denom[k % hop] for k in range(n)])
+
+
+def stft_params(sample_rate: float, win_ms: float, hop_ms: float):
+    """stft.hpp:37-46 (std::lround: half away from zero)."""
+    if not (win_ms > hop_ms and hop_ms > 0):
+        raise InvalidInputError("stft: require win_ms > hop_ms > 0")
+    rnd = lambda v: int(np.floor(abs(v) + 0.5)) * (1 if v >= 0 else -1)
+    win, hop = rnd(win_ms * 1e-3 * sample_rate), rnd(hop_ms * 1e-3 * sample_rate)
+    if win < 2 or hop < 1:
+        raise InvalidInputError("stft: window shorter than 2 samples")
+    return win, hop
+
+
+def stft_analyze(samples, sample_rate: float, win_ms: float, hop_ms: float):
+    """stft.hpp:50-88. samples (M, len) -> (X (I, J, M) complex, win, hop)."""
+    x = np.asarray(samples, np.float64)
+    if x.ndim != 2 or x.shape[0] == 0 or x.shape[1] == 0:
+        raise InvalidInputError("stft_analyze: empty waveform")
+    win, hop = stft_params(sample_rate, win_ms, hop_ms)
+    M, n = x.shape
+    pad = win - hop
+    J = (n + pad + hop - 1) // hop
+    w = hamming_window(win)
+    X = np.zeros((win // 2 + 1, J, M), np.complex128)
+    for ch in range(M):
+        for j in range(J):
+            start = j * hop - pad
+            frame = np.zeros(win)
+            lo, hi = max(start, 0), min(start + win, n)
+            if hi > lo:
+                frame[lo - start:hi - start] = x[ch, lo:hi] * w[lo - start:hi - start]
+            X[:, j, ch] = np.fft.rfft(frame)
+    return X, win, hop
+
+
+def stft_synthesize(X, sample_rate: float, win_ms: float, hop_ms: float, win_samples: int, hop_samples: int,
+                    source_samples: int = 0):
+    """stft.hpp:92-129 (weighted overlap-add with the dual window, frames in order)."""
+    X = _c(X)
+    if X.shape[0] == 0:
+        raise InvalidInputError("stft_synthesize: empty spectrogram")
+    win, hop = stft_params(sample_rate, win_ms, hop_ms)
+    if win != win_samples or hop != hop_samples:
+        raise InvalidInputError("stft_synthesize: window/hop do not match analysis")
+    if X.shape[0] != win // 2 + 1:
+        raise InvalidInputError("stft_synthesize: bin count inconsistent with window")
+    _, J, M = X.shape
+    pad = win - hop
+    n = source_samples if source_samples > 0 else J * hop - pad
+    dual = wola_dual_window(hamming_window(win), hop)
+    out = np.zeros((M, n))
+    for ch in range(M):
+        for j in range(J):
+            frame = np.fft.irfft(X[:, j, ch], n=win)
+            start = j * hop - pad
+            lo, hi = max(start, 0), min(start + win, n)
+            if hi > lo:
+                out[ch, lo:hi] += frame[lo - start:hi - start] * dual[lo - start:hi - start]
+    return out
+
+
 # ---- verify.hpp -------------------------------------------------------------
 def make_verify_instance(I, J, M, seed):
     X = np.zeros((I, J, M), np.complex128)

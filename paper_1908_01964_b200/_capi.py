@@ -97,6 +97,14 @@ SIGNATURES = {
     "rcscm_gpu_run_naive": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams),
                                            ctypes.POINTER(CHyper), _dp, ctypes.POINTER(COpts),
                                            ctypes.POINTER(CParams), ctypes.POINTER(CResult)]),
+    "rcscm_gpu_stft_shape": (ctypes.c_int, [ctypes.c_int64, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                            ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64)]),
+    "rcscm_gpu_stft_analyze": (ctypes.c_int, [_vp, _dp, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                                              ctypes.c_double, ctypes.c_double, _dp]),
+    "rcscm_gpu_stft_synthesize": (ctypes.c_int, [_vp, _dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                                 ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                                                 ctypes.c_double, ctypes.c_double, _dp]),
     "rcscm_gpu_run_algorithm1": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams),
                                                 ctypes.POINTER(CHyper), _dp, ctypes.POINTER(COpts),
                                                 ctypes.POINTER(CParams), ctypes.POINTER(CResult)]),

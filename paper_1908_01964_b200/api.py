@@ -305,6 +305,45 @@ class GpuContext:
         _raise(self._lib.rcscm_gpu_extract_noise(self._h, ctypes.byref(ci), ctypes.byref(cp), _p(X), _p(noise)))
         return noise
 
+    # ---- STFT / ISTFT (stft.hpp) ---------------------------------------------
+    def stft_shape(self, num_samples: int, sample_rate: float, win_ms: float = 64.0, hop_ms: float = 32.0):
+        """-> (win, hop, frames, bins) (stft.hpp:37-46, :58-60)."""
+        w, h = ctypes.c_int(), ctypes.c_int()
+        f, b = ctypes.c_int64(), ctypes.c_int64()
+        _raise(self._lib.rcscm_gpu_stft_shape(int(num_samples), float(sample_rate), float(win_ms), float(hop_ms),
+                                              ctypes.byref(w), ctypes.byref(h), ctypes.byref(f), ctypes.byref(b)))
+        return w.value, h.value, f.value, b.value
+
+    def stft_analyze(self, samples, sample_rate: float = 16000.0, win_ms: float = 64.0, hop_ms: float = 32.0):
+        """stft.hpp:50-88: samples (M, len) float64 -> Spectrogram X (bins, frames, M)
+        complex128 with its win / hop (dict, the Spectrogram's metadata)."""
+        x = np.asarray(samples, np.float64)
+        if x.ndim != 2:
+            raise InvalidInputError("stft_analyze: samples must be (channels, num_samples)")
+        M, n = x.shape
+        xt = np.ascontiguousarray(x.T)  # (ch, p) at ch + p*M
+        if n == 0 or M == 0:
+            _raise(self._lib.rcscm_gpu_stft_analyze(self._h, _p(xt), n, M, float(sample_rate), float(win_ms),
+                                                    float(hop_ms), None))
+        win, hop, J, B = self.stft_shape(n, sample_rate, win_ms, hop_ms)
+        X = np.zeros((B, J, M), np.complex128)
+        _raise(self._lib.rcscm_gpu_stft_analyze(self._h, _p(xt), n, M, float(sample_rate), float(win_ms),
+                                                float(hop_ms), _p(X)))
+        return X, {"sample_rate": float(sample_rate), "win_samples": win, "hop_samples": hop, "source_samples": n}
+
+    def stft_synthesize(self, X, meta: dict, win_ms: float = 64.0, hop_ms: float = 32.0):
+        """stft.hpp:92-129: Spectrogram X (bins, frames, M) + its metadata -> (M, len)."""
+        X = _cz(X)
+        I, J, M = X.shape
+        sr = float(meta.get("sample_rate", 16000.0))
+        win, hop = int(meta["win_samples"]), int(meta["hop_samples"])
+        src = int(meta.get("source_samples", 0))
+        n = src if src > 0 else J * hop - (win - hop)
+        out = np.zeros((max(n, 0), M))
+        _raise(self._lib.rcscm_gpu_stft_synthesize(self._h, _p(X), I, J, M, sr, win, hop, src, float(win_ms),
+                                                   float(hop_ms), _p(out)))
+        return np.ascontiguousarray(out.T)
+
     # ---- device-resident session ---------------------------------------------
     def session_load(self, X, W, A, T, V, n_h: int = 0):
         """X (B, I, J, M); W, A (B, I, M, M); T (B, I, K); V (B, K, J)."""

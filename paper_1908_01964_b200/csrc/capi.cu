@@ -85,6 +85,9 @@ struct rcscm_gpu_ctx {
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
   DBuf gam;  // Algorithm 1 scratch (gamma per slot)
+  // STFT: waveform, window table, frames, half spectra, Spectrogram
+  DBuf st_x, st_w, st_f, st_spec, st_X;
+  StftPlan stft_plan;
   // complex64 (FP32) mode copies of the slot arrays
   DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef, rh0f, ru0f;
   bool f32_params_current = false;  // session: FP32 r_h / r_u hold the latest iterate
@@ -839,7 +842,8 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
                   &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->lpd, &c->rh0, &c->ru0, &c->lam0, &c->tmp,
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->gam, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
-                  &c->dryf, &c->imagef, &c->rh0f, &c->ru0f})
+                  &c->dryf, &c->imagef, &c->rh0f, &c->ru0f, &c->st_x, &c->st_w, &c->st_f, &c->st_spec,
+                  &c->st_X})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -966,6 +970,93 @@ int rcscm_gpu_extract_noise(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcsc
   return guarded([&] {
     if (!noise) fail(RCSCM_INVALID_INPUT, "extract_noise: noise must not be NULL");
     extract_impl(c, in, p, X, nullptr, nullptr, noise);
+  });
+}
+
+// ---- STFT / ISTFT (stft.hpp) ------------------------------------------------------
+// detail::stft_params (stft.hpp:37-46) and the frame count of stft_analyze (:58-60)
+static void stft_params(double sample_rate, double win_ms, double hop_ms, int* win, int* hop) {
+  if (!(win_ms > hop_ms && hop_ms > 0)) fail(RCSCM_INVALID_INPUT, "stft: require win_ms > hop_ms > 0");
+  *win = static_cast<int>(std::lround(win_ms * 1e-3 * sample_rate));
+  *hop = static_cast<int>(std::lround(hop_ms * 1e-3 * sample_rate));
+  if (*win < 2 || *hop < 1) fail(RCSCM_INVALID_INPUT, "stft: window shorter than 2 samples");
+}
+
+// stft.hpp:12-17 periodic Hamming window, evaluated exactly as the reference
+static std::vector<double> hamming(int n) {
+  std::vector<double> w(n);
+  for (int k = 0; k < n; ++k) w[k] = 0.54 - 0.46 * std::cos(2.0 * M_PI * k / n);
+  return w;
+}
+
+int rcscm_gpu_stft_shape(int64_t num_samples, double sample_rate, double win_ms, double hop_ms, int* win, int* hop,
+                         int64_t* frames, int64_t* bins) {
+  return guarded([&] {
+    int w = 0, h = 0;
+    stft_params(sample_rate, win_ms, hop_ms, &w, &h);
+    if (win) *win = w;
+    if (hop) *hop = h;
+    if (frames) *frames = (num_samples + (w - h) + h - 1) / h;
+    if (bins) *bins = w / 2 + 1;
+  });
+}
+
+int rcscm_gpu_stft_analyze(rcscm_gpu_ctx* c, const double* samples, int64_t num_samples, int M, double sample_rate,
+                           double win_ms, double hop_ms, double* X) {
+  return guarded([&] {
+    if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
+    if (num_samples <= 0 || M <= 0) fail(RCSCM_INVALID_INPUT, "stft_analyze: empty waveform");
+    if (!samples || !X) fail(RCSCM_INVALID_INPUT, "stft_analyze: NULL buffer");
+    int win = 0, hop = 0;
+    stft_params(sample_rate, win_ms, hop_ms, &win, &hop);
+    const int64_t J = (num_samples + (win - hop) + hop - 1) / hop, B = win / 2 + 1, rows = J * M;
+    const std::vector<double> w = hamming(win);
+    double* dx = c->st_x.get<double>(static_cast<size_t>(num_samples) * M);
+    double* dw = c->st_w.get<double>(win);
+    h2d(c, dx, samples, static_cast<size_t>(num_samples) * M * sizeof(double));
+    h2d(c, dw, w.data(), win * sizeof(double));
+    double2* dX = c->st_X.get<double2>(static_cast<size_t>(B * rows));
+    c->launched(launch_stft_analyze(c->stream, c->stft_plan, dx, num_samples, M, win, hop, J, dw,
+                                    c->st_f.get<double>(static_cast<size_t>(rows) * win),
+                                    c->st_spec.get<double2>(static_cast<size_t>(rows * B)), dX),
+                3);
+    d2h(c, X, dX, static_cast<size_t>(B * rows) * sizeof(double2));
+    sync(c);
+  });
+}
+
+int rcscm_gpu_stft_synthesize(rcscm_gpu_ctx* c, const double* X, int64_t I, int64_t J, int M, double sample_rate,
+                              int spec_win, int spec_hop, int64_t source_samples, double win_ms, double hop_ms,
+                              double* samples) {
+  return guarded([&] {
+    if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
+    if (I <= 0) fail(RCSCM_INVALID_INPUT, "stft_synthesize: empty spectrogram");
+    int win = 0, hop = 0;
+    stft_params(sample_rate, win_ms, hop_ms, &win, &hop);
+    if (win != spec_win || hop != spec_hop)
+      fail(RCSCM_INVALID_INPUT, "stft_synthesize: window/hop do not match analysis");
+    if (I != win / 2 + 1) fail(RCSCM_INVALID_INPUT, "stft_synthesize: bin count inconsistent with window");
+    const int64_t pad = win - hop;
+    const int64_t len = source_samples > 0 ? source_samples : J * hop - pad;
+    if (len <= 0 || M <= 0 || J <= 0) fail(RCSCM_INVALID_INPUT, "stft_synthesize: empty spectrogram");
+    if (!X || !samples) fail(RCSCM_INVALID_INPUT, "stft_synthesize: NULL buffer");
+    // wola_dual_window (stft.hpp:22-29), divided by win for the unnormalised inverse DFT
+    const std::vector<double> w = hamming(win);
+    std::vector<double> denom(hop, 0.0), dual(win);
+    for (int k = 0; k < win; ++k) denom[k % hop] += w[k] * w[k];
+    for (int k = 0; k < win; ++k) dual[k] = (w[k] / denom[k % hop]) / win;
+    const int64_t rows = J * M;
+    double2* dX = c->st_X.get<double2>(static_cast<size_t>(I * rows));
+    h2d(c, dX, X, static_cast<size_t>(I * rows) * sizeof(double2));
+    double* dd = c->st_w.get<double>(win);
+    h2d(c, dd, dual.data(), win * sizeof(double));
+    double* dout = c->st_x.get<double>(static_cast<size_t>(len) * M);
+    c->launched(launch_stft_synthesize(c->stream, c->stft_plan, dX, I, J, M, win, hop, len, dd,
+                                       c->st_spec.get<double2>(static_cast<size_t>(rows * I)),
+                                       c->st_f.get<double>(static_cast<size_t>(rows) * win), dout),
+                4);
+    d2h(c, samples, dout, static_cast<size_t>(len) * M * sizeof(double));
+    sync(c);
   });
 }
 

@@ -63,7 +63,32 @@ cudaError_t launch_to_bt(cudaStream_t s, const double* src, double* dst, int64_t
 cudaError_t launch_to_ij(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J,
                          int64_t ld = 0);
 cudaError_t launch_to_ij_c(cudaStream_t s, const double2* src, double2* dst, int64_t B, int64_t I, int64_t J);
+// double2 layout change: to_bt: src (i, t) at i + t*ld -> dst[i*J + t]; else the inverse
+cudaError_t launch_transpose_c(cudaStream_t s, const double2* src, double2* dst, int64_t I, int64_t J, int64_t ld,
+                               bool to_bt);
 cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out);
+
+// STFT (stft.cu): cached batched cuFFT plans (D2Z and Z2D of length n, batch rows)
+struct StftPlan {
+  int fwd = 0, inv = 0;  // cufftHandle
+  int n = 0;
+  int64_t batch = 0;
+  StftPlan() = default;
+  StftPlan(const StftPlan&) = delete;
+  StftPlan& operator=(const StftPlan&) = delete;
+  ~StftPlan();
+  void reset();
+  cudaError_t ensure(int win, int64_t batch, cudaStream_t s);
+};
+// x: (ch, p) at ch + p*M; window[win]; scratch frames[J*M*win], spec[J*M*(win/2+1)];
+// X out: [bin][frame][mic] (stft.hpp:50-88)
+cudaError_t launch_stft_analyze(cudaStream_t s, StftPlan& plan, const double* x, int64_t len, int M, int win,
+                                int hop, int64_t J, const double* window, double* frames, double2* spec,
+                                double2* X);
+// X: [bin][frame][mic], B bins; dual_n = WOLA dual window / win; out (ch, p) at ch + p*M (stft.hpp:92-129)
+cudaError_t launch_stft_synthesize(cudaStream_t s, StftPlan& plan, const double2* X, int64_t B, int64_t J, int M,
+                                   int win, int hop, int64_t len, const double* dual_n, double2* spec,
+                                   double* frames, double* out);
 cudaError_t launch_fp32_probe(cudaStream_t s, int blocks, int iters, double* out);
 
 // complex64 (FP32) mode

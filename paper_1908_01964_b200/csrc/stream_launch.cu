@@ -68,6 +68,11 @@ cudaError_t launch_to_ij_c(cudaStream_t s, const double2* src, double2* dst, int
   return transpose<double2, false>(s, src, dst, B, I, J, I);
 }
 
+cudaError_t launch_transpose_c(cudaStream_t s, const double2* src, double2* dst, int64_t I, int64_t J, int64_t ld,
+                               bool to_bt) {
+  return to_bt ? transpose<double2, true>(s, src, dst, 1, I, J, ld) : transpose<double2, false>(s, src, dst, 1, I, J, ld);
+}
+
 cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out) {
   k_fp64_probe<8><<<blocks, 256, 0, s>>>(1.0, iters, out);
   return cudaGetLastError();

@@ -9,6 +9,8 @@
 //   rcscm::gpu::run_algorithm2    <- rcscm::run_algorithm2    solver_accel.hpp:254-258
 //   rcscm::gpu::extract_target    <- rcscm::extract_target    wiener.hpp:19-43
 //   rcscm::gpu::extract_noise     <- rcscm::extract_noise     wiener.hpp:46-53
+//   rcscm::gpu::stft_analyze      <- rcscm::stft_analyze      stft.hpp:50-88
+//   rcscm::gpu::stft_synthesize   <- rcscm::stft_synthesize   stft.hpp:92-129
 //
 // The containers below are plain std::vector stand-ins with the reference's
 // Eigen column-major layouts (see rcscm_gpu.h), so a caller holding Eigen
@@ -49,12 +51,24 @@ inline void check(int rc) {
   throw CudaError(msg);
 }
 
-// types.hpp:43-53: bins[i] is M x J col-major -> data[(i*J + t)*M + m]
+// types.hpp:43-53: bins[i] is M x J col-major -> data[(i*J + t)*M + m]; the
+// STFT metadata travel with it as in the reference
 struct Spectrogram {
   int64_t bins = 0, frames = 0;
   int mics = 0;
   std::vector<cplx> data;
+  double sample_rate = 16000.0;
+  int win_samples = 0, hop_samples = 0;
+  int64_t source_samples = 0;
   const double* ptr() const { return reinterpret_cast<const double*>(data.data()); }
+};
+
+// types.hpp:33-39: samples is channels x num_samples col-major -> data[ch + p*M]
+struct Waveform {
+  int channels = 0;
+  int64_t num_samples = 0;
+  std::vector<double> samples;
+  double sample_rate = 16000.0;
 };
 
 // model.hpp:16-25
@@ -256,6 +270,37 @@ inline Spectrogram extract_noise(Context& ctx, const RcscmInputs& in, const Rcsc
                   const_cast<double*>(p.lambda.data())};
   check(rcscm_gpu_extract_noise(ctx.get(), &v, &pv, X.ptr(), reinterpret_cast<double*>(noise.data.data())));
   return noise;
+}
+
+inline Spectrogram stft_analyze(Context& ctx, const Waveform& w, double win_ms, double hop_ms) {
+  int win = 0, hop = 0;
+  int64_t J = 0, B = 0;
+  check(rcscm_gpu_stft_shape(w.num_samples, w.sample_rate, win_ms, hop_ms, &win, &hop, &J, &B));
+  Spectrogram s;
+  s.bins = B;
+  s.frames = J;
+  s.mics = w.channels;
+  s.sample_rate = w.sample_rate;
+  s.win_samples = win;
+  s.hop_samples = hop;
+  s.source_samples = w.num_samples;
+  s.data.assign(static_cast<size_t>(B * J) * (w.channels > 0 ? w.channels : 0), cplx(0.0, 0.0));
+  check(rcscm_gpu_stft_analyze(ctx.get(), w.samples.data(), w.num_samples, w.channels, w.sample_rate, win_ms, hop_ms,
+                               reinterpret_cast<double*>(s.data.data())));
+  return s;
+}
+
+inline Waveform stft_synthesize(Context& ctx, const Spectrogram& s, double win_ms, double hop_ms) {
+  Waveform w;
+  w.channels = s.mics;
+  w.sample_rate = s.sample_rate;
+  const int64_t len = s.source_samples > 0 ? s.source_samples
+                                           : s.frames * s.hop_samples - (s.win_samples - s.hop_samples);
+  w.num_samples = len > 0 ? len : 0;
+  w.samples.assign(static_cast<size_t>(w.num_samples) * (s.mics > 0 ? s.mics : 0), 0.0);
+  check(rcscm_gpu_stft_synthesize(ctx.get(), s.ptr(), s.bins, s.frames, s.mics, s.sample_rate, s.win_samples,
+                                  s.hop_samples, s.source_samples, win_ms, hop_ms, w.samples.data()));
+  return w;
 }
 
 }  // namespace gpu

@@ -48,7 +48,27 @@ int main() {
   } catch (const InvalidInputError&) {
     threw = true;
   }
-  std::printf("shim_check: naive r_h %.17g (want %.17g) accel==naive %d wiener %d throws %d\n",
-              naive.params.r_h[0], want, ok2, ok3, threw);
-  return (ok1 && ok2 && ok3 && threw) ? 0 : 1;
+  // Algorithm 1 agrees with the naive rule on the scalar case (acceptance.cpp:34-65)
+  opt.iters = 1;
+  const SolverResult alg1 = run_algorithm1(ctx, in, p0, Hyperparams{}, X, opt);
+  const bool ok4 = std::abs(alg1.params.r_h[0] - naive.params.r_h[0]) < 1e-12 * want &&
+                   std::abs(alg1.params.lambda[0] - naive.params.lambda[0]) < 1e-12;
+  // STFT round trip (test_stft.cpp:82-97): a 440 Hz tone on 2 channels
+  Waveform w;
+  w.channels = 2;
+  w.num_samples = 16000;
+  w.samples.resize(2 * 16000);
+  for (int64_t t = 0; t < w.num_samples; ++t)
+    for (int ch = 0; ch < 2; ++ch) w.samples[ch + 2 * t] = std::sin(2.0 * M_PI * 440.0 * (t + ch) / 16000.0);
+  const Spectrogram S = stft_analyze(ctx, w, 64.0, 32.0);
+  const Waveform r = stft_synthesize(ctx, S, 64.0, 32.0);
+  double err = 0.0, ref = 0.0;
+  for (int64_t k = 2 * 1024; k < 2 * (16000 - 1024); ++k) {
+    err += (r.samples[k] - w.samples[k]) * (r.samples[k] - w.samples[k]);
+    ref += w.samples[k] * w.samples[k];
+  }
+  const bool ok5 = S.bins == 513 && S.frames == 33 && r.num_samples == w.num_samples && std::sqrt(err / ref) < 1e-8;
+  std::printf("shim_check: naive r_h %.17g (want %.17g) accel==naive %d wiener %d throws %d alg1 %d stft %d\n",
+              naive.params.r_h[0], want, ok2, ok3, threw, ok4, ok5);
+  return (ok1 && ok2 && ok3 && threw && ok4 && ok5) ? 0 : 1;
 }

@@ -449,6 +449,45 @@ def extract_noise(inputs: Inputs, p: Params, X):
     return noise
 
 
+# ---- ilrma.hpp --------------------------------------------------------------
+def sphere(X):
+    """ilrma.hpp:53-73 -> (Q (I, M, M), whitened X (I, J, M))."""
+    X = _c(X)
+    I, J, M = X.shape
+    Q = np.zeros((I, M, M), np.complex128)
+    Xw = np.zeros_like(X)
+    _check(lib().oracle_sphere(_i64(I), _i64(J), M, _p(X), _p(Q), _p(Xw)))
+    return mats_from_ref(Q), Xw
+
+
+def run_ilrma(X, K: int, iters: int, seed: int):
+    """ilrma.hpp:145-240 -> (W (I, M, M), A (I, M, M), T (M, I, K), V (M, K, J))."""
+    X = _c(X)
+    I, J, M = X.shape
+    W = np.zeros((I, M, M), np.complex128)
+    A = np.zeros((I, M, M), np.complex128)
+    T = np.zeros(M * I * K)
+    V = np.zeros(M * K * J)
+    _check(lib().oracle_run_ilrma(_i64(I), _i64(J), M, int(K), int(iters), ctypes.c_uint64(seed), _p(X), _p(W),
+                                  _p(A), _p(T), _p(V)))
+    Tn = T.reshape(M, K, I).transpose(0, 2, 1).copy()  # [n] I x K col-major
+    Vn = V.reshape(M, J, K).transpose(0, 2, 1).copy()  # [n] K x J col-major
+    return mats_from_ref(W), mats_from_ref(A), Tn, Vn
+
+
+def ilrma_objective(X, W, T, V) -> float:
+    """ilrma.hpp:86-98."""
+    X = _c(X)
+    I, J, M = X.shape
+    K = T.shape[2]
+    Tr = np.ascontiguousarray(np.asarray(T, np.float64).transpose(0, 2, 1)).ravel()
+    Vr = np.ascontiguousarray(np.asarray(V, np.float64).transpose(0, 2, 1)).ravel()
+    out = ctypes.c_double()
+    _check(lib().oracle_ilrma_objective(_i64(I), _i64(J), M, int(K), _p(X), _p(mats_to_ref(_c(W))), _p(Tr), _p(Vr),
+                                        ctypes.byref(out)))
+    return out.value
+
+
 # ---- stft.hpp (numpy restatement; the DFT is numpy's pocketfft) --------------
 def hamming_window(n: int) -> np.ndarray:
     """stft.hpp:12-17: periodic Hamming, 0.54 - 0.46 cos(2 pi k / n)."""

@@ -4,7 +4,9 @@
 // std::complex<double>, the reference algorithm of
 //   /root/reference/proj/include/rcscm/linalg.hpp        (eig, pinv, null vector)
 //   /root/reference/proj/include/rcscm/model.hpp         (build_noise_scm, init_params, map_objective)
-//   /root/reference/proj/include/rcscm/ilrma.hpp:78-83   (scale_fixed_noise_image)
+//   /root/reference/proj/include/rcscm/ilrma.hpp         (sphere, run_ilrma, ilrma_objective,
+//                                                         scale_fixed_noise_image; Eigen::FullPivLU
+//                                                         restated with its pivot and rank rules)
 //   /root/reference/proj/include/rcscm/solver_accel.hpp  (Algorithms 1 and 2)
 //   /root/reference/proj/include/rcscm/solver_naive.hpp  (naive EM)
 //   /root/reference/proj/include/rcscm/wiener.hpp        (MWF extraction)
@@ -27,6 +29,7 @@
 #include <cstring>
 #include <exception>
 #include <functional>
+#include <limits>
 #include <mutex>
 #include <random>
 #include <stdexcept>
@@ -1295,6 +1298,319 @@ static double rel_dist(const double* x, const double* y, Index n) {
   return worst;
 }
 
+// ===========================================================================
+// ilrma.hpp: sphering, Gaussian ILRMA (IP + NMF), objective
+// ===========================================================================
+
+constexpr double kNmfVarFloor = 1e-12;  // ilrma.hpp:40
+
+// Eigen::FullPivLU semantics (complete pivoting; pivot = first maximum |a_ij|
+// in column-major order of the remaining corner; rank counts pivots above
+// M * eps * |max pivot|), for the IP solve and the final inverse.
+struct FullPivLU {
+  int n = 0;
+  CMat lu;
+  std::vector<int> rowp, colp;  // row / column transpositions
+  int nonzero = 0;
+  double maxpivot = 0.0;
+  explicit FullPivLU(const CMat& A) : n(A.rows), lu(A), rowp(A.rows), colp(A.rows) {
+    nonzero = n;
+    for (int k = 0; k < n; ++k) {
+      int br = k, bc = k;
+      double big = -1.0;
+      for (int c = k; c < n; ++c)
+        for (int r = k; r < n; ++r) {
+          const double v = std::abs(lu(r, c));
+          if (v > big) {
+            big = v;
+            br = r;
+            bc = c;
+          }
+        }
+      if (big == 0.0) {
+        nonzero = k;
+        for (int i = k; i < n; ++i) rowp[i] = colp[i] = i;
+        break;
+      }
+      if (big > maxpivot) maxpivot = big;
+      rowp[k] = br;
+      colp[k] = bc;
+      if (br != k)
+        for (int c = 0; c < n; ++c) std::swap(lu(k, c), lu(br, c));
+      if (bc != k)
+        for (int r = 0; r < n; ++r) std::swap(lu(r, k), lu(r, bc));
+      for (int r = k + 1; r < n; ++r) lu(r, k) /= lu(k, k);
+      for (int c = k + 1; c < n; ++c)
+        for (int r = k + 1; r < n; ++r) lu(r, c) -= lu(r, k) * lu(k, c);
+    }
+  }
+  int rank() const {
+    const double thr = n * std::numeric_limits<double>::epsilon() * maxpivot;
+    int rk = 0;
+    for (int i = 0; i < nonzero; ++i) rk += std::abs(lu(i, i)) > thr;
+    return rk;
+  }
+  bool invertible() const { return rank() == n; }
+  CVec solve(const CVec& b) const {  // A x = b for invertible A
+    CVec y = b;
+    for (int k = 0; k < n; ++k) std::swap(y[k], y[rowp[k]]);
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < r; ++c) y[r] -= lu(r, c) * y[c];
+    for (int r = n - 1; r >= 0; --r) {
+      for (int c = r + 1; c < n; ++c) y[r] -= lu(r, c) * y[c];
+      y[r] /= lu(r, r);
+    }
+    for (int k = n - 1; k >= 0; --k) std::swap(y[k], y[colp[k]]);
+    return y;
+  }
+  CMat inverse() const {
+    CMat out(n, n);
+    for (int c = 0; c < n; ++c) {
+      CVec e(n, cplx(0, 0));
+      e[c] = 1.0;
+      const CVec x = solve(e);
+      for (int r = 0; r < n; ++r) out(r, c) = x[r];
+    }
+    return out;
+  }
+};
+
+static CMat matmul(const CMat& A, const CMat& B) {
+  CMat C(A.rows, B.cols);
+  for (int c = 0; c < B.cols; ++c)
+    for (int k = 0; k < A.cols; ++k)
+      for (int r = 0; r < A.rows; ++r) C(r, c) += A(r, k) * B(k, c);
+  return C;
+}
+
+// ilrma.hpp:53-73 sphere: per bin cov = X X^H / J + (1e-10 tr/M) I,
+// Q = sum_k v_k v_k^H / sqrt(max(l_k, 1e-300)) of eig((cov + cov^H)/2), Xw = Q X.
+static void sphere(const Spec& X, std::vector<CMat>* Q, std::vector<cplx>* Xw) {
+  const int m = X.M;
+  const Index j = X.J;
+  if (j <= m) throw InvalidInputError("sphere: need more frames than channels");
+  Q->assign(X.I, CMat());
+  Xw->assign(static_cast<size_t>(X.I * j * m), cplx(0, 0));
+  for (Index i = 0; i < X.I; ++i) {
+    CMat cov(m, m);
+    for (Index t = 0; t < j; ++t) {
+      const cplx* x = X.col(i, t);
+      for (int c = 0; c < m; ++c)
+        for (int r = 0; r < m; ++r) cov(r, c) += x[r] * std::conj(x[c]);
+    }
+    double tr = 0.0;
+    for (int r = 0; r < m; ++r) tr += std::real(cov(r, r) / static_cast<double>(j));
+    for (auto& v : cov.d) v /= static_cast<double>(j);
+    for (int r = 0; r < m; ++r) cov(r, r) += 1e-10 * tr / m;
+    CMat h(m, m);
+    for (int c = 0; c < m; ++c)
+      for (int r = 0; r < m; ++r) h(r, c) = (cov(r, c) + std::conj(cov(c, r))) / 2.0;
+    const EigResult eig = hermitian_eig(h);
+    CMat q(m, m);
+    for (int k = 0; k < m; ++k) {
+      const double l = std::max(eig.values[k], 1e-300);
+      const double s = 1.0 / std::sqrt(l);
+      for (int c = 0; c < m; ++c)
+        for (int r = 0; r < m; ++r) q(r, c) += s * eig.vectors(r, k) * std::conj(eig.vectors(c, k));
+    }
+    (*Q)[i] = q;
+    for (Index t = 0; t < j; ++t) {
+      const cplx* x = X.col(i, t);
+      cplx* y = Xw->data() + (i * j + t) * m;
+      for (int r = 0; r < m; ++r)
+        for (int c = 0; c < m; ++c) y[r] += q(r, c) * x[c];
+    }
+  }
+}
+
+struct Nmf {  // ilrma.hpp:26-29: per source T (I x K), V (K x J), column-major
+  std::vector<std::vector<double>> T, V;
+};
+
+// ilrma.hpp:100-123
+static void nmf_update(const std::vector<std::vector<double>>& P, Index I, Index J, int K, Nmf* nmf) {
+  const size_t ns = P.size();
+  std::vector<double> R(I * J), PR2(I * J), Rinv(I * J);
+  auto model = [&](const std::vector<double>& T, const std::vector<double>& V) {
+    for (Index t = 0; t < J; ++t)
+      for (Index i = 0; i < I; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < K; ++k) s += T[i + k * I] * V[k + t * K];
+        const double r = std::max(s, kNmfVarFloor);
+        R[i + t * I] = r;
+      }
+  };
+  for (size_t n = 0; n < ns; ++n) {
+    std::vector<double>& T = nmf->T[n];
+    std::vector<double>& V = nmf->V[n];
+    const std::vector<double>& Pn = P[n];
+    model(T, V);
+    for (Index e = 0; e < I * J; ++e) {
+      PR2[e] = Pn[e] / (R[e] * R[e]);
+      Rinv[e] = 1.0 / R[e];
+    }
+    std::vector<double> Tn(T.size());
+    for (int k = 0; k < K; ++k)
+      for (Index i = 0; i < I; ++i) {
+        double num = 0.0, den = 0.0;
+        for (Index t = 0; t < J; ++t) {
+          num += PR2[i + t * I] * V[k + t * K];
+          den += Rinv[i + t * I] * V[k + t * K];
+        }
+        Tn[i + k * I] = std::max(T[i + k * I] * std::sqrt(num / std::max(den, 1e-300)), 1e-300);
+      }
+    T = Tn;
+    model(T, V);
+    for (Index e = 0; e < I * J; ++e) {
+      PR2[e] = Pn[e] / (R[e] * R[e]);
+      Rinv[e] = 1.0 / R[e];
+    }
+    std::vector<double> Vn(V.size());
+    for (Index t = 0; t < J; ++t)
+      for (int k = 0; k < K; ++k) {
+        double num = 0.0, den = 0.0;
+        for (Index i = 0; i < I; ++i) {
+          num += T[i + k * I] * PR2[i + t * I];
+          den += T[i + k * I] * Rinv[i + t * I];
+        }
+        Vn[k + t * K] = std::max(V[k + t * K] * std::sqrt(num / std::max(den, 1e-300)), 1e-300);
+      }
+    V = Vn;
+  }
+}
+
+// ilrma.hpp:125-135: P[n](i, t) = |(W_i x_it)_n|^2
+static void demixed_powers(const std::vector<CMat>& W, const Spec& X, std::vector<std::vector<double>>* P) {
+  const int m = X.M;
+  for (Index i = 0; i < X.I; ++i)
+    for (Index t = 0; t < X.J; ++t) {
+      const cplx* x = X.col(i, t);
+      for (int n = 0; n < m; ++n) {
+        cplx y(0, 0);
+        for (int c = 0; c < m; ++c) y += W[i](n, c) * x[c];
+        (*P)[n][i + t * X.I] = std::norm(y);
+      }
+    }
+}
+
+// ilrma.hpp:145-240 run_ilrma
+static void run_ilrma(const Spec& X, int K, int iters, uint64_t seed, std::vector<CMat>* Wout,
+                      std::vector<CMat>* Aout, Nmf* nmf) {
+  const Index I = X.I, J = X.J;
+  const int m = X.M;
+  if (K < 1) throw InvalidInputError("run_ilrma: K must be >= 1");
+  if (iters < 0) throw InvalidInputError("run_ilrma: iters must be >= 0");
+  std::vector<CMat> W(I, CMat::identity(m));
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unif(0.1, 1.0);
+  nmf->T.assign(m, std::vector<double>());
+  nmf->V.assign(m, std::vector<double>());
+  for (int n = 0; n < m; ++n) {
+    nmf->T[n].assign(I * K, 0.0);
+    nmf->V[n].assign(static_cast<size_t>(K) * J, 0.0);
+    for (Index i = 0; i < I; ++i)
+      for (int k = 0; k < K; ++k) nmf->T[n][i + k * I] = unif(rng);
+    for (int k = 0; k < K; ++k)
+      for (Index t = 0; t < J; ++t) nmf->V[n][k + t * K] = unif(rng);
+  }
+  std::vector<std::vector<double>> P(m, std::vector<double>(I * J, 0.0));
+  demixed_powers(W, X, &P);
+  for (int pass = 0; pass < 30; ++pass) nmf_update(P, I, J, K, nmf);
+  for (int it = 0; it < iters; ++it) {
+    nmf_update(P, I, J, K, nmf);
+    std::vector<std::vector<double>> Rinv(m, std::vector<double>(I * J));
+    for (int n = 0; n < m; ++n)
+      for (Index t = 0; t < J; ++t)
+        for (Index i = 0; i < I; ++i) {
+          double s = 0.0;
+          for (int k = 0; k < K; ++k) s += nmf->T[n][i + k * I] * nmf->V[n][k + t * K];
+          Rinv[n][i + t * I] = 1.0 / std::max(s, kNmfVarFloor);
+        }
+    for (Index i = 0; i < I; ++i) {
+      CMat& Wi = W[i];
+      for (int n = 0; n < m; ++n) {
+        CMat U(m, m);
+        for (Index t = 0; t < J; ++t) {
+          const cplx* x = X.col(i, t);
+          const double w = Rinv[n][i + t * I];
+          for (int c = 0; c < m; ++c)
+            for (int r = 0; r < m; ++r) U(r, c) += w * x[r] * std::conj(x[c]);
+        }
+        for (auto& v : U.d) v /= static_cast<double>(J);
+        CMat WU = matmul(Wi, U);
+        FullPivLU lu(WU);
+        if (!lu.invertible()) {
+          double nrm = 0.0;
+          for (const auto& v : WU.d) nrm += std::norm(v);
+          const double load = 1e-8 * std::max(std::sqrt(nrm), 1e-30);
+          for (int r = 0; r < m; ++r) WU(r, r) += load;
+          lu = FullPivLU(WU);
+          if (!lu.invertible())
+            throw NumericalError("run_ilrma: singular spatial update at frequency bin " + std::to_string(i));
+        }
+        CVec e(m, cplx(0, 0));
+        e[n] = 1.0;
+        CVec w = lu.solve(e);
+        cplx uw_dot(0, 0);
+        for (int r = 0; r < m; ++r) {
+          cplx uw(0, 0);
+          for (int c = 0; c < m; ++c) uw += U(r, c) * w[c];
+          uw_dot += std::conj(w[r]) * uw;
+        }
+        const double s = std::sqrt(std::max(std::real(uw_dot), 1e-300));
+        for (int c = 0; c < m; ++c) Wi(n, c) = std::conj(w[c] / s);
+      }
+    }
+    demixed_powers(W, X, &P);
+    for (int n = 0; n < m; ++n) {
+      double sum = 0.0;
+      for (double v : P[n]) sum += v;
+      const double mu = std::sqrt(sum / static_cast<double>(I * J));
+      if (mu > 0.0 && std::isfinite(mu)) {
+        for (Index i = 0; i < I; ++i)
+          for (int c = 0; c < m; ++c) W[i](n, c) /= mu;
+        for (double& v : P[n]) v /= mu * mu;
+        for (double& v : nmf->T[n]) v /= mu * mu;
+      }
+    }
+  }
+  Aout->assign(I, CMat());
+  for (Index i = 0; i < I; ++i) {
+    FullPivLU lu(W[i]);
+    if (!lu.invertible())
+      throw NumericalError("run_ilrma: singular demixing matrix at frequency bin " + std::to_string(i));
+    (*Aout)[i] = lu.inverse();
+  }
+  *Wout = W;
+}
+
+// ilrma.hpp:86-98 ilrma_objective (|det W| by complete-pivoting LU)
+static double ilrma_objective(const std::vector<CMat>& W, const Nmf& nmf, int K, const Spec& X) {
+  const Index I = X.I, J = X.J;
+  const int m = X.M;
+  double obj = 0.0;
+  for (Index i = 0; i < I; ++i) {
+    for (int n = 0; n < m; ++n)
+      for (Index t = 0; t < J; ++t) {
+        double s = 0.0;
+        for (int k = 0; k < K; ++k) s += nmf.T[n][i + k * I] * nmf.V[n][k + t * K];
+        const double r = std::max(s, kNmfVarFloor);
+        const cplx* x = X.col(i, t);
+        cplx y(0, 0);
+        for (int c = 0; c < m; ++c) y += W[i](n, c) * x[c];
+        obj += std::norm(y) / r + std::log(r);
+      }
+    FullPivLU lu(W[i]);
+    cplx det(1.0, 0.0);
+    for (int k = 0; k < m; ++k) det *= lu.lu(k, k);
+    int swaps = 0;
+    for (int k = 0; k < m; ++k) swaps += (lu.rowp[k] != k) + (lu.colp[k] != k);
+    if (swaps % 2) det = -det;
+    obj -= 2.0 * J * std::log(std::abs(det) + 1e-300);
+  }
+  return obj;
+}
+
 }  // namespace oracle
 
 // ===========================================================================
@@ -1696,6 +2012,50 @@ double oracle_trajectory_distance(int64_t I, int64_t J, const double* r_h_a, con
                                   const double* lam_b) {
   return std::max({rel_dist(r_h_a, r_h_b, I * J), rel_dist(r_u_a, r_u_b, I * J),
                    rel_dist(lam_a, lam_b, I)});
+}
+
+// ilrma.hpp:53-73 (Q: [i][M*M] col-major, Xw: [i][t][m])
+int oracle_sphere(int64_t I, int64_t J, int M, const double* X, double* Q, double* Xw) {
+  return guarded([&] {
+    std::vector<CMat> q;
+    std::vector<cplx> xw;
+    sphere(make_spec(I, J, M, X), &q, &xw);
+    for (Index i = 0; i < I; ++i) store_mat(q[i], Q + 2 * i * M * M);
+    std::memcpy(Xw, xw.data(), sizeof(cplx) * xw.size());
+  });
+}
+
+// ilrma.hpp:145-240 (W, A: [i][M*M]; T: [n][I x K col-major]; V: [n][K x J col-major])
+int oracle_run_ilrma(int64_t I, int64_t J, int M, int K, int iters, uint64_t seed, const double* X, double* W,
+                     double* A, double* T, double* V) {
+  return guarded([&] {
+    std::vector<CMat> w, a;
+    Nmf nmf;
+    run_ilrma(make_spec(I, J, M, X), K, iters, seed, &w, &a, &nmf);
+    for (Index i = 0; i < I; ++i) {
+      store_mat(w[i], W + 2 * i * M * M);
+      store_mat(a[i], A + 2 * i * M * M);
+    }
+    for (int n = 0; n < M; ++n) {
+      std::memcpy(T + static_cast<size_t>(n) * I * K, nmf.T[n].data(), sizeof(double) * I * K);
+      std::memcpy(V + static_cast<size_t>(n) * K * J, nmf.V[n].data(), sizeof(double) * K * J);
+    }
+  });
+}
+
+// ilrma.hpp:86-98
+int oracle_ilrma_objective(int64_t I, int64_t J, int M, int K, const double* X, const double* W, const double* T,
+                           const double* V, double* out) {
+  return guarded([&] {
+    Nmf nmf;
+    nmf.T.resize(M);
+    nmf.V.resize(M);
+    for (int n = 0; n < M; ++n) {
+      nmf.T[n].assign(T + static_cast<size_t>(n) * I * K, T + static_cast<size_t>(n + 1) * I * K);
+      nmf.V[n].assign(V + static_cast<size_t>(n) * K * J, V + static_cast<size_t>(n + 1) * K * J);
+    }
+    *out = ilrma_objective(load_mats(W, I, M), nmf, K, make_spec(I, J, M, X));
+  });
 }
 
 }  // extern "C"

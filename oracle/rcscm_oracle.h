@@ -148,6 +148,15 @@ double oracle_trajectory_distance(int64_t I, int64_t J, const double* r_h_a,
                                   const double* r_h_b, const double* r_u_b,
                                   const double* lam_b);
 
+/* ilrma.hpp:53-73 sphere (Q: [i][M*M] col-major, Xw: [i][t][m]) */
+int oracle_sphere(int64_t I, int64_t J, int M, const double* X, double* Q, double* Xw);
+/* ilrma.hpp:145-240 run_ilrma (W, A: [i][M*M]; T: [n][I x K]; V: [n][K x J], col-major) */
+int oracle_run_ilrma(int64_t I, int64_t J, int M, int K, int iters, uint64_t seed, const double* X, double* W,
+                     double* A, double* T, double* V);
+/* ilrma.hpp:86-98 ilrma_objective */
+int oracle_ilrma_objective(int64_t I, int64_t J, int M, int K, const double* X, const double* W, const double* T,
+                           const double* V, double* out);
+
 #ifdef __cplusplus
 }
 #endif

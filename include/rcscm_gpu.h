@@ -14,6 +14,8 @@
  *   rcscm_gpu_extract_noise     replaces  extract_noise         wiener.hpp:46-53
  *   rcscm_gpu_stft_analyze      replaces  stft_analyze          stft.hpp:50-88
  *   rcscm_gpu_stft_synthesize   replaces  stft_synthesize       stft.hpp:92-129
+ *   rcscm_gpu_sphere            replaces  sphere                ilrma.hpp:53-73
+ *   rcscm_gpu_run_ilrma         replaces  run_ilrma             ilrma.hpp:145-240
  *
  * Plain pointers and sizes only; no CUDA or Eigen types cross the boundary.
  * Host buffers use the reference's Eigen column-major complex128 layouts:
@@ -176,6 +178,17 @@ int rcscm_gpu_stft_synthesize(rcscm_gpu_ctx* ctx, const double* X, int64_t I,
                               int64_t J, int M, double sample_rate, int spec_win,
                               int spec_hop, int64_t source_samples, double win_ms,
                               double hop_ms, double* samples);
+
+/* ---- sphering + ILRMA (the step before the path) --------------------------- */
+/* ilrma.hpp:53-73: X [i][t][m] -> Q (whitening, [i][M*M]) and Q X; either output may be NULL */
+int rcscm_gpu_sphere(rcscm_gpu_ctx* ctx, int64_t I, int64_t J, int M, const double* X,
+                     double* Q, double* Xw);
+/* ilrma.hpp:145-240: Gaussian ILRMA on (whitened) X [i][t][m] with K NMF bases
+ * (K <= 32), iters IP + NMF sweeps and the reference's seeded initialisation.
+ * Outputs (any may be NULL): W, A [i][M*M]; T [n] I x K col-major; V [n] K x J col-major. */
+int rcscm_gpu_run_ilrma(rcscm_gpu_ctx* ctx, int64_t I, int64_t J, int M, int K,
+                        int iters, uint64_t seed, const double* X, double* W, double* A,
+                        double* T, double* V);
 
 /* ---- device-resident session (bench / pipelines) -------------------------
  * A session keeps one problem (B utterances x I bins x J frames x M mics,

@@ -105,6 +105,9 @@ SIGNATURES = {
     "rcscm_gpu_stft_synthesize": (ctypes.c_int, [_vp, _dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                                  ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                                  ctypes.c_double, ctypes.c_double, _dp]),
+    "rcscm_gpu_sphere": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _dp, _dp, _dp]),
+    "rcscm_gpu_run_ilrma": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_int, ctypes.c_uint64, _dp, _dp, _dp, _dp, _dp]),
     "rcscm_gpu_run_algorithm1": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams),
                                                 ctypes.POINTER(CHyper), _dp, ctypes.POINTER(COpts),
                                                 ctypes.POINTER(CParams), ctypes.POINTER(CResult)]),

@@ -344,6 +344,29 @@ class GpuContext:
                                                    float(hop_ms), _p(out)))
         return np.ascontiguousarray(out.T)
 
+    # ---- sphering + ILRMA (ilrma.hpp) ------------------------------------------
+    def sphere(self, X):
+        """ilrma.hpp:53-73: X (I, J, M) -> (Q (I, M, M) [r, c], whitened X (I, J, M))."""
+        X = _cz(X)
+        I, J, M = X.shape
+        Q = np.zeros((I, M, M), np.complex128)  # [i][r + c*M] buffer
+        Xw = np.zeros_like(X)
+        _raise(self._lib.rcscm_gpu_sphere(self._h, I, J, M, _p(X), _p(Q), _p(Xw)))
+        return np.ascontiguousarray(Q.transpose(0, 2, 1)), Xw
+
+    def run_ilrma(self, X, K: int, iters: int, seed: int):
+        """ilrma.hpp:145-240 -> (W, A (I, M, M) [r, c]; T (M, I, K); V (M, K, J))."""
+        X = _cz(X)
+        I, J, M = X.shape
+        W = np.zeros((I, M, M), np.complex128)
+        A = np.zeros((I, M, M), np.complex128)
+        T = np.zeros((M, K, I)) if K > 0 else np.zeros(0)
+        V = np.zeros((M, J, K)) if K > 0 else np.zeros(0)
+        _raise(self._lib.rcscm_gpu_run_ilrma(self._h, I, J, M, int(K), int(iters), int(seed) & (2**64 - 1), _p(X),
+                                             _p(W), _p(A), _p(T), _p(V)))
+        tr = lambda m: np.ascontiguousarray(m.transpose(0, 2, 1))
+        return tr(W), tr(A), tr(T), tr(V)
+
     # ---- device-resident session ---------------------------------------------
     def session_load(self, X, W, A, T, V, n_h: int = 0):
         """X (B, I, J, M); W, A (B, I, M, M); T (B, I, K); V (B, K, J)."""

@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -87,6 +88,8 @@ struct rcscm_gpu_ctx {
   DBuf gam;  // Algorithm 1 scratch (gamma per slot)
   // STFT: waveform, window table, frames, half spectra, Spectrogram
   DBuf st_x, st_w, st_f, st_spec, st_X;
+  // ILRMA: whitened x, W, A, T, V, powers, partial sums, mu
+  DBuf il_X, il_W, il_A, il_T, il_V, il_P, il_part, il_mu;
   StftPlan stft_plan;
   // complex64 (FP32) mode copies of the slot arrays
   DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef, rh0f, ru0f;
@@ -175,6 +178,12 @@ int decode_err(unsigned long long key, int64_t J, std::string* msg) {
       return RCSCM_NUMERICAL;
     case kErrFirstStageSingular:
       *msg = "rho_first_stage: singular R^(u) at bin " + bs;
+      return RCSCM_NUMERICAL;
+    case kErrIlrmaSpatial:
+      *msg = "run_ilrma: singular spatial update at frequency bin " + bs;
+      return RCSCM_NUMERICAL;
+    case kErrIlrmaDemix:
+      *msg = "run_ilrma: singular demixing matrix at frequency bin " + bs;
       return RCSCM_NUMERICAL;
     default:
       *msg = "device error code " + std::to_string(code);
@@ -843,7 +852,7 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->gam, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
                   &c->dryf, &c->imagef, &c->rh0f, &c->ru0f, &c->st_x, &c->st_w, &c->st_f, &c->st_spec,
-                  &c->st_X})
+                  &c->st_X, &c->il_X, &c->il_W, &c->il_A, &c->il_T, &c->il_V, &c->il_P, &c->il_part, &c->il_mu})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1056,6 +1065,88 @@ int rcscm_gpu_stft_synthesize(rcscm_gpu_ctx* c, const double* X, int64_t I, int6
                                        c->st_f.get<double>(static_cast<size_t>(rows) * win), dout),
                 4);
     d2h(c, samples, dout, static_cast<size_t>(len) * M * sizeof(double));
+    sync(c);
+  });
+}
+
+// ---- sphering + ILRMA (ilrma.hpp) ----------------------------------------------------
+int rcscm_gpu_sphere(rcscm_gpu_ctx* c, int64_t I, int64_t J, int M, const double* X, double* Q, double* Xw) {
+  return guarded([&] {
+    if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
+    if (I < 0 || J < 0 || M < 1) fail(RCSCM_INVALID_INPUT, "sphere: bad shape");
+    check_mics(M);
+    if (J <= M) fail(RCSCM_INVALID_INPUT, "sphere: need more frames than channels");
+    if (I == 0) return;
+    const size_t S = static_cast<size_t>(I * J);
+    double2* dX = c->X.get<double2>(S * M);
+    h2d(c, dX, X, S * M * sizeof(double2));
+    double2* dQ = c->il_W.get<double2>(static_cast<size_t>(I) * M * M);
+    double2* dXw = c->il_X.get<double2>(S * M);
+    c->launched(launch_sphere(c->stream, M, dX, I, J, dQ, dXw));
+    if (Q) d2h(c, Q, dQ, static_cast<size_t>(I) * M * M * sizeof(double2));
+    if (Xw) d2h(c, Xw, dXw, S * M * sizeof(double2));
+    sync(c);
+  });
+}
+
+int rcscm_gpu_run_ilrma(rcscm_gpu_ctx* c, int64_t I, int64_t J, int M, int K, int iters, uint64_t seed,
+                        const double* X, double* W, double* A, double* T, double* V) {
+  return guarded([&] {
+    if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
+    if (K < 1) fail(RCSCM_INVALID_INPUT, "run_ilrma: K must be >= 1");
+    if (iters < 0) fail(RCSCM_INVALID_INPUT, "run_ilrma: iters must be >= 0");
+    if (I < 0 || J < 0 || M < 1) fail(RCSCM_INVALID_INPUT, "run_ilrma: bad shape");
+    check_mics(M);
+    if (K > 32) fail(RCSCM_UNSUPPORTED, "run_ilrma: K > 32 NMF bases is not supported on the GPU");
+    const size_t S = static_cast<size_t>(I * J);
+    // NMF initialisation exactly as the reference (ilrma.hpp:162-173): one
+    // mt19937_64 stream, per source T row-major over (i, k) then V over (k, t)
+    std::vector<double> hT(static_cast<size_t>(M) * I * K), hV(static_cast<size_t>(M) * K * J);
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> unif(0.1, 1.0);
+    for (int n = 0; n < M; ++n) {
+      double* Tn = hT.data() + static_cast<size_t>(n) * I * K;
+      double* Vn = hV.data() + static_cast<size_t>(n) * K * J;
+      for (int64_t i = 0; i < I; ++i)
+        for (int k = 0; k < K; ++k) Tn[i + k * I] = unif(rng);
+      for (int k = 0; k < K; ++k)
+        for (int64_t t = 0; t < J; ++t) Vn[k + t * K] = unif(rng);
+    }
+    std::vector<double> eye(static_cast<size_t>(I) * M * M * 2, 0.0);
+    for (int64_t i = 0; i < I; ++i)
+      for (int r = 0; r < M; ++r) eye[2 * (i * M * M + r + r * M)] = 1.0;
+    if (I == 0) return;
+    IlrmaArgs a{};
+    a.I = I;
+    a.J = J;
+    a.K = K;
+    double2* dX = c->il_X.get<double2>(S * M);
+    h2d(c, dX, X, S * M * sizeof(double2));
+    a.X = dX;
+    a.W = c->il_W.get<double2>(static_cast<size_t>(I) * M * M);
+    a.A = c->il_A.get<double2>(static_cast<size_t>(I) * M * M);
+    a.T = c->il_T.get<double>(hT.size());
+    a.V = c->il_V.get<double>(hV.size());
+    a.P = c->il_P.get<double>(S * M);
+    a.partial = c->il_part.get<double>(static_cast<size_t>(ilrma_partials(I, J)) * M);
+    a.mu = c->il_mu.get<double>(M);
+    a.err = c->err.get<unsigned long long>(1);
+    h2d(c, a.W, eye.data(), eye.size() * sizeof(double));
+    h2d(c, a.T, hT.data(), hT.size() * sizeof(double));
+    h2d(c, a.V, hV.data(), hV.size() * sizeof(double));
+    reset_err(c);
+    c->launched(launch_ilrma_powers(c->stream, a, M));
+    for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
+    for (int it = 0; it < iters; ++it) {
+      c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
+      c->launched(launch_ilrma_ip_scale(c->stream, a, M), 4);
+    }
+    c->launched(launch_ilrma_inverse(c->stream, a, M));
+    check_err(c, J > 0 ? J : 1);
+    if (W) d2h(c, W, a.W, static_cast<size_t>(I) * M * M * sizeof(double2));
+    if (A) d2h(c, A, a.A, static_cast<size_t>(I) * M * M * sizeof(double2));
+    if (T) d2h(c, T, a.T, hT.size() * sizeof(double));
+    if (V) d2h(c, V, a.V, hV.size() * sizeof(double));
     sync(c);
   });
 }

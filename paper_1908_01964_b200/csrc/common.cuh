@@ -29,6 +29,15 @@ __device__ __forceinline__ double2 cfmac(double2 a, double2 b, double2 acc) {
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cnorm(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+// a / b (Smith's algorithm: no overflow of |b|^2)
+__device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
+  if (fabs(b.x) >= fabs(b.y)) {
+    const double r = b.y / b.x, d = b.x + r * b.y;
+    return make_double2((a.x + r * a.y) / d, (a.y - r * a.x) / d);
+  }
+  const double r = b.x / b.y, d = b.y + r * b.x;
+  return make_double2((a.x * r + a.y) / d, (a.y * r - a.x) / d);
+}
 
 // The per-slot quadratic forms of solver_accel.hpp:33-64 for one x (M complex):
 // sigma_bx = b^H x, tau_ax = (R'^+ a)^H x, tau_xx = max(Re x^H R'^+ x, 0), in
@@ -126,6 +135,8 @@ enum ErrCode : unsigned {
   kErrEigNoConverge = 7,   // linalg.hpp:31-32
   kErrFirstStageLambda = 8,    // solver_accel.hpp:90-92
   kErrFirstStageSingular = 9,  // solver_accel.hpp:95-97
+  kErrIlrmaSpatial = 10,       // ilrma.hpp:212-216
+  kErrIlrmaDemix = 11,         // ilrma.hpp:232-236
 };
 __device__ __forceinline__ void report_error(unsigned long long* err, long long slot, unsigned code) {
   atomicMin(err, (static_cast<unsigned long long>(slot) << 8) | code);

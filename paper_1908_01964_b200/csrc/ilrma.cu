@@ -1,0 +1,532 @@
+// ilrma.cu -- sphering and Gaussian ILRMA (iterative projection + NMF) on the GPU,
+// the step before the SCM path, sm_100a.
+//
+// Reference: ilrma.hpp:53-73 (sphere), :100-123 (ilrma_nmf_update), :125-135
+// (demixed_powers), :145-240 (run_ilrma). Layouts: X [bin][frame][mic];
+// W, A [bin][M*M] column-major; T[n] I x K and V[n] K x J column-major (the
+// reference's NmfModel); P[n] [bin][frame].
+//
+// Kernels (all reductions in a fixed order, so results are deterministic):
+//   k_sphere       CTA per bin: covariance (lower triangle, block tree), one
+//                  thread's Jacobi eig -> Q, then Q x for every frame
+//   k_nmf_t        CTA per (bin, source): R, P/R^2, 1/R on the fly, the K
+//                  numerator / denominator sums over frames, T update
+//   k_nmf_v        CTA per (32-frame tile, source): the K sums over bins with the
+//                  new T, V update
+//   k_ip           CTA per bin: the M weighted covariances U_n (one source at a
+//                  time, lower triangle, block tree) and, by one thread, the
+//                  sequential row updates W_n <- (W U_n)^{-1} e_n / norm with
+//                  Eigen::FullPivLU's pivot and rank rules (diagonal-loading retry)
+//   k_powers       P[n] = |W x|^2 per slot + per-CTA partial sums for the mean
+//   k_scale_mu     one CTA: mu_n = sqrt(mean P[n]) from the partials in order
+//   k_scale_apply  W rows /= mu, P /= mu^2, T /= mu^2 (mu > 0 and finite)
+//   k_demix_inv    thread per bin: A = W^{-1} (FullPivLU), singular -> error
+#include "dispatch.cuh"
+#include "launch.h"
+
+namespace rcscm {
+
+namespace {
+
+constexpr double kNmfVarFloor = 1e-12;  // ilrma.hpp:40
+
+// Eigen::FullPivLU on an n x n column-major matrix held by one thread (in place).
+// Pivot: first maximum |a_rc| in column-major order of the remaining corner;
+// rank counts pivots above n * eps * |max pivot|.
+template <int MAXN>
+struct DevFullPivLU {
+  int n, nonzero;
+  double maxpivot;
+  int rowp[MAXN], colp[MAXN];
+  __device__ void compute(double2* lu, int nn) {
+    n = nn;
+    nonzero = n;
+    maxpivot = 0.0;
+    for (int k = 0; k < n; ++k) {
+      int br = k, bc = k;
+      double big = -1.0;
+      for (int c = k; c < n; ++c)
+        for (int r = k; r < n; ++r) {
+          const double v = hypot(lu[r + c * n].x, lu[r + c * n].y);
+          if (v > big) {
+            big = v;
+            br = r;
+            bc = c;
+          }
+        }
+      if (big == 0.0) {
+        nonzero = k;
+        for (int i = k; i < n; ++i) rowp[i] = colp[i] = i;
+        return;
+      }
+      if (big > maxpivot) maxpivot = big;
+      rowp[k] = br;
+      colp[k] = bc;
+      if (br != k)
+        for (int c = 0; c < n; ++c) {
+          const double2 t = lu[k + c * n];
+          lu[k + c * n] = lu[br + c * n];
+          lu[br + c * n] = t;
+        }
+      if (bc != k)
+        for (int r = 0; r < n; ++r) {
+          const double2 t = lu[r + k * n];
+          lu[r + k * n] = lu[r + bc * n];
+          lu[r + bc * n] = t;
+        }
+      const double2 piv = lu[k + k * n];
+      for (int r = k + 1; r < n; ++r) lu[r + k * n] = cdiv(lu[r + k * n], piv);
+      for (int c = k + 1; c < n; ++c)
+        for (int r = k + 1; r < n; ++r) lu[r + c * n] = csub(lu[r + c * n], cmul(lu[r + k * n], lu[k + c * n]));
+    }
+  }
+  __device__ bool invertible(const double2* lu) const {
+    const double thr = n * 2.220446049250313e-16 * maxpivot;
+    int rk = 0;
+    for (int i = 0; i < nonzero; ++i) rk += hypot(lu[i + i * n].x, lu[i + i * n].y) > thr;
+    return rk == n;
+  }
+  // y := A^{-1} y
+  __device__ void solve(const double2* lu, double2* y) const {
+    for (int k = 0; k < n; ++k) {
+      const double2 t = y[k];
+      y[k] = y[rowp[k]];
+      y[rowp[k]] = t;
+    }
+    for (int r = 0; r < n; ++r)
+      for (int c = 0; c < r; ++c) y[r] = csub(y[r], cmul(lu[r + c * n], y[c]));
+    for (int r = n - 1; r >= 0; --r) {
+      for (int c = r + 1; c < n; ++c) y[r] = csub(y[r], cmul(lu[r + c * n], y[c]));
+      y[r] = cdiv(y[r], lu[r + r * n]);
+    }
+    for (int k = n - 1; k >= 0; --k) {
+      const double2 t = y[k];
+      y[k] = y[colp[k]];
+      y[colp[k]] = t;
+    }
+  }
+};
+
+// Fixed-order block sum of NV doubles per thread (NT threads): xor butterfly in
+// each warp, then the warp partials summed in warp order. out[NV] in shared
+// memory; scratch red[NT/32][NV].
+template <int NT, int NV>
+__device__ void block_sum(const double (&v)[NV], double* red, double* out) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int e = 0; e < NV; ++e) {
+    double s = v[e];
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+    if (lane == 0) red[warp * NV + e] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < NV; e += NT) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += red[w * NV + e];
+    out[e] = s;
+  }
+  __syncthreads();
+}
+
+}  // namespace
+
+// ---- sphere (ilrma.hpp:53-73) ------------------------------------------------------
+template <int M, int NT>
+__global__ void __launch_bounds__(NT) k_sphere(const double2* __restrict__ X, int64_t J, double2* __restrict__ Q,
+                                               double2* __restrict__ Xw) {
+  constexpr int NE = M * (M + 1) / 2;  // lower triangle
+  __shared__ double red[NT / 32 * 2 * NE];
+  __shared__ double tot[2 * NE];
+  __shared__ double2 sQ[M * M];
+  const int64_t bin = blockIdx.x;
+  double acc[2 * NE];
+#pragma unroll
+  for (int e = 0; e < 2 * NE; ++e) acc[e] = 0.0;
+  for (int64_t t = threadIdx.x; t < J; t += NT) {
+    double2 x[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) x[m] = X[(bin * J + t) * M + m];
+    int e = 0;
+#pragma unroll
+    for (int c = 0; c < M; ++c)
+#pragma unroll
+      for (int r = c; r < M; ++r, ++e) {
+        const double2 v = cmul(x[r], cconj(x[c]));
+        acc[2 * e] += v.x;
+        acc[2 * e + 1] += v.y;
+      }
+  }
+  block_sum<NT, 2 * NE>(acc, red, tot);
+  if (threadIdx.x == 0) {
+    double2 H[M * M];
+    int e = 0;
+    for (int c = 0; c < M; ++c)
+      for (int r = c; r < M; ++r, ++e) {
+        const double2 v = make_double2(tot[2 * e] / static_cast<double>(J), tot[2 * e + 1] / static_cast<double>(J));
+        H[r + c * M] = v;
+        H[c + r * M] = cconj(v);
+      }
+    double tr = 0.0;
+    for (int r = 0; r < M; ++r) tr += H[r + r * M].x;
+    for (int r = 0; r < M; ++r) H[r + r * M].x += 1e-10 * tr / M;
+    for (int r = 0; r < M; ++r) H[r + r * M].y = 0.0;  // (cov + cov^H) / 2
+    double vals[M];
+    double2 V[M * M];
+    hermitian_eig_jacobi<M>(H, vals, V);
+    for (int k = 0; k < M * M; ++k) sQ[k] = make_double2(0.0, 0.0);
+    for (int k = 0; k < M; ++k) {
+      const double s = 1.0 / sqrt(fmax(vals[k], 1e-300));
+      for (int c = 0; c < M; ++c)
+        for (int r = 0; r < M; ++r)
+          sQ[r + c * M] = cadd(sQ[r + c * M], cscale(cmul(V[r + k * M], cconj(V[c + k * M])), s));
+    }
+    for (int k = 0; k < M * M; ++k) Q[bin * M * M + k] = sQ[k];
+  }
+  __syncthreads();
+  for (int64_t t = threadIdx.x; t < J; t += NT) {
+    double2 x[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) x[m] = X[(bin * J + t) * M + m];
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < M; ++c) y = cfma(sQ[r + c * M], x[c], y);
+      Xw[(bin * J + t) * M + r] = y;
+    }
+  }
+}
+
+// ---- NMF (ilrma.hpp:100-123) -----------------------------------------------------
+// T update for (bin i = blockIdx.x, source n = blockIdx.y)
+template <int KMAX, int NT>
+__global__ void __launch_bounds__(NT) k_nmf_t(IlrmaArgs A) {
+  __shared__ double red[NT / 32 * 2 * KMAX];
+  __shared__ double tot[2 * KMAX];
+  const int64_t i = blockIdx.x, I = A.I, J = A.J;
+  const int n = blockIdx.y, K = A.K;
+  double* T = A.T + static_cast<int64_t>(n) * I * K;
+  const double* V = A.V + static_cast<int64_t>(n) * K * J;
+  const double* P = A.P + (static_cast<int64_t>(n) * I + i) * J;
+  double tk[KMAX], acc[2 * KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    tk[k] = k < K ? T[i + k * I] : 0.0;
+    acc[2 * k] = acc[2 * k + 1] = 0.0;
+  }
+  __syncthreads();  // every thread has read T(i, :) before thread k rewrites it
+  for (int64_t t = threadIdx.x; t < J; t += NT) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) s = fma(tk[k], V[k + t * K], s);
+    const double r = fmax(s, kNmfVarFloor);
+    const double pr2 = P[t] / (r * r), rinv = 1.0 / r;
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) {
+        const double v = V[k + t * K];
+        acc[2 * k] = fma(pr2, v, acc[2 * k]);
+        acc[2 * k + 1] = fma(rinv, v, acc[2 * k + 1]);
+      }
+  }
+  block_sum<NT, 2 * KMAX>(acc, red, tot);
+  // thread k alone reads and rewrites T(i, k)
+  for (int k = threadIdx.x; k < K; k += NT)
+    T[i + k * I] = fmax(T[i + k * I] * sqrt(tot[2 * k] / fmax(tot[2 * k + 1], 1e-300)), 1e-300);
+}
+
+// V update for (32-frame tile = blockIdx.x, source n = blockIdx.y); 32 x 8 threads
+template <int KMAX>
+__global__ void __launch_bounds__(256) k_nmf_v(IlrmaArgs A) {
+  __shared__ double acc_s[32][2 * KMAX];
+  const int64_t I = A.I, J = A.J;
+  const int n = blockIdx.y, K = A.K;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * 32 + tx;
+  const double* T = A.T + static_cast<int64_t>(n) * I * K;
+  double* V = A.V + static_cast<int64_t>(n) * K * J;
+  const double* P = A.P + static_cast<int64_t>(n) * I * J;
+  double vk[KMAX], acc[2 * KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) {
+    vk[k] = (k < K && t < J) ? V[k + t * K] : 0.0;
+    acc[2 * k] = acc[2 * k + 1] = 0.0;
+  }
+  if (t < J) {
+    for (int64_t i = ty; i < I; i += 8) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) s = fma(T[i + k * I], vk[k], s);
+      const double r = fmax(s, kNmfVarFloor);
+      const double pr2 = P[i * J + t] / (r * r), rinv = 1.0 / r;
+#pragma unroll
+      for (int k = 0; k < KMAX; ++k)
+        if (k < K) {
+          const double tv = T[i + k * I];
+          acc[2 * k] = fma(tv, pr2, acc[2 * k]);
+          acc[2 * k + 1] = fma(tv, rinv, acc[2 * k + 1]);
+        }
+    }
+  }
+  // fixed-order sum over the 8 row groups
+  for (int y = 0; y < 8; ++y) {
+    if (ty == y) {
+#pragma unroll
+      for (int e = 0; e < 2 * KMAX; ++e) acc_s[tx][e] = (y == 0 ? 0.0 : acc_s[tx][e]) + acc[e];
+    }
+    __syncthreads();
+  }
+  if (ty == 0 && t < J)
+    for (int k = 0; k < K; ++k)
+      V[k + t * K] = fmax(vk[k] * sqrt(acc_s[tx][2 * k] / fmax(acc_s[tx][2 * k + 1], 1e-300)), 1e-300);
+}
+
+// ---- iterative projection (ilrma.hpp:190-216) -----------------------------------
+template <int M, int NT>
+__global__ void __launch_bounds__(NT) k_ip(IlrmaArgs A) {
+  constexpr int NE = M * (M + 1) / 2;
+  __shared__ double red[NT / 32 * 2 * NE];
+  __shared__ double tot[2 * NE];
+  __shared__ double2 sW[M * M];
+  __shared__ int s_fail;
+  const int64_t i = blockIdx.x, I = A.I, J = A.J;
+  const int K = A.K;
+  if (threadIdx.x < M * M) sW[threadIdx.x] = A.W[i * M * M + threadIdx.x];
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  for (int n = 0; n < M; ++n) {
+    const double* T = A.T + static_cast<int64_t>(n) * I * K;
+    const double* V = A.V + static_cast<int64_t>(n) * K * J;
+    double acc[2 * NE];
+#pragma unroll
+    for (int e = 0; e < 2 * NE; ++e) acc[e] = 0.0;
+    for (int64_t t = threadIdx.x; t < J; t += NT) {
+      double s = 0.0;
+      for (int k = 0; k < K; ++k) s = fma(T[i + k * I], V[k + t * K], s);
+      const double w = 1.0 / fmax(s, kNmfVarFloor);
+      double2 x[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) x[m] = A.X[(i * J + t) * M + m];
+      int e = 0;
+#pragma unroll
+      for (int c = 0; c < M; ++c)
+#pragma unroll
+        for (int r = c; r < M; ++r, ++e) {
+          const double2 v = cscale(cmul(x[r], cconj(x[c])), w);
+          acc[2 * e] += v.x;
+          acc[2 * e + 1] += v.y;
+        }
+    }
+      block_sum<NT, 2 * NE>(acc, red, tot);
+    if (threadIdx.x == 0 && !s_fail) {
+      double2 U[M * M], WU[M * M];
+      int e = 0;
+      for (int c = 0; c < M; ++c)
+        for (int r = c; r < M; ++r, ++e) {
+          const double2 v = make_double2(tot[2 * e] / static_cast<double>(J), tot[2 * e + 1] / static_cast<double>(J));
+          U[r + c * M] = v;
+          U[c + r * M] = cconj(v);
+        }
+      for (int c = 0; c < M; ++c)
+        for (int r = 0; r < M; ++r) {
+          double2 s = make_double2(0.0, 0.0);
+          for (int k = 0; k < M; ++k) s = cfma(sW[r + k * M], U[k + c * M], s);
+          WU[r + c * M] = s;
+        }
+      double2 lu[M * M];
+      for (int k = 0; k < M * M; ++k) lu[k] = WU[k];
+      DevFullPivLU<M> f;
+      f.compute(lu, M);
+      bool ok = f.invertible(lu);
+      if (!ok) {  // diagonal-loading retry (ilrma.hpp:205-211)
+        double nrm = 0.0;
+        for (int k = 0; k < M * M; ++k) nrm += cnorm(WU[k]);
+        const double load = 1e-8 * fmax(sqrt(nrm), 1e-30);
+        for (int k = 0; k < M * M; ++k) lu[k] = WU[k];
+        for (int r = 0; r < M; ++r) lu[r + r * M].x += load;
+        f.compute(lu, M);
+        ok = f.invertible(lu);
+      }
+      if (!ok) {
+        report_error(A.err, i * J, kErrIlrmaSpatial);
+        s_fail = 1;
+      } else {
+        double2 w[M];
+        for (int r = 0; r < M; ++r) w[r] = make_double2(r == n ? 1.0 : 0.0, 0.0);
+        f.solve(lu, w);
+        double2 q = make_double2(0.0, 0.0);
+        for (int r = 0; r < M; ++r) {
+          double2 uw = make_double2(0.0, 0.0);
+          for (int c = 0; c < M; ++c) uw = cfma(U[r + c * M], w[c], uw);
+          q = cfmac(w[r], uw, q);
+        }
+        const double s = sqrt(fmax(q.x, 1e-300));
+        for (int c = 0; c < M; ++c) sW[n + c * M] = cconj(make_double2(w[c].x / s, w[c].y / s));
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < M * M) A.W[i * M * M + threadIdx.x] = sW[threadIdx.x];
+}
+
+// ---- demixed powers, scale normalisation, final inverse --------------------------
+// P[n][i][t] = |(W_i x_it)_n|^2; partial[n][cta] = this CTA's sum (grid: bins x chunks)
+template <int M, int NT>
+__global__ void __launch_bounds__(NT) k_powers(IlrmaArgs A) {
+  __shared__ double red[NT / 32 * M];
+  __shared__ double tot[M];
+  __shared__ double2 sW[M * M];
+  const int64_t i = blockIdx.x, I = A.I, J = A.J;
+  if (threadIdx.x < M * M) sW[threadIdx.x] = A.W[i * M * M + threadIdx.x];
+  __syncthreads();
+  double acc[M];
+#pragma unroll
+  for (int n = 0; n < M; ++n) acc[n] = 0.0;
+  const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + threadIdx.x;
+  if (t < J) {
+    double2 x[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) x[m] = A.X[(i * J + t) * M + m];
+#pragma unroll
+    for (int n = 0; n < M; ++n) {
+      double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < M; ++c) y = cfma(sW[n + c * M], x[c], y);
+      const double p = cnorm(y);
+      A.P[(static_cast<int64_t>(n) * I + i) * J + t] = p;
+      acc[n] = p;
+    }
+  }
+  block_sum<NT, M>(acc, red, tot);
+  const int64_t cta = i * gridDim.y + blockIdx.y, ncta = I * gridDim.y;
+  if (threadIdx.x < M) A.partial[threadIdx.x * ncta + cta] = tot[threadIdx.x];
+}
+
+// mu_n = sqrt(mean P[n]) (ilrma.hpp:221-229), partials summed in CTA order
+__global__ void k_scale_mu(IlrmaArgs A, int64_t ncta, int M) {
+  __shared__ double red[32 * 16];
+  const int n = blockIdx.x;
+  double s = 0.0;
+  for (int64_t c = threadIdx.x; c < ncta; c += blockDim.x) s += A.partial[n * ncta + c];
+  for (int m = 16; m > 0; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+    A.mu[n] = sqrt(tot / static_cast<double>(A.I * A.J));
+  }
+  (void)M;
+}
+
+// W rows /= mu, P /= mu^2, T /= mu^2 where mu > 0 and finite
+__global__ void k_scale_apply(IlrmaArgs A, int M) {
+  const int64_t I = A.I, J = A.J;
+  const int K = A.K;
+  const int64_t nP = static_cast<int64_t>(M) * I * J, nT = static_cast<int64_t>(M) * I * K,
+                nW = I * static_cast<int64_t>(M) * M;
+  for (int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; q < nP + nT + nW;
+       q += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    int n;
+    if (q < nP) {
+      n = static_cast<int>(q / (I * J));
+      const double mu = A.mu[n];
+      if (mu > 0.0 && isfinite(mu)) A.P[q] /= mu * mu;
+    } else if (q < nP + nT) {
+      const int64_t r = q - nP;
+      n = static_cast<int>(r / (I * K));
+      const double mu = A.mu[n];
+      if (mu > 0.0 && isfinite(mu)) A.T[r] /= mu * mu;
+    } else {
+      const int64_t r = q - nP - nT;
+      const int64_t e = r % (static_cast<int64_t>(M) * M);
+      n = static_cast<int>(e % M);  // row of the column-major entry
+      const double mu = A.mu[n];
+      if (mu > 0.0 && isfinite(mu)) A.W[r] = make_double2(A.W[r].x / mu, A.W[r].y / mu);
+    }
+  }
+}
+
+template <int M>
+__global__ void k_demix_inv(IlrmaArgs A) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= A.I) return;
+  double2 lu[M * M];
+  for (int k = 0; k < M * M; ++k) lu[k] = A.W[i * M * M + k];
+  DevFullPivLU<M> f;
+  f.compute(lu, M);
+  if (!f.invertible(lu)) {
+    report_error(A.err, i * A.J, kErrIlrmaDemix);
+    return;
+  }
+  for (int c = 0; c < M; ++c) {
+    double2 e[M];
+    for (int r = 0; r < M; ++r) e[r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    f.solve(lu, e);
+    for (int r = 0; r < M; ++r) A.A[i * M * M + r + c * M] = e[r];
+  }
+}
+
+// ---- launchers -------------------------------------------------------------------
+constexpr int kIlrmaNT = 128;
+
+cudaError_t launch_sphere(cudaStream_t s, int M, const double2* X, int64_t I, int64_t J, double2* Q, double2* Xw) {
+  if (I * J == 0) return cudaSuccess;
+  return dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    k_sphere<MM, kIlrmaNT><<<static_cast<unsigned>(I), kIlrmaNT, 0, s>>>(X, J, Q, Xw);
+    return cudaGetLastError();
+  });
+}
+
+int64_t ilrma_partials(int64_t I, int64_t J) { return I * ((J + kIlrmaNT - 1) / kIlrmaNT); }
+
+template <int KMAX>
+static cudaError_t nmf_update(cudaStream_t s, const IlrmaArgs& A, int M) {
+  k_nmf_t<KMAX, kIlrmaNT><<<dim3(static_cast<unsigned>(A.I), M), kIlrmaNT, 0, s>>>(A);
+  k_nmf_v<KMAX><<<dim3(static_cast<unsigned>((A.J + 31) / 32), M), 256, 0, s>>>(A);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ilrma_nmf(cudaStream_t s, const IlrmaArgs& A, int M) {
+  if (A.K <= 4) return nmf_update<4>(s, A, M);
+  if (A.K <= 8) return nmf_update<8>(s, A, M);
+  if (A.K <= 16) return nmf_update<16>(s, A, M);
+  if (A.K <= 32) return nmf_update<32>(s, A, M);
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_ilrma_powers(cudaStream_t s, const IlrmaArgs& A, int M) {
+  return dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    k_powers<MM, kIlrmaNT><<<dim3(static_cast<unsigned>(A.I), static_cast<unsigned>((A.J + kIlrmaNT - 1) / kIlrmaNT)),
+                             kIlrmaNT, 0, s>>>(A);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M) {
+  cudaError_t e = dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    k_ip<MM, kIlrmaNT><<<static_cast<unsigned>(A.I), kIlrmaNT, 0, s>>>(A);
+    return cudaGetLastError();
+  });
+  if (e != cudaSuccess) return e;
+  if ((e = launch_ilrma_powers(s, A, M)) != cudaSuccess) return e;
+  k_scale_mu<<<M, 512, 0, s>>>(A, ilrma_partials(A.I, A.J), M);
+  k_scale_apply<<<148 * 8, 256, 0, s>>>(A, M);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ilrma_inverse(cudaStream_t s, const IlrmaArgs& A, int M) {
+  return dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    k_demix_inv<MM><<<static_cast<unsigned>((A.I + 127) / 128), 128, 0, s>>>(A);
+    return cudaGetLastError();
+  });
+}
+
+}  // namespace rcscm

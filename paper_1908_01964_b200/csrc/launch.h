@@ -68,6 +68,27 @@ cudaError_t launch_transpose_c(cudaStream_t s, const double2* src, double2* dst,
                                bool to_bt);
 cudaError_t launch_fp64_probe(cudaStream_t s, int blocks, int iters, double* out);
 
+// ILRMA (ilrma.cu): sphering, NMF / IP sweeps, scale normalisation, inverses
+struct IlrmaArgs {
+  int64_t I, J;
+  int K;
+  const double2* X;  // [bin][t][m] (whitened)
+  double2* W;        // [bin][M*M]
+  double2* A;        // [bin][M*M]
+  double* T;         // [n][I x K col-major]
+  double* V;         // [n][K x J col-major]
+  double* P;         // [n][bin][t]
+  double* partial;   // [n][ilrma_partials(I, J)]
+  double* mu;        // [n]
+  unsigned long long* err;
+};
+int64_t ilrma_partials(int64_t I, int64_t J);
+cudaError_t launch_sphere(cudaStream_t s, int M, const double2* X, int64_t I, int64_t J, double2* Q, double2* Xw);
+cudaError_t launch_ilrma_powers(cudaStream_t s, const IlrmaArgs& A, int M);
+cudaError_t launch_ilrma_nmf(cudaStream_t s, const IlrmaArgs& A, int M);     // K <= 32
+cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M);  // IP sweep + powers + scaling
+cudaError_t launch_ilrma_inverse(cudaStream_t s, const IlrmaArgs& A, int M);
+
 // STFT (stft.cu): cached batched cuFFT plans (D2Z and Z2D of length n, batch rows)
 struct StftPlan {
   int fwd = 0, inv = 0;  // cufftHandle

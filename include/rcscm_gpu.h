@@ -16,6 +16,7 @@
  *   rcscm_gpu_stft_synthesize   replaces  stft_synthesize       stft.hpp:92-129
  *   rcscm_gpu_sphere            replaces  sphere                ilrma.hpp:53-73
  *   rcscm_gpu_run_ilrma         replaces  run_ilrma             ilrma.hpp:145-240
+ *   rcscm_gpu_extract           replaces  cmd_extract's pipeline tools/rcscm.cpp:158-221
  *
  * Plain pointers and sizes only; no CUDA or Eigen types cross the boundary.
  * Host buffers use the reference's Eigen column-major complex128 layouts:
@@ -189,6 +190,33 @@ int rcscm_gpu_sphere(rcscm_gpu_ctx* ctx, int64_t I, int64_t J, int M, const doub
 int rcscm_gpu_run_ilrma(rcscm_gpu_ctx* ctx, int64_t I, int64_t J, int M, int K,
                         int iters, uint64_t seed, const double* X, double* W, double* A,
                         double* T, double* V);
+
+/* ---- cmd_extract on the device (tools/rcscm.cpp:158-221) ------------------
+ * STFT -> sphering -> ILRMA -> fold (W = W_ilrma Q, A = W^{-1}) -> target index
+ * (select_target_index when target_index < 0) -> build_noise_scm -> init_params
+ * -> solver (backend 0 naive, 1 Algorithm 1, 2 Algorithm 2; optional objective
+ * per iteration with the rel_obj_tol early stop) -> extract_target / extract_noise
+ * -> WOLA synthesis, with every intermediate resident in HBM. samples, target and
+ * noise are M x num_samples col-major (Waveform::samples); target / noise may be NULL. */
+typedef struct {
+  double sample_rate, win_ms, hop_ms; /* 16000, 64, 32 in cmd_extract */
+  int nmf_bases, ilrma_iters;         /* RunConfig defaults 10, 50 */
+  uint64_t seed;
+  int target_index;                   /* < 0: select_target_index */
+  int backend;                        /* 0 naive, 1 accel1, 2 accel2 */
+  int iters;
+  double alpha, beta, eps_var, rel_obj_tol;
+  int compute_objective;              /* cmd_extract sets it */
+} rcscm_extract_opts;
+typedef struct {
+  int target_index, n_iters;
+  int64_t bins, frames;
+  double* objective;                  /* caller buffer, >= iters + 1 entries, or NULL */
+  int n_objective;
+} rcscm_extract_result;
+int rcscm_gpu_extract(rcscm_gpu_ctx* ctx, const rcscm_extract_opts* opts,
+                      const double* samples, int64_t num_samples, int M,
+                      double* target, double* noise, rcscm_extract_result* result);
 
 /* ---- device-resident session (bench / pipelines) -------------------------
  * A session keeps one problem (B utterances x I bins x J frames x M mics,

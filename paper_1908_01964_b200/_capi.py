@@ -82,6 +82,36 @@ class CResult(ctypes.Structure):
     ]
 
 
+class CExtractOpts(ctypes.Structure):
+    _fields_ = [
+        ("sample_rate", ctypes.c_double),
+        ("win_ms", ctypes.c_double),
+        ("hop_ms", ctypes.c_double),
+        ("nmf_bases", ctypes.c_int),
+        ("ilrma_iters", ctypes.c_int),
+        ("seed", ctypes.c_uint64),
+        ("target_index", ctypes.c_int),
+        ("backend", ctypes.c_int),
+        ("iters", ctypes.c_int),
+        ("alpha", ctypes.c_double),
+        ("beta", ctypes.c_double),
+        ("eps_var", ctypes.c_double),
+        ("rel_obj_tol", ctypes.c_double),
+        ("compute_objective", ctypes.c_int),
+    ]
+
+
+class CExtractResult(ctypes.Structure):
+    _fields_ = [
+        ("target_index", ctypes.c_int),
+        ("n_iters", ctypes.c_int),
+        ("bins", ctypes.c_int64),
+        ("frames", ctypes.c_int64),
+        ("objective", _dp),
+        ("n_objective", ctypes.c_int),
+    ]
+
+
 # Every symbol include/rcscm_gpu.h declares, with its ctypes signature.
 SIGNATURES = {
     "rcscm_gpu_create": (ctypes.c_int, [ctypes.POINTER(GpuConfig), ctypes.POINTER(_vp)]),
@@ -105,6 +135,8 @@ SIGNATURES = {
     "rcscm_gpu_stft_synthesize": (ctypes.c_int, [_vp, _dp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                                  ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                                                  ctypes.c_double, ctypes.c_double, _dp]),
+    "rcscm_gpu_extract": (ctypes.c_int, [_vp, ctypes.POINTER(CExtractOpts), _dp, ctypes.c_int64, ctypes.c_int, _dp,
+                                         _dp, ctypes.POINTER(CExtractResult)]),
     "rcscm_gpu_sphere": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, _dp, _dp, _dp]),
     "rcscm_gpu_run_ilrma": (ctypes.c_int, [_vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int,
                                            ctypes.c_int, ctypes.c_uint64, _dp, _dp, _dp, _dp, _dp]),

@@ -367,6 +367,32 @@ class GpuContext:
         tr = lambda m: np.ascontiguousarray(m.transpose(0, 2, 1))
         return tr(W), tr(A), tr(T), tr(V)
 
+    # ---- cmd_extract on the device (tools/rcscm.cpp:158-221) --------------------
+    def extract(self, samples, sample_rate: float = 16000.0, nmf_bases: int = 10, ilrma_iters: int = 50,
+                seed: int = 0, target_index: int = -1, backend: str = "accel2", iters: int = 100,
+                hyper: Optional["Hyperparams"] = None, eps_var: float = 1e-12, compute_objective: bool = True,
+                rel_obj_tol: float = 0.0, win_ms: float = 64.0, hop_ms: float = 32.0):
+        """STFT -> sphere -> ILRMA -> fold -> target index -> build_noise_scm ->
+        init_params -> solver -> Wiener image / noise -> WOLA synthesis, all on the
+        device. samples (M, len) -> dict(target, noise (M, len), target_index,
+        objective, n_iters)."""
+        hyper = hyper or Hyperparams()
+        x = np.asarray(samples, np.float64)
+        M, n = x.shape
+        xt = np.ascontiguousarray(x.T)
+        o = C.CExtractOpts(float(sample_rate), float(win_ms), float(hop_ms), int(nmf_bases), int(ilrma_iters),
+                           int(seed) & (2**64 - 1), int(target_index),
+                           {"naive": 0, "accel1": 1, "accel2": 2}[backend], int(iters), hyper.alpha, hyper.beta,
+                           float(eps_var), float(rel_obj_tol), int(bool(compute_objective)))
+        obj = np.zeros(max(iters, 0) + 1)
+        r = C.CExtractResult(0, 0, 0, 0, _p(obj), 0)
+        tgt = np.zeros((n, M))
+        noi = np.zeros((n, M))
+        _raise(self._lib.rcscm_gpu_extract(self._h, ctypes.byref(o), _p(xt), n, M, _p(tgt), _p(noi), ctypes.byref(r)))
+        return {"target": np.ascontiguousarray(tgt.T), "noise": np.ascontiguousarray(noi.T),
+                "target_index": r.target_index, "objective": obj[:r.n_objective].tolist(), "n_iters": r.n_iters,
+                "bins": r.bins, "frames": r.frames}
+
     # ---- device-resident session ---------------------------------------------
     def session_load(self, X, W, A, T, V, n_h: int = 0):
         """X (B, I, J, M); W, A (B, I, M, M); T (B, I, K); V (B, K, J)."""

@@ -90,6 +90,8 @@ struct rcscm_gpu_ctx {
   DBuf st_x, st_w, st_f, st_spec, st_X;
   // ILRMA: whitened x, W, A, T, V, powers, partial sums, mu
   DBuf il_X, il_W, il_A, il_T, il_V, il_P, il_part, il_mu;
+  // extract pipeline: whitening Q, folded W / A, target powers, output waveform
+  DBuf ex_Q, ex_W, ex_A, ex_pow, ex_out;
   StftPlan stft_plan;
   // complex64 (FP32) mode copies of the slot arrays
   DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef, rh0f, ru0f;
@@ -852,7 +854,8 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->gam, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
                   &c->dryf, &c->imagef, &c->rh0f, &c->ru0f, &c->st_x, &c->st_w, &c->st_f, &c->st_spec,
-                  &c->st_X, &c->il_X, &c->il_W, &c->il_A, &c->il_T, &c->il_V, &c->il_P, &c->il_part, &c->il_mu})
+                  &c->st_X, &c->il_X, &c->il_W, &c->il_A, &c->il_T, &c->il_V, &c->il_P, &c->il_part, &c->il_mu,
+                  &c->ex_Q, &c->ex_W, &c->ex_A, &c->ex_pow, &c->ex_out})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1010,6 +1013,42 @@ int rcscm_gpu_stft_shape(int64_t num_samples, double sample_rate, double win_ms,
   });
 }
 
+// device STFT of the device waveform dx (M x len) into c->st_X ([bin][frame][mic])
+static void stft_analyze_dev(rcscm_gpu_ctx* c, const double* dx, int64_t len, int M, double sample_rate,
+                             double win_ms, double hop_ms, int* win_o, int* hop_o, int64_t* J_o, int64_t* B_o) {
+  int win = 0, hop = 0;
+  stft_params(sample_rate, win_ms, hop_ms, &win, &hop);
+  const int64_t J = (len + (win - hop) + hop - 1) / hop, B = win / 2 + 1, rows = J * M;
+  const std::vector<double> w = hamming(win);
+  double* dw = c->st_w.get<double>(win);
+  h2d(c, dw, w.data(), win * sizeof(double));
+  double2* dX = c->st_X.get<double2>(static_cast<size_t>(B * rows));
+  c->launched(launch_stft_analyze(c->stream, c->stft_plan, dx, len, M, win, hop, J, dw,
+                                  c->st_f.get<double>(static_cast<size_t>(rows) * win),
+                                  c->st_spec.get<double2>(static_cast<size_t>(rows * B)), dX),
+              3);
+  *win_o = win;
+  *hop_o = hop;
+  *J_o = J;
+  *B_o = B;
+}
+
+// device WOLA synthesis of dX ([bin][frame][mic], I = win/2 + 1 bins) into dout (M x len)
+static void stft_synth_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64_t J, int M, int win, int hop,
+                           int64_t len, double* dout) {
+  const std::vector<double> w = hamming(win);
+  std::vector<double> denom(hop, 0.0), dual(win);
+  for (int k = 0; k < win; ++k) denom[k % hop] += w[k] * w[k];
+  for (int k = 0; k < win; ++k) dual[k] = (w[k] / denom[k % hop]) / win;  // wola_dual_window / win
+  double* dd = c->st_w.get<double>(win);
+  h2d(c, dd, dual.data(), win * sizeof(double));
+  const int64_t rows = J * M;
+  c->launched(launch_stft_synthesize(c->stream, c->stft_plan, dX, I, J, M, win, hop, len, dd,
+                                     c->st_spec.get<double2>(static_cast<size_t>(rows * I)),
+                                     c->st_f.get<double>(static_cast<size_t>(rows) * win), dout),
+              4);
+}
+
 int rcscm_gpu_stft_analyze(rcscm_gpu_ctx* c, const double* samples, int64_t num_samples, int M, double sample_rate,
                            double win_ms, double hop_ms, double* X) {
   return guarded([&] {
@@ -1018,18 +1057,11 @@ int rcscm_gpu_stft_analyze(rcscm_gpu_ctx* c, const double* samples, int64_t num_
     if (!samples || !X) fail(RCSCM_INVALID_INPUT, "stft_analyze: NULL buffer");
     int win = 0, hop = 0;
     stft_params(sample_rate, win_ms, hop_ms, &win, &hop);
-    const int64_t J = (num_samples + (win - hop) + hop - 1) / hop, B = win / 2 + 1, rows = J * M;
-    const std::vector<double> w = hamming(win);
     double* dx = c->st_x.get<double>(static_cast<size_t>(num_samples) * M);
-    double* dw = c->st_w.get<double>(win);
     h2d(c, dx, samples, static_cast<size_t>(num_samples) * M * sizeof(double));
-    h2d(c, dw, w.data(), win * sizeof(double));
-    double2* dX = c->st_X.get<double2>(static_cast<size_t>(B * rows));
-    c->launched(launch_stft_analyze(c->stream, c->stft_plan, dx, num_samples, M, win, hop, J, dw,
-                                    c->st_f.get<double>(static_cast<size_t>(rows) * win),
-                                    c->st_spec.get<double2>(static_cast<size_t>(rows * B)), dX),
-                3);
-    d2h(c, X, dX, static_cast<size_t>(B * rows) * sizeof(double2));
+    int64_t J = 0, B = 0;
+    stft_analyze_dev(c, dx, num_samples, M, sample_rate, win_ms, hop_ms, &win, &hop, &J, &B);
+    d2h(c, X, c->st_X.p, static_cast<size_t>(B * J * M) * sizeof(double2));
     sync(c);
   });
 }
@@ -1049,21 +1081,11 @@ int rcscm_gpu_stft_synthesize(rcscm_gpu_ctx* c, const double* X, int64_t I, int6
     const int64_t len = source_samples > 0 ? source_samples : J * hop - pad;
     if (len <= 0 || M <= 0 || J <= 0) fail(RCSCM_INVALID_INPUT, "stft_synthesize: empty spectrogram");
     if (!X || !samples) fail(RCSCM_INVALID_INPUT, "stft_synthesize: NULL buffer");
-    // wola_dual_window (stft.hpp:22-29), divided by win for the unnormalised inverse DFT
-    const std::vector<double> w = hamming(win);
-    std::vector<double> denom(hop, 0.0), dual(win);
-    for (int k = 0; k < win; ++k) denom[k % hop] += w[k] * w[k];
-    for (int k = 0; k < win; ++k) dual[k] = (w[k] / denom[k % hop]) / win;
     const int64_t rows = J * M;
     double2* dX = c->st_X.get<double2>(static_cast<size_t>(I * rows));
     h2d(c, dX, X, static_cast<size_t>(I * rows) * sizeof(double2));
-    double* dd = c->st_w.get<double>(win);
-    h2d(c, dd, dual.data(), win * sizeof(double));
     double* dout = c->st_x.get<double>(static_cast<size_t>(len) * M);
-    c->launched(launch_stft_synthesize(c->stream, c->stft_plan, dX, I, J, M, win, hop, len, dd,
-                                       c->st_spec.get<double2>(static_cast<size_t>(rows * I)),
-                                       c->st_f.get<double>(static_cast<size_t>(rows) * win), dout),
-                4);
+    stft_synth_dev(c, dX, I, J, M, win, hop, len, dout);
     d2h(c, samples, dout, static_cast<size_t>(len) * M * sizeof(double));
     sync(c);
   });
@@ -1089,6 +1111,59 @@ int rcscm_gpu_sphere(rcscm_gpu_ctx* c, int64_t I, int64_t J, int M, const double
   });
 }
 
+// run_ilrma on the device-resident (whitened) dX; results stay in c->il_* (W, A, T, V)
+static IlrmaArgs ilrma_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64_t J, int M, int K, int iters,
+                           uint64_t seed) {
+  if (K < 1) fail(RCSCM_INVALID_INPUT, "run_ilrma: K must be >= 1");
+  if (iters < 0) fail(RCSCM_INVALID_INPUT, "run_ilrma: iters must be >= 0");
+  check_mics(M);
+  if (K > 32) fail(RCSCM_UNSUPPORTED, "run_ilrma: K > 32 NMF bases is not supported on the GPU");
+  const size_t S = static_cast<size_t>(I * J);
+  // NMF initialisation exactly as the reference (ilrma.hpp:162-173): one
+  // mt19937_64 stream, per source T row-major over (i, k) then V over (k, t)
+  std::vector<double> hT(static_cast<size_t>(M) * I * K), hV(static_cast<size_t>(M) * K * J);
+  std::mt19937_64 rng(seed);
+  std::uniform_real_distribution<double> unif(0.1, 1.0);
+  for (int n = 0; n < M; ++n) {
+    double* Tn = hT.data() + static_cast<size_t>(n) * I * K;
+    double* Vn = hV.data() + static_cast<size_t>(n) * K * J;
+    for (int64_t i = 0; i < I; ++i)
+      for (int k = 0; k < K; ++k) Tn[i + k * I] = unif(rng);
+    for (int k = 0; k < K; ++k)
+      for (int64_t t = 0; t < J; ++t) Vn[k + t * K] = unif(rng);
+  }
+  std::vector<double> eye(static_cast<size_t>(I) * M * M * 2, 0.0);
+  for (int64_t i = 0; i < I; ++i)
+    for (int r = 0; r < M; ++r) eye[2 * (i * M * M + r + r * M)] = 1.0;
+  IlrmaArgs a{};
+  a.I = I;
+  a.J = J;
+  a.K = K;
+  a.X = dX;
+  a.W = c->il_W.get<double2>(static_cast<size_t>(I) * M * M);
+  a.A = c->il_A.get<double2>(static_cast<size_t>(I) * M * M);
+  a.T = c->il_T.get<double>(hT.size());
+  a.V = c->il_V.get<double>(hV.size());
+  a.P = c->il_P.get<double>(S * M);
+  a.partial = c->il_part.get<double>(static_cast<size_t>(ilrma_partials(I, J)) * M);
+  a.mu = c->il_mu.get<double>(M);
+  a.err = c->err.get<unsigned long long>(1);
+  if (I == 0) return a;
+  h2d(c, a.W, eye.data(), eye.size() * sizeof(double));
+  h2d(c, a.T, hT.data(), hT.size() * sizeof(double));
+  h2d(c, a.V, hV.data(), hV.size() * sizeof(double));
+  reset_err(c);
+  c->launched(launch_ilrma_powers(c->stream, a, M));
+  for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
+  for (int it = 0; it < iters; ++it) {
+    c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
+    c->launched(launch_ilrma_ip_scale(c->stream, a, M), 4);
+  }
+  c->launched(launch_ilrma_inverse(c->stream, a, M));
+  check_err(c, J > 0 ? J : 1);
+  return a;
+}
+
 int rcscm_gpu_run_ilrma(rcscm_gpu_ctx* c, int64_t I, int64_t J, int M, int K, int iters, uint64_t seed,
                         const double* X, double* W, double* A, double* T, double* V) {
   return guarded([&] {
@@ -1096,65 +1171,24 @@ int rcscm_gpu_run_ilrma(rcscm_gpu_ctx* c, int64_t I, int64_t J, int M, int K, in
     if (K < 1) fail(RCSCM_INVALID_INPUT, "run_ilrma: K must be >= 1");
     if (iters < 0) fail(RCSCM_INVALID_INPUT, "run_ilrma: iters must be >= 0");
     if (I < 0 || J < 0 || M < 1) fail(RCSCM_INVALID_INPUT, "run_ilrma: bad shape");
-    check_mics(M);
-    if (K > 32) fail(RCSCM_UNSUPPORTED, "run_ilrma: K > 32 NMF bases is not supported on the GPU");
     const size_t S = static_cast<size_t>(I * J);
-    // NMF initialisation exactly as the reference (ilrma.hpp:162-173): one
-    // mt19937_64 stream, per source T row-major over (i, k) then V over (k, t)
-    std::vector<double> hT(static_cast<size_t>(M) * I * K), hV(static_cast<size_t>(M) * K * J);
-    std::mt19937_64 rng(seed);
-    std::uniform_real_distribution<double> unif(0.1, 1.0);
-    for (int n = 0; n < M; ++n) {
-      double* Tn = hT.data() + static_cast<size_t>(n) * I * K;
-      double* Vn = hV.data() + static_cast<size_t>(n) * K * J;
-      for (int64_t i = 0; i < I; ++i)
-        for (int k = 0; k < K; ++k) Tn[i + k * I] = unif(rng);
-      for (int k = 0; k < K; ++k)
-        for (int64_t t = 0; t < J; ++t) Vn[k + t * K] = unif(rng);
-    }
-    std::vector<double> eye(static_cast<size_t>(I) * M * M * 2, 0.0);
-    for (int64_t i = 0; i < I; ++i)
-      for (int r = 0; r < M; ++r) eye[2 * (i * M * M + r + r * M)] = 1.0;
-    if (I == 0) return;
-    IlrmaArgs a{};
-    a.I = I;
-    a.J = J;
-    a.K = K;
     double2* dX = c->il_X.get<double2>(S * M);
-    h2d(c, dX, X, S * M * sizeof(double2));
-    a.X = dX;
-    a.W = c->il_W.get<double2>(static_cast<size_t>(I) * M * M);
-    a.A = c->il_A.get<double2>(static_cast<size_t>(I) * M * M);
-    a.T = c->il_T.get<double>(hT.size());
-    a.V = c->il_V.get<double>(hV.size());
-    a.P = c->il_P.get<double>(S * M);
-    a.partial = c->il_part.get<double>(static_cast<size_t>(ilrma_partials(I, J)) * M);
-    a.mu = c->il_mu.get<double>(M);
-    a.err = c->err.get<unsigned long long>(1);
-    h2d(c, a.W, eye.data(), eye.size() * sizeof(double));
-    h2d(c, a.T, hT.data(), hT.size() * sizeof(double));
-    h2d(c, a.V, hV.data(), hV.size() * sizeof(double));
-    reset_err(c);
-    c->launched(launch_ilrma_powers(c->stream, a, M));
-    for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
-    for (int it = 0; it < iters; ++it) {
-      c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
-      c->launched(launch_ilrma_ip_scale(c->stream, a, M), 4);
-    }
-    c->launched(launch_ilrma_inverse(c->stream, a, M));
-    check_err(c, J > 0 ? J : 1);
+    if (S) h2d(c, dX, X, S * M * sizeof(double2));
+    const IlrmaArgs a = ilrma_dev(c, dX, I, J, M, K, iters, seed);
+    if (I == 0) return;
     if (W) d2h(c, W, a.W, static_cast<size_t>(I) * M * M * sizeof(double2));
     if (A) d2h(c, A, a.A, static_cast<size_t>(I) * M * M * sizeof(double2));
-    if (T) d2h(c, T, a.T, hT.size() * sizeof(double));
-    if (V) d2h(c, V, a.V, hV.size() * sizeof(double));
+    if (T) d2h(c, T, a.T, static_cast<size_t>(M) * I * K * sizeof(double));
+    if (V) d2h(c, V, a.V, static_cast<size_t>(M) * K * J * sizeof(double));
     sync(c);
   });
 }
 
 // ---- session ------------------------------------------------------------------
-int rcscm_gpu_session_load(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M, int K, int n_h, const double* X,
-                           const double* W, const double* A, const double* T, const double* V) {
-  return guarded([&] {
+// session_load from host (H2D) or device (D2D) buffers
+static void session_load_impl(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M, int K, int n_h,
+                              const void* X, const void* W, const void* A, const void* T, const void* V,
+                              cudaMemcpyKind kind) {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
     if (B < 1 || I < 1 || J < 1 || M < 1 || K < 0) fail(RCSCM_INVALID_INPUT, "session_load: bad shape");
     if (n_h < 0 || n_h >= M) fail(RCSCM_INVALID_INPUT, "session_load: target index out of range");
@@ -1172,11 +1206,14 @@ int rcscm_gpu_session_load(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, in
     c->dry.get<double2>(S);
     c->image.get<double2>(S * M);
     c->scratch.get<double2>(S);
-    h2d(c, c->X.p, X, S * M * sizeof(double2));
-    h2d(c, c->W.p, W, nb * M * M * sizeof(double2));
-    h2d(c, c->A.p, A, nb * M * M * sizeof(double2));
-    h2d(c, c->T.p, T, B * I * K * sizeof(double));
-    h2d(c, c->V.p, V, B * K * J * sizeof(double));
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes && dst != src) CK(cudaMemcpyAsync(dst, src, bytes, kind, c->stream));
+    };
+    cp(c->X.p, X, S * M * sizeof(double2));
+    cp(c->W.p, W, nb * M * M * sizeof(double2));
+    cp(c->A.p, A, nb * M * M * sizeof(double2));
+    cp(c->T.p, T, B * I * K * sizeof(double));
+    cp(c->V.p, V, B * K * J * sizeof(double));
     if (f32(c)) {
       alloc_f32(c, nb, J, M);
       c->dryf.get<float2>(S);
@@ -1196,7 +1233,11 @@ int rcscm_gpu_session_load(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, in
     c->s_reset_pending = false;
     reset_err(c);
     sync(c);
-  });
+}
+
+int rcscm_gpu_session_load(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M, int K, int n_h, const double* X,
+                           const double* W, const double* A, const double* T, const double* V) {
+  return guarded([&] { session_load_impl(c, B, I, J, M, K, n_h, X, W, A, T, V, cudaMemcpyHostToDevice); });
 }
 
 // Applies a pending RESET to the working iterate (rh, ru, lam and the FP32 copies).
@@ -1359,6 +1400,129 @@ static int probe(rcscm_gpu_ctx* c, bool fp32, double* tflops, double* ms) {
     const double flops = 2.0 * kNacc * static_cast<double>(iters) * blocks * kNt;
     *tflops = flops / (t * 1e-3) / 1e12;
     if (ms) *ms = t;
+  });
+}
+
+// ---- cmd_extract on the device (tools/rcscm.cpp:158-221) ---------------------------
+int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const double* samples, int64_t num_samples,
+                      int M, double* target, double* noise, rcscm_extract_result* res) {
+  return guarded([&] {
+    if (!c || !o || !samples) fail(RCSCM_INVALID_INPUT, "extract: NULL argument");
+    if (num_samples <= 0 || M <= 0) fail(RCSCM_INVALID_INPUT, "stft_analyze: empty waveform");
+    if (o->iters < 0) fail(RCSCM_INVALID_INPUT, "run_accelerated: iters must be >= 0");
+    if (o->backend < 0 || o->backend > 2) fail(RCSCM_INVALID_INPUT, "extract: unknown backend");
+    check_mics(M);
+    const rcscm_hyper h{o->alpha, o->beta};
+    // 1. STFT (stft.hpp:50-88)
+    double* dx = c->st_x.get<double>(static_cast<size_t>(num_samples) * M);
+    h2d(c, dx, samples, static_cast<size_t>(num_samples) * M * sizeof(double));
+    int win = 0, hop = 0;
+    int64_t J = 0, I = 0;
+    stft_analyze_dev(c, dx, num_samples, M, o->sample_rate, o->win_ms, o->hop_ms, &win, &hop, &J, &I);
+    const size_t S = static_cast<size_t>(I * J);
+    const double2* dX = c->st_X.as<double2>();
+    // 2. sphering + ILRMA in the whitened domain (ilrma.hpp:53-73, :145-240)
+    if (J <= M) fail(RCSCM_INVALID_INPUT, "sphere: need more frames than channels");
+    double2* dQ = c->ex_Q.get<double2>(static_cast<size_t>(I) * M * M);
+    double2* dXw = c->il_X.get<double2>(S * M);
+    c->launched(launch_sphere(c->stream, M, dX, I, J, dQ, dXw));
+    IlrmaArgs a = ilrma_dev(c, dXw, I, J, M, o->nmf_bases, o->ilrma_iters, o->seed);
+    // 3. fold the whitening back: W = W_ilrma Q, A = W^{-1} (tools/rcscm.cpp:176-180)
+    double2* dW = c->ex_W.get<double2>(static_cast<size_t>(I) * M * M);
+    double2* dA = c->ex_A.get<double2>(static_cast<size_t>(I) * M * M);
+    c->launched(launch_ilrma_fold(c->stream, a, M, dQ, dW, dA));
+    check_err(c, J);
+    // 4. target index (model.hpp:43-54) unless given
+    int n_h = o->target_index;
+    if (n_h >= M) fail(RCSCM_INVALID_INPUT, "extract: target index out of range");
+    if (n_h < 0) {
+      double* dp = c->ex_pow.get<double>(static_cast<size_t>(M) * I);
+      c->launched(launch_target_power(c->stream, M, dX, dW, dA, I, J, dp));
+      std::vector<double> pw(static_cast<size_t>(M) * I);
+      d2h(c, pw.data(), dp, pw.size() * sizeof(double));
+      sync(c);
+      double best = -1.0;
+      for (int n = 0; n < M; ++n) {
+        double p = 0.0;
+        for (int64_t i = 0; i < I; ++i) p += pw[n * I + i];
+        if (p > best) {
+          best = p;
+          n_h = n;
+        }
+      }
+    }
+    // 5. build_noise_scm + init_params on the device (model.hpp:58-124): the
+    //    session's SETUP with T[n_h], V[n_h]
+    const int K = o->nmf_bases;
+    session_load_impl(c, 1, I, J, M, K, n_h, dX, dW, dA, a.T + static_cast<size_t>(n_h) * I * K,
+                      a.V + static_cast<size_t>(n_h) * K * J, cudaMemcpyDeviceToDevice);
+    int rc = rcscm_gpu_session_run(c, RCSCM_STAGE_SETUP | RCSCM_STAGE_PRECOMPUTE, 0, &h, o->eps_var);
+    if (rc != RCSCM_OK) fail(rc, rcscm_gpu_last_error());
+    // 6. the solver (tools/rcscm.cpp:135-142, 184-190)
+    std::vector<double> objv;
+    const bool want_obj = o->compute_objective != 0;
+    auto eval = [&] {
+      return o->backend == 2 ? objective_fast(c, I, J, M, h) : objective(c, I, J, M, h);
+    };
+    if (want_obj && o->backend == 2) c->launched(launch_logpdet(c->stream, problem(c, 1, I, J, M)));
+    if (want_obj) objv.push_back(eval());
+    const int step = want_obj ? 1 : o->iters;
+    int done = 0;
+    while (done < o->iters) {
+      const int n = std::min(step, o->iters - done);
+      if (o->backend == 2) {
+        rc = rcscm_gpu_session_run(c, RCSCM_STAGE_ACCEL, n, &h, o->eps_var);
+        if (rc != RCSCM_OK) fail(rc, rcscm_gpu_last_error());
+        if (f32(c)) params_from_f32(c, S);
+      } else if (o->backend == 0) {
+        rc = rcscm_gpu_session_run(c, RCSCM_STAGE_NAIVE, n, &h, o->eps_var);
+        if (rc != RCSCM_OK) fail(rc, rcscm_gpu_last_error());
+      } else {
+        c->launched(launch_accel1(c->stream, M, accel1_args(c, I, J, n, h, o->eps_var, 0.0)));
+      }
+      done += n;
+      if (want_obj) {
+        objv.push_back(eval());
+        const double prev = objv[objv.size() - 2], cur = objv.back();
+        if (o->rel_obj_tol > 0.0 && std::abs(cur - prev) <= o->rel_obj_tol * std::abs(prev)) break;
+      }
+    }
+    check_err(c, J);
+    // 7. Wiener image and noise (wiener.hpp:19-53), then WOLA synthesis of both
+    WienerArgs Wa{};
+    Wa.nb = I;
+    Wa.J = J;
+    Wa.X = c->X.as<double2>();
+    Wa.a = c->a.as<double2>();
+    Wa.b = c->b.as<double2>();
+    Wa.Rpp = c->Rpp.as<double2>();
+    Wa.r_h = c->rh.as<double>();
+    Wa.r_u = c->ru.as<double>();
+    Wa.lambda = c->lam.as<double>();
+    Wa.dry = c->dry.get<double2>(S);
+    Wa.image = c->image.get<double2>(S * M);
+    Wa.noise = c->noise.get<double2>(S * M);
+    c->launched(launch_wiener(c->stream, M, Wa, true, true));
+    double* dout = c->ex_out.get<double>(static_cast<size_t>(num_samples) * M);
+    if (target) {
+      stft_synth_dev(c, Wa.image, I, J, M, win, hop, num_samples, dout);
+      d2h(c, target, dout, static_cast<size_t>(num_samples) * M * sizeof(double));
+    }
+    if (noise) {
+      sync(c);
+      stft_synth_dev(c, Wa.noise, I, J, M, win, hop, num_samples, dout);
+      d2h(c, noise, dout, static_cast<size_t>(num_samples) * M * sizeof(double));
+    }
+    sync(c);
+    if (res) {
+      res->target_index = n_h;
+      res->n_iters = done;
+      res->bins = I;
+      res->frames = J;
+      if (res->objective && want_obj)
+        std::memcpy(res->objective, objv.data(), objv.size() * sizeof(double));
+      res->n_objective = static_cast<int>(objv.size());
+    }
   });
 }
 

@@ -470,6 +470,68 @@ __global__ void k_demix_inv(IlrmaArgs A) {
   }
 }
 
+// ---- fold + target selection (tools/rcscm.cpp:173-181, model.hpp:43-54) -----------
+// W_i = W_ilrma,i Q_i (back to the observation domain), A_i = W_i^{-1}
+template <int M>
+__global__ void k_fold(IlrmaArgs A, const double2* __restrict__ Q, double2* __restrict__ Wout,
+                       double2* __restrict__ Aout) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= A.I) return;
+  double2 W[M * M], lu[M * M];
+  for (int c = 0; c < M; ++c)
+    for (int r = 0; r < M; ++r) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int k = 0; k < M; ++k) s = cfma(A.W[i * M * M + r + k * M], Q[i * M * M + k + c * M], s);
+      W[r + c * M] = s;
+      lu[r + c * M] = s;
+    }
+  DevFullPivLU<M> f;
+  f.compute(lu, M);
+  if (!f.invertible(lu)) {
+    report_error(A.err, i * A.J, kErrIlrmaDemix);
+    return;
+  }
+  for (int k = 0; k < M * M; ++k) Wout[i * M * M + k] = W[k];
+  for (int c = 0; c < M; ++c) {
+    double2 e[M];
+    for (int r = 0; r < M; ++r) e[r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    f.solve(lu, e);
+    for (int r = 0; r < M; ++r) Aout[i * M * M + r + c * M] = e[r];
+  }
+}
+
+// power[n][i] = ||(W_i X_i)_n||^2 ||A_i(:, n)||^2 (select_target_index, per bin)
+template <int M, int NT>
+__global__ void __launch_bounds__(NT) k_target_power(const double2* __restrict__ X, const double2* __restrict__ W,
+                                                     const double2* __restrict__ Am, int64_t I, int64_t J,
+                                                     double* __restrict__ power) {
+  __shared__ double red[NT / 32 * M];
+  __shared__ double tot[M];
+  const int64_t i = blockIdx.x;
+  double acc[M];
+#pragma unroll
+  for (int n = 0; n < M; ++n) acc[n] = 0.0;
+  for (int64_t t = threadIdx.x; t < J; t += NT) {
+    double2 x[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) x[m] = X[(i * J + t) * M + m];
+#pragma unroll
+    for (int n = 0; n < M; ++n) {
+      double2 y = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < M; ++c) y = cfma(W[i * M * M + n + c * M], x[c], y);
+      acc[n] += cnorm(y);
+    }
+  }
+  block_sum<NT, M>(acc, red, tot);
+  if (threadIdx.x < M) {
+    const int n = threadIdx.x;
+    double a2 = 0.0;
+    for (int r = 0; r < M; ++r) a2 += cnorm(Am[i * M * M + r + n * M]);
+    power[n * I + i] = tot[n] * a2;
+  }
+}
+
 // ---- launchers -------------------------------------------------------------------
 constexpr int kIlrmaNT = 128;
 
@@ -519,6 +581,23 @@ cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M) {
   k_scale_mu<<<M, 512, 0, s>>>(A, ilrma_partials(A.I, A.J), M);
   k_scale_apply<<<148 * 8, 256, 0, s>>>(A, M);
   return cudaGetLastError();
+}
+
+cudaError_t launch_ilrma_fold(cudaStream_t s, const IlrmaArgs& A, int M, const double2* Q, double2* W, double2* Am) {
+  return dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    k_fold<MM><<<static_cast<unsigned>((A.I + 127) / 128), 128, 0, s>>>(A, Q, W, Am);
+    return cudaGetLastError();
+  });
+}
+
+cudaError_t launch_target_power(cudaStream_t s, int M, const double2* X, const double2* W, const double2* Am,
+                                int64_t I, int64_t J, double* power) {
+  return dispatch_mics(M, [&](auto mm) {
+    constexpr int MM = decltype(mm)::value;
+    k_target_power<MM, kIlrmaNT><<<static_cast<unsigned>(I), kIlrmaNT, 0, s>>>(X, W, Am, I, J, power);
+    return cudaGetLastError();
+  });
 }
 
 cudaError_t launch_ilrma_inverse(cudaStream_t s, const IlrmaArgs& A, int M) {

@@ -88,6 +88,11 @@ cudaError_t launch_ilrma_powers(cudaStream_t s, const IlrmaArgs& A, int M);
 cudaError_t launch_ilrma_nmf(cudaStream_t s, const IlrmaArgs& A, int M);     // K <= 32
 cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M);  // IP sweep + powers + scaling
 cudaError_t launch_ilrma_inverse(cudaStream_t s, const IlrmaArgs& A, int M);
+// W = W_ilrma Q, Am = W^{-1} per bin (A.W holds W_ilrma)
+cudaError_t launch_ilrma_fold(cudaStream_t s, const IlrmaArgs& A, int M, const double2* Q, double2* W, double2* Am);
+// power[n][i] = ||(W_i X_i)_n||^2 ||Am_i(:, n)||^2
+cudaError_t launch_target_power(cudaStream_t s, int M, const double2* X, const double2* W, const double2* Am,
+                                int64_t I, int64_t J, double* power);
 
 // STFT (stft.cu): cached batched cuFFT plans (D2Z and Z2D of length n, batch rows)
 struct StftPlan {

@@ -24,7 +24,10 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
   for (int cl : {1, 2, 4, 8, 16}) {
     if (force_cl && cl != force_cl) continue;
     const int64_t jc = (J + cl - 1) / cl;
-    const int max_spt = (cl == 16 || f32) ? 8 : 6;  // FP32 state takes half the registers
+    // FP32 state takes half the registers; clusters are bound by the per-iteration
+    // DSMEM exchange, so the fewest CTAs per bin win (measured on B200: J = 4096
+    // runs 33 % faster as 2 CTAs x 8 slots/thread than as 4 x 4)
+    const int max_spt = (cl >= 2 || f32) ? 8 : 6;
     if (jc > 256LL * (force_spt ? force_spt : max_spt)) continue;
     int64_t best_waste = -1;
     for (int spt = 1; spt <= 8; ++spt) {

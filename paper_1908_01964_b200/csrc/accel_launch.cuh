@@ -73,6 +73,14 @@ cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& 
       if (g.smem == 0) return launch_accel_spt<CL, true, false, 0, 3, true>(s, A, g.nt, g.spt);
     }
   }
+  if (g.direct) {  // r_u from rho(lambda_new) after the reduction (the faster form on B200)
+    if (g.smem) {
+      if (g.full) return launch_accel_spt<CL, true, false, 1, 0, true>(s, A, g.nt, g.spt);
+      return launch_accel_spt<CL, false, false, 1, 0, true>(s, A, g.nt, g.spt);
+    }
+    if (g.full) return launch_accel_spt<CL, true, false, 0, 0, true>(s, A, g.nt, g.spt);
+    return launch_accel_spt<CL, false, false, 0, 0, true>(s, A, g.nt, g.spt);
+  }
   if (g.smem) {
     if (g.full) return launch_accel_spt<CL, true, false, 1>(s, A, g.nt, g.spt);
     return launch_accel_spt<CL, false, false, 1>(s, A, g.nt, g.spt);

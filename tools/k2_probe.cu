@@ -60,19 +60,24 @@ int main(int argc, char** argv) {
 #define K2_SPT 5
 #define K2_MINB 3
 #endif
+#ifndef K2_SMEMC
+#define K2_SMEMC 0
+#endif
     const int nt = J / K2_SPT;
-    auto kern = k_accel<K2_SPT, 1, true, false, 0, K2_MINB, true, double>;
+    auto kern = k_accel<K2_SPT, 1, true, false, K2_SMEMC, K2_MINB, true, double>;
+    const size_t dsm = K2_SMEMC ? static_cast<size_t>(K2_SPT) * nt * (K2_SMEMC == 1 ? 6 : 4) * sizeof(double) : 0;
+    if (dsm) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsm)));
 #ifdef RCSCM_K2_STAGGER
     CK(cudaMemcpyToSymbol(g_k2_stagger, &st, sizeof(st)));
     std::vector<unsigned> zero(256, 0);
 #endif
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    for (int r = 0; r < 3; ++r) kern<<<nb, nt>>>(A);
+    for (int r = 0; r < 3; ++r) kern<<<nb, nt, dsm>>>(A);
 #ifdef RCSCM_K2_STAGGER
     CK(cudaMemcpyToSymbol(g_k2_smcount, zero.data(), 256 * sizeof(unsigned)));
 #endif
     cudaEventRecord(e0);
-    kern<<<nb, nt>>>(A);
+    kern<<<nb, nt, dsm>>>(A);
     cudaEventRecord(e1);
     CK(cudaDeviceSynchronize());
     float ms; cudaEventElapsedTime(&ms, e0, e1);

@@ -89,9 +89,10 @@ struct rcscm_gpu_ctx {
   // STFT: waveform, window table, frames, half spectra, Spectrogram
   DBuf st_x, st_w, st_f, st_spec, st_X;
   // ILRMA: whitened x, W, A, T, V, powers, partial sums, mu
-  DBuf il_X, il_W, il_A, il_T, il_V, il_P, il_part, il_mu;
-  // extract pipeline: whitening Q, folded W / A, target powers, output waveform
-  DBuf ex_Q, ex_W, ex_A, ex_pow, ex_out;
+  DBuf il_X, il_W, il_A, il_T, il_V, il_P, il_part, il_mu, il_vpart;
+  // extract pipeline: whitening Q, folded W / A, target powers, output waveform,
+  // objective trace
+  DBuf ex_Q, ex_W, ex_A, ex_pow, ex_out, ex_obj;
   StftPlan stft_plan;
   // complex64 (FP32) mode copies of the slot arrays
   DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef, rh0f, ru0f;
@@ -392,7 +393,8 @@ NaiveArgs naive_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int iters, const r
 }
 
 // Objective of the current device state -> host double (synchronizes).
-double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h) {
+// dev_out: leave the value in that device slot (no host round trip; returns 0)
+double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h, double* dev_out = nullptr) {
   if (nb * J == 0) return 0.0;
   ObjArgs O{};
   O.nb = nb;
@@ -410,8 +412,9 @@ double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyp
   O.err = c->err.as<unsigned long long>();
   int64_t np = 0;
   c->launched(launch_objective(c->stream, M, O, &np));
-  double* out = c->obj.get<double>(1);
+  double* out = dev_out ? dev_out : c->obj.get<double>(1);
   c->launched(launch_sum_partials(c->stream, O.partial, np, out));
+  if (dev_out) return 0.0;
   double v = 0.0;
   d2h(c, &v, out, sizeof(double));
   check_err(c, J);
@@ -420,7 +423,8 @@ double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyp
 
 // O(1)-per-slot objective from the resident sigma/tau precompute (needs
 // logpdet, see launch_logpdet); synchronizes.
-double objective_fast(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h) {
+// dev_out: leave the value in that device slot (no host round trip; returns 0)
+double objective_fast(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h, double* dev_out = nullptr) {
   if (nb * J == 0) return 0.0;
   ObjFastArgs O{};
   O.nb = nb;
@@ -441,8 +445,9 @@ double objective_fast(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcsc
   O.err = c->err.as<unsigned long long>();
   int64_t np = 0;
   c->launched(launch_objective_fast(c->stream, O, &np));
-  double* out = c->obj.get<double>(1);
+  double* out = dev_out ? dev_out : c->obj.get<double>(1);
   c->launched(launch_sum_partials(c->stream, O.partial, np, out));
+  if (dev_out) return 0.0;
   double v = 0.0;
   d2h(c, &v, out, sizeof(double));
   check_err(c, J);
@@ -854,8 +859,8 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->gam, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
                   &c->dryf, &c->imagef, &c->rh0f, &c->ru0f, &c->st_x, &c->st_w, &c->st_f, &c->st_spec,
-                  &c->st_X, &c->il_X, &c->il_W, &c->il_A, &c->il_T, &c->il_V, &c->il_P, &c->il_part, &c->il_mu,
-                  &c->ex_Q, &c->ex_W, &c->ex_A, &c->ex_pow, &c->ex_out})
+                  &c->st_X, &c->il_X, &c->il_W, &c->il_A, &c->il_T, &c->il_V, &c->il_P, &c->il_part, &c->il_mu, &c->il_vpart,
+                  &c->ex_Q, &c->ex_W, &c->ex_A, &c->ex_pow, &c->ex_out, &c->ex_obj})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
@@ -1147,6 +1152,7 @@ static IlrmaArgs ilrma_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64
   a.P = c->il_P.get<double>(S * M);
   a.partial = c->il_part.get<double>(static_cast<size_t>(ilrma_partials(I, J)) * M);
   a.mu = c->il_mu.get<double>(M);
+  a.vpart = c->il_vpart.get<double>(static_cast<size_t>(ilrma_vpart(I, J, K)) * M);
   a.err = c->err.get<unsigned long long>(1);
   if (I == 0) return a;
   h2d(c, a.W, eye.data(), eye.size() * sizeof(double));
@@ -1154,9 +1160,9 @@ static IlrmaArgs ilrma_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64
   h2d(c, a.V, hV.data(), hV.size() * sizeof(double));
   reset_err(c);
   c->launched(launch_ilrma_powers(c->stream, a, M));
-  for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
+  for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 3);
   for (int it = 0; it < iters; ++it) {
-    c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
+    c->launched(launch_ilrma_nmf(c->stream, a, M), 3);
     c->launched(launch_ilrma_ip_scale(c->stream, a, M), 4);
   }
   c->launched(launch_ilrma_inverse(c->stream, a, M));
@@ -1461,8 +1467,14 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
     // 6. the solver (tools/rcscm.cpp:135-142, 184-190)
     std::vector<double> objv;
     const bool want_obj = o->compute_objective != 0;
+    // without the early stop the trace stays on the device until the end
+    const bool obj_dev = want_obj && !(o->rel_obj_tol > 0.0);
+    double* dobj = obj_dev ? c->ex_obj.get<double>(static_cast<size_t>(o->iters) + 1) : nullptr;
+    int nobj = 0;
     auto eval = [&] {
-      return o->backend == 2 ? objective_fast(c, I, J, M, h) : objective(c, I, J, M, h);
+      double* slot = obj_dev ? dobj + nobj : nullptr;
+      ++nobj;
+      return o->backend == 2 ? objective_fast(c, I, J, M, h, slot) : objective(c, I, J, M, h, slot);
     };
     if (want_obj && o->backend == 2) c->launched(launch_logpdet(c->stream, problem(c, 1, I, J, M)));
     if (want_obj) objv.push_back(eval());
@@ -1484,9 +1496,10 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
       if (want_obj) {
         objv.push_back(eval());
         const double prev = objv[objv.size() - 2], cur = objv.back();
-        if (o->rel_obj_tol > 0.0 && std::abs(cur - prev) <= o->rel_obj_tol * std::abs(prev)) break;
+        if (!obj_dev && std::abs(cur - prev) <= o->rel_obj_tol * std::abs(prev)) break;
       }
     }
+    if (obj_dev) d2h(c, objv.data(), dobj, objv.size() * sizeof(double));
     check_err(c, J);
     // 7. Wiener image and noise (wiener.hpp:19-53), then WOLA synthesis of both
     WienerArgs Wa{};

@@ -11,8 +11,9 @@
 //                  thread's Jacobi eig -> Q, then Q x for every frame
 //   k_nmf_t        CTA per (bin, source): R, P/R^2, 1/R on the fly, the K
 //                  numerator / denominator sums over frames, T update
-//   k_nmf_v        CTA per (32-frame tile, source): the K sums over bins with the
-//                  new T, V update
+//   k_nmf_v        CTA per (32-frame tile, source, 64-bin chunk): the chunk's K
+//                  sums over bins with the new T; k_nmf_v_fin sums the chunks in
+//                  order and updates V
 //   k_ip           CTA per bin: the M weighted covariances U_n (one source at a
 //                  time, lower triangle, block tree) and, by one thread, the
 //                  sequential row updates W_n <- (W U_n)^{-1} e_n / norm with
@@ -30,80 +31,106 @@ namespace {
 
 constexpr double kNmfVarFloor = 1e-12;  // ilrma.hpp:40
 
-// Eigen::FullPivLU on an n x n column-major matrix held by one thread (in place).
-// Pivot: first maximum |a_rc| in column-major order of the remaining corner;
-// rank counts pivots above n * eps * |max pivot|.
-template <int MAXN>
+// Eigen::FullPivLU on an M x M column-major matrix held by one thread (in place,
+// registers: every loop has compile-time bounds and the pivot swaps are
+// predicated selects). Pivot: first maximum |a_rc| in column-major order of the
+// remaining corner; rank counts pivots above M * eps * |max pivot|.
+template <int M>
 struct DevFullPivLU {
-  int n, nonzero;
+  int nonzero;
   double maxpivot;
-  int rowp[MAXN], colp[MAXN];
-  __device__ void compute(double2* lu, int nn) {
-    n = nn;
-    nonzero = n;
+  int rowp[M], colp[M];
+  __device__ __forceinline__ void compute(double2 (&lu)[M * M]) {
+    nonzero = M;
     maxpivot = 0.0;
-    for (int k = 0; k < n; ++k) {
+    bool done = false;
+#pragma unroll
+    for (int k = 0; k < M; ++k) {
       int br = k, bc = k;
       double big = -1.0;
-      for (int c = k; c < n; ++c)
-        for (int r = k; r < n; ++r) {
-          const double v = hypot(lu[r + c * n].x, lu[r + c * n].y);
+#pragma unroll
+      for (int c = k; c < M; ++c)
+#pragma unroll
+        for (int r = k; r < M; ++r) {
+          const double v = cnorm(lu[r + c * M]);
           if (v > big) {
             big = v;
             br = r;
             bc = c;
           }
         }
-      if (big == 0.0) {
+      if (!done && big == 0.0) {
         nonzero = k;
-        for (int i = k; i < n; ++i) rowp[i] = colp[i] = i;
-        return;
+        done = true;
       }
-      if (big > maxpivot) maxpivot = big;
-      rowp[k] = br;
-      colp[k] = bc;
-      if (br != k)
-        for (int c = 0; c < n; ++c) {
-          const double2 t = lu[k + c * n];
-          lu[k + c * n] = lu[br + c * n];
-          lu[br + c * n] = t;
-        }
-      if (bc != k)
-        for (int r = 0; r < n; ++r) {
-          const double2 t = lu[r + k * n];
-          lu[r + k * n] = lu[r + bc * n];
-          lu[r + bc * n] = t;
-        }
-      const double2 piv = lu[k + k * n];
-      for (int r = k + 1; r < n; ++r) lu[r + k * n] = cdiv(lu[r + k * n], piv);
-      for (int c = k + 1; c < n; ++c)
-        for (int r = k + 1; r < n; ++r) lu[r + c * n] = csub(lu[r + c * n], cmul(lu[r + k * n], lu[k + c * n]));
+      rowp[k] = done ? k : br;
+      colp[k] = done ? k : bc;
+      if (done) continue;
+      maxpivot = fmax(maxpivot, sqrt(big));
+#pragma unroll
+      for (int r = k + 1; r < M; ++r)
+        if (r == br)
+#pragma unroll
+          for (int c = 0; c < M; ++c) {
+            const double2 t = lu[k + c * M];
+            lu[k + c * M] = lu[r + c * M];
+            lu[r + c * M] = t;
+          }
+#pragma unroll
+      for (int c = k + 1; c < M; ++c)
+        if (c == bc)
+#pragma unroll
+          for (int r = 0; r < M; ++r) {
+            const double2 t = lu[r + k * M];
+            lu[r + k * M] = lu[r + c * M];
+            lu[r + c * M] = t;
+          }
+      const double2 piv = lu[k + k * M];
+#pragma unroll
+      for (int r = k + 1; r < M; ++r) lu[r + k * M] = cdiv(lu[r + k * M], piv);
+#pragma unroll
+      for (int c = k + 1; c < M; ++c)
+#pragma unroll
+        for (int r = k + 1; r < M; ++r) lu[r + c * M] = csub(lu[r + c * M], cmul(lu[r + k * M], lu[k + c * M]));
     }
   }
-  __device__ bool invertible(const double2* lu) const {
-    const double thr = n * 2.220446049250313e-16 * maxpivot;
+  __device__ __forceinline__ bool invertible(const double2 (&lu)[M * M]) const {
+    const double thr = M * 2.220446049250313e-16 * maxpivot;
     int rk = 0;
-    for (int i = 0; i < nonzero; ++i) rk += hypot(lu[i + i * n].x, lu[i + i * n].y) > thr;
-    return rk == n;
+#pragma unroll
+    for (int i = 0; i < M; ++i) rk += (i < nonzero) && hypot(lu[i + i * M].x, lu[i + i * M].y) > thr;
+    return rk == M;
   }
   // y := A^{-1} y
-  __device__ void solve(const double2* lu, double2* y) const {
-    for (int k = 0; k < n; ++k) {
-      const double2 t = y[k];
-      y[k] = y[rowp[k]];
-      y[rowp[k]] = t;
+  __device__ __forceinline__ void solve(const double2 (&lu)[M * M], double2 (&y)[M]) const {
+#pragma unroll
+    for (int k = 0; k < M; ++k)
+#pragma unroll
+      for (int r = k + 1; r < M; ++r)
+        if (r == rowp[k]) {
+          const double2 t = y[k];
+          y[k] = y[r];
+          y[r] = t;
+        }
+#pragma unroll
+    for (int r = 0; r < M; ++r)
+#pragma unroll
+      for (int c = 0; c < r; ++c) y[r] = csub(y[r], cmul(lu[r + c * M], y[c]));
+#pragma unroll
+    for (int r = M - 1; r >= 0; --r) {
+#pragma unroll
+      for (int c = r + 1; c < M; ++c) y[r] = csub(y[r], cmul(lu[r + c * M], y[c]));
+      y[r] = cdiv(y[r], lu[r + r * M]);
     }
-    for (int r = 0; r < n; ++r)
-      for (int c = 0; c < r; ++c) y[r] = csub(y[r], cmul(lu[r + c * n], y[c]));
-    for (int r = n - 1; r >= 0; --r) {
-      for (int c = r + 1; c < n; ++c) y[r] = csub(y[r], cmul(lu[r + c * n], y[c]));
-      y[r] = cdiv(y[r], lu[r + r * n]);
-    }
-    for (int k = n - 1; k >= 0; --k) {
-      const double2 t = y[k];
-      y[k] = y[colp[k]];
-      y[colp[k]] = t;
-    }
+#pragma unroll
+    for (int k = M - 1; k >= 0; --k)
+#pragma unroll
+      for (int r = k + 1; r < M; ++r)
+        if (r == colp[k]) {
+          const double2 t = y[k];
+          y[k] = y[r];
+          y[r] = t;
+        }
   }
 };
 
@@ -237,7 +264,10 @@ __global__ void __launch_bounds__(NT) k_nmf_t(IlrmaArgs A) {
     T[i + k * I] = fmax(T[i + k * I] * sqrt(tot[2 * k] / fmax(tot[2 * k + 1], 1e-300)), 1e-300);
 }
 
-// V update for (32-frame tile = blockIdx.x, source n = blockIdx.y); 32 x 8 threads
+// V update, pass 1: CTA per (32-frame tile = blockIdx.x, source n = blockIdx.y,
+// chunk of kVChunk bins = blockIdx.z), 32 x 8 threads; the K numerator /
+// denominator sums of the chunk go to vpart[n][chunk][t][2K] (fixed order within)
+constexpr int kVChunk = 64;
 template <int KMAX>
 __global__ void __launch_bounds__(256) k_nmf_v(IlrmaArgs A) {
   __shared__ double acc_s[32][2 * KMAX];
@@ -245,8 +275,9 @@ __global__ void __launch_bounds__(256) k_nmf_v(IlrmaArgs A) {
   const int n = blockIdx.y, K = A.K;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t t = static_cast<int64_t>(blockIdx.x) * 32 + tx;
+  const int64_t i0 = static_cast<int64_t>(blockIdx.z) * kVChunk, i1 = min(I, i0 + kVChunk);
   const double* T = A.T + static_cast<int64_t>(n) * I * K;
-  double* V = A.V + static_cast<int64_t>(n) * K * J;
+  const double* V = A.V + static_cast<int64_t>(n) * K * J;
   const double* P = A.P + static_cast<int64_t>(n) * I * J;
   double vk[KMAX], acc[2 * KMAX];
 #pragma unroll
@@ -255,7 +286,7 @@ __global__ void __launch_bounds__(256) k_nmf_v(IlrmaArgs A) {
     acc[2 * k] = acc[2 * k + 1] = 0.0;
   }
   if (t < J) {
-    for (int64_t i = ty; i < I; i += 8) {
+    for (int64_t i = i0 + ty; i < i1; i += 8) {
       double s = 0.0;
 #pragma unroll
       for (int k = 0; k < KMAX; ++k)
@@ -279,9 +310,30 @@ __global__ void __launch_bounds__(256) k_nmf_v(IlrmaArgs A) {
     }
     __syncthreads();
   }
-  if (ty == 0 && t < J)
-    for (int k = 0; k < K; ++k)
-      V[k + t * K] = fmax(vk[k] * sqrt(acc_s[tx][2 * k] / fmax(acc_s[tx][2 * k + 1], 1e-300)), 1e-300);
+  if (ty == 0 && t < J) {
+    double* dst = A.vpart + ((static_cast<int64_t>(n) * gridDim.z + blockIdx.z) * J + t) * (2 * K);
+    for (int e = 0; e < 2 * K; ++e) dst[e] = acc_s[tx][e];
+  }
+}
+
+// V update, pass 2: thread per (frame, source) sums the chunks in order
+__global__ void k_nmf_v_fin(IlrmaArgs A, int nchunks, int M) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t J = A.J;
+  const int K = A.K;
+  if (q >= J * M) return;
+  const int n = static_cast<int>(q / J);
+  const int64_t t = q % J;
+  double* V = A.V + static_cast<int64_t>(n) * K * J;
+  for (int k = 0; k < K; ++k) {
+    double num = 0.0, den = 0.0;
+    for (int c = 0; c < nchunks; ++c) {
+      const double* src = A.vpart + ((static_cast<int64_t>(n) * nchunks + c) * J + t) * (2 * K);
+      num += src[2 * k];
+      den += src[2 * k + 1];
+    }
+    V[k + t * K] = fmax(V[k + t * K] * sqrt(num / fmax(den, 1e-300)), 1e-300);
+  }
 }
 
 // ---- iterative projection (ilrma.hpp:190-216) -----------------------------------
@@ -339,7 +391,7 @@ __global__ void __launch_bounds__(NT) k_ip(IlrmaArgs A) {
       double2 lu[M * M];
       for (int k = 0; k < M * M; ++k) lu[k] = WU[k];
       DevFullPivLU<M> f;
-      f.compute(lu, M);
+      f.compute(lu);
       bool ok = f.invertible(lu);
       if (!ok) {  // diagonal-loading retry (ilrma.hpp:205-211)
         double nrm = 0.0;
@@ -347,7 +399,7 @@ __global__ void __launch_bounds__(NT) k_ip(IlrmaArgs A) {
         const double load = 1e-8 * fmax(sqrt(nrm), 1e-30);
         for (int k = 0; k < M * M; ++k) lu[k] = WU[k];
         for (int r = 0; r < M; ++r) lu[r + r * M].x += load;
-        f.compute(lu, M);
+        f.compute(lu);
         ok = f.invertible(lu);
       }
       if (!ok) {
@@ -457,7 +509,7 @@ __global__ void k_demix_inv(IlrmaArgs A) {
   double2 lu[M * M];
   for (int k = 0; k < M * M; ++k) lu[k] = A.W[i * M * M + k];
   DevFullPivLU<M> f;
-  f.compute(lu, M);
+  f.compute(lu);
   if (!f.invertible(lu)) {
     report_error(A.err, i * A.J, kErrIlrmaDemix);
     return;
@@ -486,7 +538,7 @@ __global__ void k_fold(IlrmaArgs A, const double2* __restrict__ Q, double2* __re
       lu[r + c * M] = s;
     }
   DevFullPivLU<M> f;
-  f.compute(lu, M);
+  f.compute(lu);
   if (!f.invertible(lu)) {
     report_error(A.err, i * A.J, kErrIlrmaDemix);
     return;
@@ -546,10 +598,14 @@ cudaError_t launch_sphere(cudaStream_t s, int M, const double2* X, int64_t I, in
 
 int64_t ilrma_partials(int64_t I, int64_t J) { return I * ((J + kIlrmaNT - 1) / kIlrmaNT); }
 
+int64_t ilrma_vpart(int64_t I, int64_t J, int K) { return ((I + kVChunk - 1) / kVChunk) * J * 2 * K; }
+
 template <int KMAX>
 static cudaError_t nmf_update(cudaStream_t s, const IlrmaArgs& A, int M) {
   k_nmf_t<KMAX, kIlrmaNT><<<dim3(static_cast<unsigned>(A.I), M), kIlrmaNT, 0, s>>>(A);
-  k_nmf_v<KMAX><<<dim3(static_cast<unsigned>((A.J + 31) / 32), M), 256, 0, s>>>(A);
+  const int nchunks = static_cast<int>((A.I + kVChunk - 1) / kVChunk);
+  k_nmf_v<KMAX><<<dim3(static_cast<unsigned>((A.J + 31) / 32), M, nchunks), 256, 0, s>>>(A);
+  k_nmf_v_fin<<<static_cast<unsigned>((A.J * M + 127) / 128), 128, 0, s>>>(A, nchunks, M);
   return cudaGetLastError();
 }
 

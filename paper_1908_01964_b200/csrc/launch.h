@@ -80,9 +80,12 @@ struct IlrmaArgs {
   double* P;         // [n][bin][t]
   double* partial;   // [n][ilrma_partials(I, J)]
   double* mu;        // [n]
+  double* vpart;     // [n][ilrma_vpart(I, J, K)]
   unsigned long long* err;
 };
 int64_t ilrma_partials(int64_t I, int64_t J);
+// V-update partial sums per source: chunks x J x 2K doubles
+int64_t ilrma_vpart(int64_t I, int64_t J, int K);
 cudaError_t launch_sphere(cudaStream_t s, int M, const double2* X, int64_t I, int64_t J, double2* Q, double2* Xw);
 cudaError_t launch_ilrma_powers(cudaStream_t s, const IlrmaArgs& A, int M);
 cudaError_t launch_ilrma_nmf(cudaStream_t s, const IlrmaArgs& A, int M);     // K <= 32

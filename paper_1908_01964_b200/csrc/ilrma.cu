@@ -14,10 +14,11 @@
 //   k_nmf_v        CTA per (32-frame tile, source, 64-bin chunk): the chunk's K
 //                  sums over bins with the new T; k_nmf_v_fin sums the chunks in
 //                  order and updates V
-//   k_ip           CTA per bin: the M weighted covariances U_n (one source at a
-//                  time, lower triangle, block tree) and, by one thread, the
-//                  sequential row updates W_n <- (W U_n)^{-1} e_n / norm with
-//                  Eigen::FullPivLU's pivot and rank rules (diagonal-loading retry)
+//   k_ip_cov       CTA per (bin, source): the weighted covariance U_n (lower
+//                  triangle, block tree) -- independent of W, so all in parallel
+//   k_ip_solve     thread per bin: the sequential row updates
+//                  W_n <- (W U_n)^{-1} e_n / norm with Eigen::FullPivLU's pivot and
+//                  rank rules (diagonal-loading retry)
 //   k_powers       P[n] = |W x|^2 per slot + per-CTA partial sums for the mean
 //   k_scale_mu     one CTA: mu_n = sqrt(mean P[n]) from the partials in order
 //   k_scale_apply  W rows /= mu, P /= mu^2, T /= mu^2 (mu > 0 and finite)
@@ -31,26 +32,24 @@ namespace {
 
 constexpr double kNmfVarFloor = 1e-12;  // ilrma.hpp:40
 
-// Eigen::FullPivLU on an M x M column-major matrix held by one thread (in place,
-// registers: every loop has compile-time bounds and the pivot swaps are
-// predicated selects). Pivot: first maximum |a_rc| in column-major order of the
-// remaining corner; rank counts pivots above M * eps * |max pivot|.
+// Eigen::FullPivLU on an M x M column-major matrix of one thread, in place in
+// that thread's slice of shared memory (runtime loops: the row / column pivots
+// index dynamically, which registers cannot). Pivot: first maximum |a_rc| in
+// column-major order of the remaining corner; rank counts pivots above
+// M * eps * |max pivot|. perm: 2M ints (row, then column transpositions).
 template <int M>
 struct DevFullPivLU {
+  double2* lu;
+  int* perm;
   int nonzero;
   double maxpivot;
-  int rowp[M], colp[M];
-  __device__ __forceinline__ void compute(double2 (&lu)[M * M]) {
+  __device__ void compute() {
     nonzero = M;
     maxpivot = 0.0;
-    bool done = false;
-#pragma unroll
     for (int k = 0; k < M; ++k) {
       int br = k, bc = k;
       double big = -1.0;
-#pragma unroll
       for (int c = k; c < M; ++c)
-#pragma unroll
         for (int r = k; r < M; ++r) {
           const double v = cnorm(lu[r + c * M]);
           if (v > big) {
@@ -59,80 +58,72 @@ struct DevFullPivLU {
             bc = c;
           }
         }
-      if (!done && big == 0.0) {
+      if (big == 0.0) {
         nonzero = k;
-        done = true;
+        for (int q = k; q < M; ++q) perm[q] = perm[M + q] = q;
+        return;
       }
-      rowp[k] = done ? k : br;
-      colp[k] = done ? k : bc;
-      if (done) continue;
       maxpivot = fmax(maxpivot, sqrt(big));
-#pragma unroll
-      for (int r = k + 1; r < M; ++r)
-        if (r == br)
-#pragma unroll
-          for (int c = 0; c < M; ++c) {
-            const double2 t = lu[k + c * M];
-            lu[k + c * M] = lu[r + c * M];
-            lu[r + c * M] = t;
-          }
-#pragma unroll
-      for (int c = k + 1; c < M; ++c)
-        if (c == bc)
-#pragma unroll
-          for (int r = 0; r < M; ++r) {
-            const double2 t = lu[r + k * M];
-            lu[r + k * M] = lu[r + c * M];
-            lu[r + c * M] = t;
-          }
+      perm[k] = br;
+      perm[M + k] = bc;
+      if (br != k)
+        for (int c = 0; c < M; ++c) {
+          const double2 t = lu[k + c * M];
+          lu[k + c * M] = lu[br + c * M];
+          lu[br + c * M] = t;
+        }
+      if (bc != k)
+        for (int r = 0; r < M; ++r) {
+          const double2 t = lu[r + k * M];
+          lu[r + k * M] = lu[r + bc * M];
+          lu[r + bc * M] = t;
+        }
       const double2 piv = lu[k + k * M];
-#pragma unroll
       for (int r = k + 1; r < M; ++r) lu[r + k * M] = cdiv(lu[r + k * M], piv);
-#pragma unroll
-      for (int c = k + 1; c < M; ++c)
-#pragma unroll
-        for (int r = k + 1; r < M; ++r) lu[r + c * M] = csub(lu[r + c * M], cmul(lu[r + k * M], lu[k + c * M]));
+      for (int c = k + 1; c < M; ++c) {
+        const double2 u = lu[k + c * M];
+        for (int r = k + 1; r < M; ++r) lu[r + c * M] = csub(lu[r + c * M], cmul(lu[r + k * M], u));
+      }
     }
   }
-  __device__ __forceinline__ bool invertible(const double2 (&lu)[M * M]) const {
+  __device__ bool invertible() const {
     const double thr = M * 2.220446049250313e-16 * maxpivot;
     int rk = 0;
-#pragma unroll
-    for (int i = 0; i < M; ++i) rk += (i < nonzero) && hypot(lu[i + i * M].x, lu[i + i * M].y) > thr;
+    for (int q = 0; q < nonzero; ++q) rk += hypot(lu[q + q * M].x, lu[q + q * M].y) > thr;
     return rk == M;
   }
   // y := A^{-1} y
-  __device__ __forceinline__ void solve(const double2 (&lu)[M * M], double2 (&y)[M]) const {
-#pragma unroll
-    for (int k = 0; k < M; ++k)
-#pragma unroll
-      for (int r = k + 1; r < M; ++r)
-        if (r == rowp[k]) {
-          const double2 t = y[k];
-          y[k] = y[r];
-          y[r] = t;
-        }
-#pragma unroll
+  __device__ void solve(double2* y) const {
+    for (int k = 0; k < M; ++k) {
+      const int r = perm[k];
+      const double2 t = y[k];
+      y[k] = y[r];
+      y[r] = t;
+    }
     for (int r = 0; r < M; ++r)
-#pragma unroll
       for (int c = 0; c < r; ++c) y[r] = csub(y[r], cmul(lu[r + c * M], y[c]));
-#pragma unroll
     for (int r = M - 1; r >= 0; --r) {
-#pragma unroll
       for (int c = r + 1; c < M; ++c) y[r] = csub(y[r], cmul(lu[r + c * M], y[c]));
       y[r] = cdiv(y[r], lu[r + r * M]);
     }
-#pragma unroll
-    for (int k = M - 1; k >= 0; --k)
-#pragma unroll
-      for (int r = k + 1; r < M; ++r)
-        if (r == colp[k]) {
-          const double2 t = y[k];
-          y[k] = y[r];
-          y[r] = t;
-        }
+    for (int k = M - 1; k >= 0; --k) {
+      const int c = perm[M + k];
+      const double2 t = y[k];
+      y[k] = y[c];
+      y[c] = t;
+    }
   }
 };
+// threads per CTA of the thread-per-bin kernels (per-thread smem slices)
+template <int M>
+constexpr int lu_tpb() {
+  return M <= 4 ? 32 : (M <= 8 ? 16 : 4);  // <= 48 KB of static shared memory
+}
+// per-thread shared slice: W, lu (M*M each), w (M) as double2 + 2M ints
+template <int M>
+constexpr int lu_slice() {
+  return ((2 * M * M + M) * 16 + 2 * M * 4 + 15) / 16 * 16;  // 16-byte aligned slices
+}
 
 // Fixed-order block sum of NV doubles per thread (NT threads): xor butterfly in
 // each warp, then the warp partials summed in warp order. out[NV] in shared
@@ -337,91 +328,106 @@ __global__ void k_nmf_v_fin(IlrmaArgs A, int nchunks, int M) {
 }
 
 // ---- iterative projection (ilrma.hpp:190-216) -----------------------------------
+// Pass 1: the weighted covariances U_n = (1/J) sum_t x x^H / r_n(t) do not depend
+// on W, so all (bin, source) pairs run in parallel: CTA per (bin, source), lower
+// triangle accumulated per thread, fixed-order block tree, full Hermitian U_n
+// stored to ucov[(bin*M + n)][M*M].
 template <int M, int NT>
-__global__ void __launch_bounds__(NT) k_ip(IlrmaArgs A) {
+__global__ void __launch_bounds__(NT) k_ip_cov(IlrmaArgs A) {
   constexpr int NE = M * (M + 1) / 2;
   __shared__ double red[NT / 32 * 2 * NE];
   __shared__ double tot[2 * NE];
-  __shared__ double2 sW[M * M];
-  __shared__ int s_fail;
   const int64_t i = blockIdx.x, I = A.I, J = A.J;
-  const int K = A.K;
-  if (threadIdx.x < M * M) sW[threadIdx.x] = A.W[i * M * M + threadIdx.x];
-  if (threadIdx.x == 0) s_fail = 0;
-  __syncthreads();
-  for (int n = 0; n < M; ++n) {
-    const double* T = A.T + static_cast<int64_t>(n) * I * K;
-    const double* V = A.V + static_cast<int64_t>(n) * K * J;
-    double acc[2 * NE];
+  const int n = blockIdx.y, K = A.K;
+  const double* T = A.T + static_cast<int64_t>(n) * I * K;
+  const double* V = A.V + static_cast<int64_t>(n) * K * J;
+  double acc[2 * NE];
 #pragma unroll
-    for (int e = 0; e < 2 * NE; ++e) acc[e] = 0.0;
-    for (int64_t t = threadIdx.x; t < J; t += NT) {
-      double s = 0.0;
-      for (int k = 0; k < K; ++k) s = fma(T[i + k * I], V[k + t * K], s);
-      const double w = 1.0 / fmax(s, kNmfVarFloor);
-      double2 x[M];
+  for (int e = 0; e < 2 * NE; ++e) acc[e] = 0.0;
+  for (int64_t t = threadIdx.x; t < J; t += NT) {
+    double s = 0.0;
+    for (int k = 0; k < K; ++k) s = fma(T[i + k * I], V[k + t * K], s);
+    const double w = 1.0 / fmax(s, kNmfVarFloor);
+    double2 x[M];
 #pragma unroll
-      for (int m = 0; m < M; ++m) x[m] = A.X[(i * J + t) * M + m];
-      int e = 0;
+    for (int m = 0; m < M; ++m) x[m] = A.X[(i * J + t) * M + m];
+    int e = 0;
 #pragma unroll
-      for (int c = 0; c < M; ++c)
+    for (int c = 0; c < M; ++c)
 #pragma unroll
-        for (int r = c; r < M; ++r, ++e) {
-          const double2 v = cscale(cmul(x[r], cconj(x[c])), w);
-          acc[2 * e] += v.x;
-          acc[2 * e + 1] += v.y;
-        }
+      for (int r = c; r < M; ++r, ++e) {
+        const double2 v = cscale(cmul(x[r], cconj(x[c])), w);
+        acc[2 * e] += v.x;
+        acc[2 * e + 1] += v.y;
+      }
+  }
+  block_sum<NT, 2 * NE>(acc, red, tot);
+  double2* U = A.ucov + (i * M + n) * M * M;
+  for (int q = threadIdx.x; q < NE; q += NT) {
+    int c = 0, r = q;  // q-th lower-triangle entry in (c, r >= c) order
+    while (r >= M - c) {
+      r -= M - c;
+      ++c;
     }
-      block_sum<NT, 2 * NE>(acc, red, tot);
-    if (threadIdx.x == 0 && !s_fail) {
-      double2 U[M * M], WU[M * M];
-      int e = 0;
-      for (int c = 0; c < M; ++c)
-        for (int r = c; r < M; ++r, ++e) {
-          const double2 v = make_double2(tot[2 * e] / static_cast<double>(J), tot[2 * e + 1] / static_cast<double>(J));
-          U[r + c * M] = v;
-          U[c + r * M] = cconj(v);
-        }
+    r += c;
+    const double2 v = make_double2(tot[2 * q] / static_cast<double>(J), tot[2 * q + 1] / static_cast<double>(J));
+    U[r + c * M] = v;
+    U[c + r * M] = cconj(v);
+  }
+}
+
+// Pass 2: thread per bin, the sequential row updates (ilrma.hpp:195-215):
+// W_n <- (W U_n)^{-1} e_n / sqrt(max(Re w^H U_n w, 1e-300)), conjugated into row n,
+// with Eigen::FullPivLU's pivot / rank rules and the diagonal-loading retry.
+// W, the LU and w live in the thread's shared-memory slice.
+template <int M>
+__global__ void __launch_bounds__(lu_tpb<M>()) k_ip_solve(IlrmaArgs A) {
+  __shared__ __align__(16) unsigned char slab[lu_tpb<M>() * lu_slice<M>()];
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= A.I) return;
+  double2* W = reinterpret_cast<double2*>(slab + threadIdx.x * lu_slice<M>());
+  double2* lu = W + M * M;
+  double2* w = lu + M * M;
+  int* perm = reinterpret_cast<int*>(w + M);
+  for (int k = 0; k < M * M; ++k) W[k] = A.W[i * M * M + k];
+  DevFullPivLU<M> f{lu, perm, 0, 0.0};
+  for (int n = 0; n < M; ++n) {
+    const double2* U = A.ucov + (i * M + n) * M * M;
+    auto form_wu = [&](double load) {  // lu = W U (+ load I)
       for (int c = 0; c < M; ++c)
         for (int r = 0; r < M; ++r) {
           double2 s = make_double2(0.0, 0.0);
-          for (int k = 0; k < M; ++k) s = cfma(sW[r + k * M], U[k + c * M], s);
-          WU[r + c * M] = s;
+          for (int k = 0; k < M; ++k) s = cfma(W[r + k * M], U[k + c * M], s);
+          if (r == c) s.x += load;
+          lu[r + c * M] = s;
         }
-      double2 lu[M * M];
-      for (int k = 0; k < M * M; ++k) lu[k] = WU[k];
-      DevFullPivLU<M> f;
-      f.compute(lu);
-      bool ok = f.invertible(lu);
-      if (!ok) {  // diagonal-loading retry (ilrma.hpp:205-211)
-        double nrm = 0.0;
-        for (int k = 0; k < M * M; ++k) nrm += cnorm(WU[k]);
-        const double load = 1e-8 * fmax(sqrt(nrm), 1e-30);
-        for (int k = 0; k < M * M; ++k) lu[k] = WU[k];
-        for (int r = 0; r < M; ++r) lu[r + r * M].x += load;
-        f.compute(lu);
-        ok = f.invertible(lu);
-      }
-      if (!ok) {
-        report_error(A.err, i * J, kErrIlrmaSpatial);
-        s_fail = 1;
-      } else {
-        double2 w[M];
-        for (int r = 0; r < M; ++r) w[r] = make_double2(r == n ? 1.0 : 0.0, 0.0);
-        f.solve(lu, w);
-        double2 q = make_double2(0.0, 0.0);
-        for (int r = 0; r < M; ++r) {
-          double2 uw = make_double2(0.0, 0.0);
-          for (int c = 0; c < M; ++c) uw = cfma(U[r + c * M], w[c], uw);
-          q = cfmac(w[r], uw, q);
-        }
-        const double s = sqrt(fmax(q.x, 1e-300));
-        for (int c = 0; c < M; ++c) sW[n + c * M] = cconj(make_double2(w[c].x / s, w[c].y / s));
-      }
+    };
+    form_wu(0.0);
+    double nrm = 0.0;
+    for (int k = 0; k < M * M; ++k) nrm += cnorm(lu[k]);
+    f.compute();
+    bool ok = f.invertible();
+    if (!ok) {  // diagonal-loading retry (ilrma.hpp:205-211)
+      form_wu(1e-8 * fmax(sqrt(nrm), 1e-30));
+      f.compute();
+      ok = f.invertible();
     }
-    __syncthreads();
+    if (!ok) {
+      report_error(A.err, i * A.J, kErrIlrmaSpatial);
+      return;  // the bin keeps its W (the reference stops updating it too)
+    }
+    for (int r = 0; r < M; ++r) w[r] = make_double2(r == n ? 1.0 : 0.0, 0.0);
+    f.solve(w);
+    double2 q = make_double2(0.0, 0.0);
+    for (int r = 0; r < M; ++r) {
+      double2 uw = make_double2(0.0, 0.0);
+      for (int c = 0; c < M; ++c) uw = cfma(U[r + c * M], w[c], uw);
+      q = cfmac(w[r], uw, q);
+    }
+    const double sc = sqrt(fmax(q.x, 1e-300));
+    for (int c = 0; c < M; ++c) W[n + c * M] = cconj(make_double2(w[c].x / sc, w[c].y / sc));
   }
-  if (threadIdx.x < M * M) A.W[i * M * M + threadIdx.x] = sW[threadIdx.x];
+  for (int k = 0; k < M * M; ++k) A.W[i * M * M + k] = W[k];
 }
 
 // ---- demixed powers, scale normalisation, final inverse --------------------------
@@ -502,54 +508,51 @@ __global__ void k_scale_apply(IlrmaArgs A, int M) {
   }
 }
 
+// Inverse of the M x M matrix src (bin i) by the thread's shared-memory FullPivLU
+// into dst; false if Eigen's rank rule calls it singular.
 template <int M>
-__global__ void k_demix_inv(IlrmaArgs A) {
+__device__ bool lu_inverse(unsigned char* slab, const double2* src, double2* dst) {
+  double2* lu = reinterpret_cast<double2*>(slab + threadIdx.x * lu_slice<M>()) + M * M;
+  double2* e = lu + M * M;
+  int* perm = reinterpret_cast<int*>(e + M);
+  for (int k = 0; k < M * M; ++k) lu[k] = src[k];
+  DevFullPivLU<M> f{lu, perm, 0, 0.0};
+  f.compute();
+  if (!f.invertible()) return false;
+  for (int c = 0; c < M; ++c) {
+    for (int r = 0; r < M; ++r) e[r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+    f.solve(e);
+    for (int r = 0; r < M; ++r) dst[r + c * M] = e[r];
+  }
+  return true;
+}
+
+// A = W^{-1} per bin (ilrma.hpp:232-238)
+template <int M>
+__global__ void __launch_bounds__(lu_tpb<M>()) k_demix_inv(IlrmaArgs A) {
+  __shared__ __align__(16) unsigned char slab[lu_tpb<M>() * lu_slice<M>()];
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= A.I) return;
-  double2 lu[M * M];
-  for (int k = 0; k < M * M; ++k) lu[k] = A.W[i * M * M + k];
-  DevFullPivLU<M> f;
-  f.compute(lu);
-  if (!f.invertible(lu)) {
-    report_error(A.err, i * A.J, kErrIlrmaDemix);
-    return;
-  }
-  for (int c = 0; c < M; ++c) {
-    double2 e[M];
-    for (int r = 0; r < M; ++r) e[r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
-    f.solve(lu, e);
-    for (int r = 0; r < M; ++r) A.A[i * M * M + r + c * M] = e[r];
-  }
+  if (!lu_inverse<M>(slab, A.W + i * M * M, A.A + i * M * M)) report_error(A.err, i * A.J, kErrIlrmaDemix);
 }
 
 // ---- fold + target selection (tools/rcscm.cpp:173-181, model.hpp:43-54) -----------
 // W_i = W_ilrma,i Q_i (back to the observation domain), A_i = W_i^{-1}
 template <int M>
-__global__ void k_fold(IlrmaArgs A, const double2* __restrict__ Q, double2* __restrict__ Wout,
-                       double2* __restrict__ Aout) {
+__global__ void __launch_bounds__(lu_tpb<M>()) k_fold(IlrmaArgs A, const double2* __restrict__ Q,
+                                                     double2* __restrict__ Wout, double2* __restrict__ Aout) {
+  __shared__ __align__(16) unsigned char slab[lu_tpb<M>() * lu_slice<M>()];
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i >= A.I) return;
-  double2 W[M * M], lu[M * M];
+  double2* W = reinterpret_cast<double2*>(slab + threadIdx.x * lu_slice<M>());
   for (int c = 0; c < M; ++c)
     for (int r = 0; r < M; ++r) {
       double2 s = make_double2(0.0, 0.0);
       for (int k = 0; k < M; ++k) s = cfma(A.W[i * M * M + r + k * M], Q[i * M * M + k + c * M], s);
       W[r + c * M] = s;
-      lu[r + c * M] = s;
+      Wout[i * M * M + r + c * M] = s;
     }
-  DevFullPivLU<M> f;
-  f.compute(lu);
-  if (!f.invertible(lu)) {
-    report_error(A.err, i * A.J, kErrIlrmaDemix);
-    return;
-  }
-  for (int k = 0; k < M * M; ++k) Wout[i * M * M + k] = W[k];
-  for (int c = 0; c < M; ++c) {
-    double2 e[M];
-    for (int r = 0; r < M; ++r) e[r] = make_double2(r == c ? 1.0 : 0.0, 0.0);
-    f.solve(lu, e);
-    for (int r = 0; r < M; ++r) Aout[i * M * M + r + c * M] = e[r];
-  }
+  if (!lu_inverse<M>(slab, W, Aout + i * M * M)) report_error(A.err, i * A.J, kErrIlrmaDemix);
 }
 
 // power[n][i] = ||(W_i X_i)_n||^2 ||A_i(:, n)||^2 (select_target_index, per bin)
@@ -629,7 +632,9 @@ cudaError_t launch_ilrma_powers(cudaStream_t s, const IlrmaArgs& A, int M) {
 cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M) {
   cudaError_t e = dispatch_mics(M, [&](auto mm) {
     constexpr int MM = decltype(mm)::value;
-    k_ip<MM, kIlrmaNT><<<static_cast<unsigned>(A.I), kIlrmaNT, 0, s>>>(A);
+    k_ip_cov<MM, kIlrmaNT><<<dim3(static_cast<unsigned>(A.I), MM), kIlrmaNT, 0, s>>>(A);
+    constexpr int tpb = lu_tpb<MM>();
+    k_ip_solve<MM><<<static_cast<unsigned>((A.I + tpb - 1) / tpb), tpb, 0, s>>>(A);
     return cudaGetLastError();
   });
   if (e != cudaSuccess) return e;
@@ -642,7 +647,8 @@ cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M) {
 cudaError_t launch_ilrma_fold(cudaStream_t s, const IlrmaArgs& A, int M, const double2* Q, double2* W, double2* Am) {
   return dispatch_mics(M, [&](auto mm) {
     constexpr int MM = decltype(mm)::value;
-    k_fold<MM><<<static_cast<unsigned>((A.I + 127) / 128), 128, 0, s>>>(A, Q, W, Am);
+    constexpr int tpb = lu_tpb<MM>();
+    k_fold<MM><<<static_cast<unsigned>((A.I + tpb - 1) / tpb), tpb, 0, s>>>(A, Q, W, Am);
     return cudaGetLastError();
   });
 }
@@ -659,7 +665,8 @@ cudaError_t launch_target_power(cudaStream_t s, int M, const double2* X, const d
 cudaError_t launch_ilrma_inverse(cudaStream_t s, const IlrmaArgs& A, int M) {
   return dispatch_mics(M, [&](auto mm) {
     constexpr int MM = decltype(mm)::value;
-    k_demix_inv<MM><<<static_cast<unsigned>((A.I + 127) / 128), 128, 0, s>>>(A);
+    constexpr int tpb = lu_tpb<MM>();
+    k_demix_inv<MM><<<static_cast<unsigned>((A.I + tpb - 1) / tpb), tpb, 0, s>>>(A);
     return cudaGetLastError();
   });
 }

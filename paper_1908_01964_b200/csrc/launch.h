@@ -81,6 +81,7 @@ struct IlrmaArgs {
   double* partial;   // [n][ilrma_partials(I, J)]
   double* mu;        // [n]
   double* vpart;     // [n][ilrma_vpart(I, J, K)]
+  double2* ucov;     // [bin][n][M*M] IP weighted covariances
   unsigned long long* err;
 };
 int64_t ilrma_partials(int64_t I, int64_t J);

@@ -310,8 +310,10 @@ def run_gpu(args):
     fp64_peak = tf.value if rc == 0 else NOMINAL_FP64_TFLOPS
     k2_avg = sum(k2_ms) / len(k2_ms)
     # algorithmic flops of the fused launch: the sigma / tau forms once per slot
-    # (8 M^2 + 24 M) plus 47 per slot-iteration
-    pre_flops = 8.0 * M * M + 24.0 * M
+    # (b^H x and (R'^+ a)^H x: 8 M each; x^H R'^+ x with R'^+ Hermitian: 3 M on the
+    # diagonal + 8 per lower-triangle pair -> 4 M^2 + 15 M) plus 47 per
+    # slot-iteration
+    pre_flops = 4.0 * M * M + 15.0 * M
     launch_flops = FLOPS_ACCEL * slot_iters + pre_flops * B * I * J
     achieved = launch_flops / (k2_avg * 1e-3) / 1e12
     roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",

@@ -42,24 +42,33 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 // The per-slot quadratic forms of solver_accel.hpp:33-64 for one x (M complex):
 // sigma_bx = b^H x, tau_ax = (R'^+ a)^H x, tau_xx = max(Re x^H R'^+ x, 0), in
 // the one arithmetic order shared by K1 (k_pre, k_slots) and K2's fused
-// precompute, so both produce the same bits. sb = b, sp = R'^+ a, sR = R'^+
+// precompute, so both produce the same bits. tau_xx uses R'^+'s Hermitian
+// symmetry (the reference evaluates the full form; rounding-level difference). sb = b, sp = R'^+ a, sR = R'^+
 // (column-major M x M).
 template <int M>
 __device__ __forceinline__ void slot_forms(const double2 (&x)[M], const double2* sb, const double2* sp,
                                            const double2* sR, double2& sbx, double2& tax, double& txx) {
   sbx = make_double2(0.0, 0.0);
   tax = make_double2(0.0, 0.0);
-  double2 xx = make_double2(0.0, 0.0);
 #pragma unroll
   for (int r = 0; r < M; ++r) {
     sbx = cfmac(sb[r], x[r], sbx);
     tax = cfmac(sp[r], x[r], tax);
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int q = 0; q < M; ++q) acc = cfma(sR[r + q * M], x[q], acc);
-    xx = cfmac(x[r], acc, xx);
   }
-  txx = fmax(xx.x, 0.0);
+  // x^H R x of the Hermitian R from its lower triangle:
+  //   sum_r R_rr |x_r|^2 + 2 sum_{r > c} Re(conj(x_r) R_rc x_c)
+  // (a third of the FP64 work of the full quadratic form)
+  double d = 0.0, o = 0.0;
+#pragma unroll
+  for (int r = 0; r < M; ++r) {
+    d = fma(sR[r + r * M].x, cnorm(x[r]), d);
+#pragma unroll
+    for (int c = 0; c < r; ++c) {
+      const double2 y = cmul(sR[r + c * M], x[c]);
+      o = fma(x[r].x, y.x, fma(x[r].y, y.y, o));
+    }
+  }
+  txx = fmax(fma(2.0, o, d), 0.0);
 }
 
 // Launch shape of the slot-stream kernels (K1 precompute, K4 Wiener): each

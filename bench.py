@@ -400,10 +400,11 @@ def run_gpu(args):
 
 
 def stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, torch, C):
-    """K1 (standalone precompute) and K4 (Wiener) against the HBM peak: each
-    launch timed alone after an L2 flush (cold L2, median of 7), on the bench
-    utterance (68 / 84 MB: launch-latency bound) and on a batch of 8 copies of
-    it (0.5 / 0.7 GB: the streaming regime the batched configs run in)."""
+    """K1 (standalone precompute) and K4 (Wiener) against the HBM peak: the
+    bench-utterance launch timed alone after an L2 flush (68 / 84 MB: launch-
+    latency bound), the same launch 8 times back to back on distinct copies
+    (steady state), and one launch over a batch of 8 copies (0.5 / 0.7 GB: the
+    streaming regime the batched configs run in)."""
     from paper_1908_01964_b200 import GpuContext
     import numpy as np
 
@@ -428,6 +429,34 @@ def stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, 
     out = {"k_pre": entry(cold(ctx, C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S),
            "k_wiener": entry(cold(ctx, C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S)}
     nb = 8
+    # the single-utterance launch in steady state: 8 contexts, each holding its own
+    # copy of the utterance (0.5 GB in all, > L2), launched back to back after one
+    # flush, so each launch streams cold data and the launch latency overlaps
+    ctxs = [GpuContext(local, stream=tstream.cuda_stream) for _ in range(nb)]
+    for cx in ctxs:
+        cx.session_load(X, W, A, T, V, 0)
+        cx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
+        cx.session_run(C.STAGE_ACCEL, 3, hyper)
+
+    def chain(stages, reps=5):
+        ts = []
+        for r in range(reps + 1):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(tstream)
+            for cx in ctxs:
+                cx.session_run(stages, 0, hyper)
+            e1.record(tstream)
+            e1.synchronize()
+            if r:
+                ts.append(e0.elapsed_time(e1) / nb)
+        return statistics.median(ts)
+
+    out["k_pre_steady"] = entry(chain(C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S)
+    out["k_wiener_steady"] = entry(chain(C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S)
+    for cx in ctxs:
+        cx.session_check()
+        cx.close()
     big = GpuContext(local, stream=tstream.cuda_stream)
     rep = lambda v: np.concatenate([v] * nb, axis=0)
     big.session_load(rep(X), rep(W), rep(A), rep(T), rep(V), 0)
@@ -437,8 +466,10 @@ def stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, 
     out["k_wiener_batch8"] = entry(cold(big, C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S * nb)
     big.session_check()
     big.close()
-    out["note"] = ("each launch alone after an L2 flush; algorithmic bytes (K1: read x, write sigma_bx, tau_ax, "
-                   "tau_xx; K4: read sigma_bx, tau_ax, r_h, r_u, write dry + image)")
+    out["note"] = ("k_pre / k_wiener: one launch alone after an L2 flush (launch latency included); *_steady: "
+                   "the same single-utterance launch, 8 back to back on distinct copies after one flush (cold "
+                   "data, latency overlapped); *_batch8: one launch over 8 utterances; algorithmic bytes (K1: "
+                   "read x, write sigma_bx, tau_ax, tau_xx; K4: read sigma_bx, tau_ax, r_h, r_u, write dry + image)")
     return out
 
 

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // setup_launch.cu -- launchers of K1a / K1b / K1 (setup.cuh).
 #include <algorithm>
 
@@ -46,9 +47,16 @@ cudaError_t launch_slots(cudaStream_t s, const DevProblem& P, bool init, bool pr
     constexpr int MM = decltype(mm)::value;
     if (!init) {  // the precompute pass alone (every solve): k_pre
       constexpr int SPT = pre_spt<MM>();
-      const SlotGrid g = slot_grid(P.J, SPT);
-      k_pre<MM, SPT><<<dim3(P.nb, g.chunks), g.nt, 0, s>>>(P);
-      return cudaGetLastError();
+      const char* e = std::getenv("RCSCM_STREAM_SPT");  // tuning knob
+      const int spt = e ? std::atoi(e) : SPT;
+      auto go = [&](auto kern, int sp) {
+        const SlotGrid g = slot_grid(P.J, sp);
+        kern<<<dim3(P.nb, g.chunks), g.nt, 0, s>>>(P);
+        return cudaGetLastError();
+      };
+      if (spt == 1) return go(k_pre<MM, 1>, 1);
+      if (spt == 2 && SPT >= 2) return go(k_pre<MM, (SPT >= 2 ? 2 : 1)>, 2);
+      return go(k_pre<MM, SPT>, SPT);
     }
     dim3 grid(P.nb, (P.J + kSlotNT - 1) / kSlotNT);
     if (init && pre)

@@ -1,3 +1,4 @@
+#include <cstdlib>
 // stream_launch.cu -- launchers of K4 (Wiener), the objective, the layout
 // transposes and the FP64 probe (stream.cuh).
 #include "dispatch.cuh"
@@ -19,6 +20,10 @@ cudaError_t launch_wiener(cudaStream_t s, int M, const WienerArgs& W, bool from_
     };
     if (from_x && noise) return go(k_wiener<MM, wiener_spt<MM, true>(), true, true>, wiener_spt<MM, true>());
     if (from_x) return go(k_wiener<MM, wiener_spt<MM, true>(), true, false>, wiener_spt<MM, true>());
+    const char* e = std::getenv("RCSCM_STREAM_SPT");  // tuning knob
+    const int spt = e ? std::atoi(e) : wiener_spt<MM, false>();
+    if (spt == 1) return go(k_wiener<MM, 1, false, false>, 1);
+    if (spt == 2) return go(k_wiener<MM, 2, false, false>, 2);
     return go(k_wiener<MM, wiener_spt<MM, false>(), false, false>, wiener_spt<MM, false>());
   });
 }

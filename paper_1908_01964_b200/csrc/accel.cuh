@@ -10,27 +10,30 @@
 //
 // Mapping: one CTA (CL == 1) or one thread-block cluster of CL CTAs per
 // frequency bin. Each thread owns SPT slots of the bin and keeps every
-// per-slot quantity (r_h, r_u, rho~_ax, tau_ax, s_ab*s_bx, s_bx, tau_xx, |s_bx|^2)
-// in REGISTERS for all iterations: HBM is touched once to load (56 B/slot) and
-// once to store (16 B/slot). The only cross-slot dependency -- lambda's sum over
-// frames -- is a fixed-order tree: in-thread pairwise sum, a warp total on the
-// FP64 tensor core (DMMA), a zero-padded 8-way block tree (+ DSMEM exchange
-// across the cluster), so results are deterministic and independent of how
-// many GPUs the bins are sharded over.
+// per-slot quantity (r_h, r_u, rho~_ax, tau_ax, c = s_ab s_bx / |s_ab|^2,
+// tau_xx / M, |s_bx|^2 / M) in REGISTERS for all iterations (SMEMC moves the
+// constants to shared memory): HBM is touched once on the way in and once on
+// the way out. With PREM = M the sigma / tau forms are computed from x in the
+// prologue (the precompute fused into the kernel). The only cross-slot
+// dependency -- lambda's sum over frames -- is a fixed-order tree: in-thread
+// pairwise sum, a warp total (one DMMA + a 3-level xor butterfly), a
+// zero-padded 4/8-way block tree (+ a DSMEM exchange across the cluster), so
+// results are deterministic and independent of how the bins are sharded.
 //
-// Latency structure: the lambda reduction is the only serial step of an
-// iteration, so each iteration computes the lambda-critical values first,
-// starts the warp reduction, and overlaps it with everything that does not
-// depend on the new lambda -- r_h and the two coefficients of r_u, which is
-// affine in 1/lambda_new (M r_u = P0 + P1/lambda_new). After the block total only
-// three FMAs per slot remain (r_u, and rho_ax for the next iteration).
+// Per iteration: the lambda-critical values first (gamma, 1/r~_u and the
+// lambda term), the warp reduction overlapped with r_h, then after the block
+// total r_u and rho_ax with lambda_new in the reference's order (DIRECT; the
+// non-DIRECT variant forms r_u as P0 + P1/lambda_new with all but three FMAs
+// before the reduction).
 //
-// Instruction budget per slot-iteration (47 canonical flops): 35 FP64 ops
-// (DFMA/DMUL) + 1 MUFU.RCP64H; floors run on the integer ALUs. The reference's
-// two divisions share one reciprocal (inv = 1/(D r~_u) gives gamma = r~_h r~_u inv
-// and 1/r~_u = D inv); gamma_fault rides in an FMA; 1/M is folded into the
-// per-slot constants (exact for power-of-two M); `max(v, eps)` keeps the
-// reference's std::max semantics.
+// Instruction budget per slot-iteration (47 canonical flops): 29 FP64 ops
+// (DFMA/DMUL/DADD, incl. the per-iteration reduction and lambda chain) + 1
+// MUFU.RCP64H; floors run on the integer ALUs. The reference's two divisions
+// share one reciprocal (inv = 1/(D r~_u) gives gamma = r~_h r~_u inv and
+// 1/r~_u = D inv); |s_ab|^2 leaves the per-slot lambda term (scaled residual);
+// gamma_fault rides in an FMA; 1/M is folded into the per-slot constants
+// (exact for power-of-two M); `max(v, eps)` keeps the reference's std::max
+// semantics. DESIGN.md section 4 records what bounds it on B200.
 #pragma once
 
 #include <cooperative_groups.h>

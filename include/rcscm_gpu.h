@@ -185,7 +185,7 @@ int rcscm_gpu_stft_synthesize(rcscm_gpu_ctx* ctx, const double* X, int64_t I,
 int rcscm_gpu_sphere(rcscm_gpu_ctx* ctx, int64_t I, int64_t J, int M, const double* X,
                      double* Q, double* Xw);
 /* ilrma.hpp:145-240: Gaussian ILRMA on (whitened) X [i][t][m] with K NMF bases
- * (K <= 32), iters IP + NMF sweeps and the reference's seeded initialisation.
+ * (K <= 16), iters IP + NMF sweeps and the reference's seeded initialisation.
  * Outputs (any may be NULL): W, A [i][M*M]; T [n] I x K col-major; V [n] K x J col-major. */
 int rcscm_gpu_run_ilrma(rcscm_gpu_ctx* ctx, int64_t I, int64_t J, int M, int K,
                         int iters, uint64_t seed, const double* X, double* W, double* A,

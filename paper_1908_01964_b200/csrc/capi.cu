@@ -89,7 +89,7 @@ struct rcscm_gpu_ctx {
   // STFT: waveform, window table, frames, half spectra, Spectrogram
   DBuf st_x, st_w, st_f, st_spec, st_X;
   // ILRMA: whitened x, W, A, T, V, powers, partial sums, mu
-  DBuf il_X, il_W, il_A, il_T, il_V, il_P, il_part, il_mu, il_vpart, il_ucov;
+  DBuf il_X, il_W, il_A, il_T, il_V, il_P, il_part, il_mu, il_Pt, il_ucov;
   // extract pipeline: whitening Q, folded W / A, target powers, output waveform,
   // objective trace
   DBuf ex_Q, ex_W, ex_A, ex_pow, ex_out, ex_obj;
@@ -859,7 +859,7 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->gam, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
                   &c->dryf, &c->imagef, &c->rh0f, &c->ru0f, &c->st_x, &c->st_w, &c->st_f, &c->st_spec,
-                  &c->st_X, &c->il_X, &c->il_W, &c->il_A, &c->il_T, &c->il_V, &c->il_P, &c->il_part, &c->il_mu, &c->il_vpart, &c->il_ucov,
+                  &c->st_X, &c->il_X, &c->il_W, &c->il_A, &c->il_T, &c->il_V, &c->il_P, &c->il_part, &c->il_mu, &c->il_Pt, &c->il_ucov,
                   &c->ex_Q, &c->ex_W, &c->ex_A, &c->ex_pow, &c->ex_out, &c->ex_obj})
     b->release();
   if (c->ev0) cudaEventDestroy(c->ev0);
@@ -1122,7 +1122,7 @@ static IlrmaArgs ilrma_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64
   if (K < 1) fail(RCSCM_INVALID_INPUT, "run_ilrma: K must be >= 1");
   if (iters < 0) fail(RCSCM_INVALID_INPUT, "run_ilrma: iters must be >= 0");
   check_mics(M);
-  if (K > 32) fail(RCSCM_UNSUPPORTED, "run_ilrma: K > 32 NMF bases is not supported on the GPU");
+  if (K > 16) fail(RCSCM_UNSUPPORTED, "run_ilrma: K > 16 NMF bases is not supported on the GPU");
   const size_t S = static_cast<size_t>(I * J);
   // NMF initialisation exactly as the reference (ilrma.hpp:162-173): one
   // mt19937_64 stream, per source T row-major over (i, k) then V over (k, t)
@@ -1152,7 +1152,7 @@ static IlrmaArgs ilrma_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64
   a.P = c->il_P.get<double>(S * M);
   a.partial = c->il_part.get<double>(static_cast<size_t>(ilrma_partials(I, J)) * M);
   a.mu = c->il_mu.get<double>(M);
-  a.vpart = c->il_vpart.get<double>(static_cast<size_t>(ilrma_vpart(I, J, K)) * M);
+  a.Pt = c->il_Pt.get<double>(S * M);
   a.ucov = c->il_ucov.get<double2>(static_cast<size_t>(I) * M * M * M);
   a.err = c->err.get<unsigned long long>(1);
   if (I == 0) return a;
@@ -1161,9 +1161,9 @@ static IlrmaArgs ilrma_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64
   h2d(c, a.V, hV.data(), hV.size() * sizeof(double));
   reset_err(c);
   c->launched(launch_ilrma_powers(c->stream, a, M));
-  for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 3);
+  for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
   for (int it = 0; it < iters; ++it) {
-    c->launched(launch_ilrma_nmf(c->stream, a, M), 3);
+    c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
     c->launched(launch_ilrma_ip_scale(c->stream, a, M), 5);
   }
   c->launched(launch_ilrma_inverse(c->stream, a, M));

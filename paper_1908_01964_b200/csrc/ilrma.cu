@@ -9,11 +9,10 @@
 // Kernels (all reductions in a fixed order, so results are deterministic):
 //   k_sphere       CTA per bin: covariance (lower triangle, block tree), one
 //                  thread's Jacobi eig -> Q, then Q x for every frame
-//   k_nmf_t        CTA per (bin, source): R, P/R^2, 1/R on the fly, the K
+//   k_nmf_t        warp per (bin, source): R, P/R^2, 1/R on the fly, the K
 //                  numerator / denominator sums over frames, T update
-//   k_nmf_v        CTA per (32-frame tile, source, 64-bin chunk): the chunk's K
-//                  sums over bins with the new T; k_nmf_v_fin sums the chunks in
-//                  order and updates V
+//   k_nmf_v        warp per (frame, source) over a transposed copy of P: the K
+//                  sums over bins with the new T, V update
 //   k_ip_cov       CTA per (bin, source): the weighted covariance U_n (lower
 //                  triangle, block tree) -- independent of W, so all in parallel
 //   k_ip_solve     thread per bin: the sequential row updates
@@ -217,13 +216,55 @@ __global__ void __launch_bounds__(NT) k_sphere(const double2* __restrict__ X, in
 }
 
 // ---- NMF (ilrma.hpp:100-123) -----------------------------------------------------
-// T update for (bin i = blockIdx.x, source n = blockIdx.y)
-template <int KMAX, int NT>
-__global__ void __launch_bounds__(NT) k_nmf_t(IlrmaArgs A) {
-  __shared__ double red[NT / 32 * 2 * KMAX];
-  __shared__ double tot[2 * KMAX];
-  const int64_t i = blockIdx.x, I = A.I, J = A.J;
-  const int n = blockIdx.y, K = A.K;
+// Warp reduce-scatter of 32 values per lane: after five halving steps (31
+// shuffles instead of 32 x 5 for a butterfly per value) lane l holds the warp
+// total of value l. Each partial sum is formed once, in a fixed order, so the
+// result is deterministic.
+__device__ __forceinline__ double warp_reduce_scatter32(const double (&v)[32]) {
+  const int lane = threadIdx.x & 31;
+  double a[16];
+  {
+    const bool up = lane & 16;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const double keep = up ? v[j + 16] : v[j], send = up ? v[j] : v[j + 16];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+    }
+  }
+#pragma unroll
+  for (int m = 8; m > 0; m >>= 1) {
+    const bool up = lane & m;
+#pragma unroll
+    for (int j = 0; j < m; ++j) {
+      const double keep = up ? a[j + m] : a[j], send = up ? a[j] : a[j + m];
+      a[j] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  return a[0];
+}
+// Warp totals of NV <= 32 values (zero-padded to 32): lane l gets the total of
+// value l (0 for l >= NV).
+template <int NV>
+__device__ __forceinline__ double warp_totals(const double (&v)[NV]) {
+  static_assert(NV <= 32, "at most 32 values");
+  double w[32];
+#pragma unroll
+  for (int e = 0; e < 32; ++e) w[e] = e < NV ? v[e] : 0.0;
+  return warp_reduce_scatter32(w);
+}
+
+// T update: one warp per (bin i, source n); lanes stride over frames, R = T V,
+// P / R^2 and 1 / R on the fly, the K numerator / denominator sums over frames
+// by a warp butterfly, lane k rewrites T(i, k).
+template <int KMAX>
+__global__ void __launch_bounds__(128) k_nmf_t(IlrmaArgs A, int M) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t I = A.I, J = A.J;
+  const int K = A.K;
+  if (w >= I * M) return;
+  const int n = static_cast<int>(w / I);
+  const int64_t i = w % I;
   double* T = A.T + static_cast<int64_t>(n) * I * K;
   const double* V = A.V + static_cast<int64_t>(n) * K * J;
   const double* P = A.P + (static_cast<int64_t>(n) * I + i) * J;
@@ -233,14 +274,13 @@ __global__ void __launch_bounds__(NT) k_nmf_t(IlrmaArgs A) {
     tk[k] = k < K ? T[i + k * I] : 0.0;
     acc[2 * k] = acc[2 * k + 1] = 0.0;
   }
-  __syncthreads();  // every thread has read T(i, :) before thread k rewrites it
-  for (int64_t t = threadIdx.x; t < J; t += NT) {
+  for (int64_t t = lane; t < J; t += 32) {
     double s = 0.0;
 #pragma unroll
     for (int k = 0; k < KMAX; ++k)
       if (k < K) s = fma(tk[k], V[k + t * K], s);
     const double r = fmax(s, kNmfVarFloor);
-    const double pr2 = P[t] / (r * r), rinv = 1.0 / r;
+    const double rinv = rcp_pos(r), pr2 = P[t] * rinv * rinv;  // MUFU + Newton, no IEEE divisions
 #pragma unroll
     for (int k = 0; k < KMAX; ++k)
       if (k < K) {
@@ -249,82 +289,52 @@ __global__ void __launch_bounds__(NT) k_nmf_t(IlrmaArgs A) {
         acc[2 * k + 1] = fma(rinv, v, acc[2 * k + 1]);
       }
   }
-  block_sum<NT, 2 * KMAX>(acc, red, tot);
-  // thread k alone reads and rewrites T(i, k)
-  for (int k = threadIdx.x; k < K; k += NT)
-    T[i + k * I] = fmax(T[i + k * I] * sqrt(tot[2 * k] / fmax(tot[2 * k + 1], 1e-300)), 1e-300);
+  // lane 2k: numerator total of base k; lane 2k + 1: its denominator (2 K <= 32)
+  const double tot = warp_totals<2 * KMAX>(acc);
+  const double den = __shfl_down_sync(0xffffffffu, tot, 1);
+  const int k = lane >> 1;
+  if (!(lane & 1) && k < K) T[i + k * I] = fmax(T[i + k * I] * sqrt(tot / fmax(den, 1e-300)), 1e-300);
 }
 
-// V update, pass 1: CTA per (32-frame tile = blockIdx.x, source n = blockIdx.y,
-// chunk of kVChunk bins = blockIdx.z), 32 x 8 threads; the K numerator /
-// denominator sums of the chunk go to vpart[n][chunk][t][2K] (fixed order within)
-constexpr int kVChunk = 64;
+// V update: one warp per (frame t, source n) over the transposed powers
+// Pt[n][t][bin]; lanes stride over bins with the new T, lane k rewrites V(k, t).
 template <int KMAX>
-__global__ void __launch_bounds__(256) k_nmf_v(IlrmaArgs A) {
-  __shared__ double acc_s[32][2 * KMAX];
+__global__ void __launch_bounds__(128) k_nmf_v(IlrmaArgs A, int M) {
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
   const int64_t I = A.I, J = A.J;
-  const int n = blockIdx.y, K = A.K;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t t = static_cast<int64_t>(blockIdx.x) * 32 + tx;
-  const int64_t i0 = static_cast<int64_t>(blockIdx.z) * kVChunk, i1 = min(I, i0 + kVChunk);
+  const int K = A.K;
+  if (w >= J * M) return;
+  const int n = static_cast<int>(w / J);
+  const int64_t t = w % J;
   const double* T = A.T + static_cast<int64_t>(n) * I * K;
-  const double* V = A.V + static_cast<int64_t>(n) * K * J;
-  const double* P = A.P + static_cast<int64_t>(n) * I * J;
+  double* V = A.V + static_cast<int64_t>(n) * K * J;
+  const double* Pt = A.Pt + (static_cast<int64_t>(n) * J + t) * I;
   double vk[KMAX], acc[2 * KMAX];
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) {
-    vk[k] = (k < K && t < J) ? V[k + t * K] : 0.0;
+    vk[k] = k < K ? V[k + t * K] : 0.0;
     acc[2 * k] = acc[2 * k + 1] = 0.0;
   }
-  if (t < J) {
-    for (int64_t i = i0 + ty; i < i1; i += 8) {
-      double s = 0.0;
+  for (int64_t i = lane; i < I; i += 32) {
+    double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k)
-        if (k < K) s = fma(T[i + k * I], vk[k], s);
-      const double r = fmax(s, kNmfVarFloor);
-      const double pr2 = P[i * J + t] / (r * r), rinv = 1.0 / r;
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) s = fma(T[i + k * I], vk[k], s);
+    const double r = fmax(s, kNmfVarFloor);
+    const double rinv = rcp_pos(r), pr2 = Pt[i] * rinv * rinv;
 #pragma unroll
-      for (int k = 0; k < KMAX; ++k)
-        if (k < K) {
-          const double tv = T[i + k * I];
-          acc[2 * k] = fma(tv, pr2, acc[2 * k]);
-          acc[2 * k + 1] = fma(tv, rinv, acc[2 * k + 1]);
-        }
-    }
+    for (int k = 0; k < KMAX; ++k)
+      if (k < K) {
+        const double tv = T[i + k * I];
+        acc[2 * k] = fma(tv, pr2, acc[2 * k]);
+        acc[2 * k + 1] = fma(tv, rinv, acc[2 * k + 1]);
+      }
   }
-  // fixed-order sum over the 8 row groups
-  for (int y = 0; y < 8; ++y) {
-    if (ty == y) {
-#pragma unroll
-      for (int e = 0; e < 2 * KMAX; ++e) acc_s[tx][e] = (y == 0 ? 0.0 : acc_s[tx][e]) + acc[e];
-    }
-    __syncthreads();
-  }
-  if (ty == 0 && t < J) {
-    double* dst = A.vpart + ((static_cast<int64_t>(n) * gridDim.z + blockIdx.z) * J + t) * (2 * K);
-    for (int e = 0; e < 2 * K; ++e) dst[e] = acc_s[tx][e];
-  }
-}
-
-// V update, pass 2: thread per (frame, source) sums the chunks in order
-__global__ void k_nmf_v_fin(IlrmaArgs A, int nchunks, int M) {
-  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  const int64_t J = A.J;
-  const int K = A.K;
-  if (q >= J * M) return;
-  const int n = static_cast<int>(q / J);
-  const int64_t t = q % J;
-  double* V = A.V + static_cast<int64_t>(n) * K * J;
-  for (int k = 0; k < K; ++k) {
-    double num = 0.0, den = 0.0;
-    for (int c = 0; c < nchunks; ++c) {
-      const double* src = A.vpart + ((static_cast<int64_t>(n) * nchunks + c) * J + t) * (2 * K);
-      num += src[2 * k];
-      den += src[2 * k + 1];
-    }
-    V[k + t * K] = fmax(V[k + t * K] * sqrt(num / fmax(den, 1e-300)), 1e-300);
-  }
+  const double tot = warp_totals<2 * KMAX>(acc);
+  const double den = __shfl_down_sync(0xffffffffu, tot, 1);
+  const int k = lane >> 1;
+  if (!(lane & 1) && k < K) V[k + t * K] = fmax(V[k + t * K] * sqrt(tot / fmax(den, 1e-300)), 1e-300);
 }
 
 // ---- iterative projection (ilrma.hpp:190-216) -----------------------------------
@@ -371,6 +381,57 @@ __global__ void __launch_bounds__(NT) k_ip_cov(IlrmaArgs A) {
     }
     r += c;
     const double2 v = make_double2(tot[2 * q] / static_cast<double>(J), tot[2 * q + 1] / static_cast<double>(J));
+    U[r + c * M] = v;
+    U[c + r * M] = cconj(v);
+  }
+}
+
+// Pass 1, warp form for M <= 5 (2 * NE <= 32): one warp per (bin, source),
+// lanes stride over frames, the lower triangle reduced by a warp reduce-scatter.
+template <int M>
+__global__ void __launch_bounds__(128) k_ip_cov_warp(IlrmaArgs A) {
+  constexpr int NE = M * (M + 1) / 2;
+  static_assert(2 * NE <= 32, "warp form needs 2 NE <= 32");
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const int64_t I = A.I, J = A.J;
+  const int K = A.K;
+  if (w >= I * M) return;
+  const int n = static_cast<int>(w % M);
+  const int64_t i = w / M;
+  const double* T = A.T + static_cast<int64_t>(n) * I * K;
+  const double* V = A.V + static_cast<int64_t>(n) * K * J;
+  double acc[2 * NE];
+#pragma unroll
+  for (int e = 0; e < 2 * NE; ++e) acc[e] = 0.0;
+  for (int64_t t = lane; t < J; t += 32) {
+    double s = 0.0;
+    for (int k = 0; k < K; ++k) s = fma(T[i + k * I], V[k + t * K], s);
+    const double wt = rcp_pos(fmax(s, kNmfVarFloor));
+    double2 x[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) x[m] = A.X[(i * J + t) * M + m];
+    int e = 0;
+#pragma unroll
+    for (int c = 0; c < M; ++c)
+#pragma unroll
+      for (int r = c; r < M; ++r, ++e) {
+        const double2 v = cscale(cmul(x[r], cconj(x[c])), wt);
+        acc[2 * e] += v.x;
+        acc[2 * e + 1] += v.y;
+      }
+  }
+  const double tot = warp_totals<2 * NE>(acc);  // lane 2q: Re of entry q, lane 2q + 1: Im
+  const double im = __shfl_down_sync(0xffffffffu, tot, 1);
+  if (!(lane & 1) && lane < 2 * NE) {
+    int q = lane >> 1, c = 0;
+    while (q >= M - c) {
+      q -= M - c;
+      ++c;
+    }
+    const int r = q + c;
+    const double2 v = make_double2(tot / static_cast<double>(J), im / static_cast<double>(J));
+    double2* U = A.ucov + (i * M + n) * M * M;
     U[r + c * M] = v;
     U[c + r * M] = cconj(v);
   }
@@ -455,6 +516,7 @@ __global__ void __launch_bounds__(NT) k_powers(IlrmaArgs A) {
       for (int c = 0; c < M; ++c) y = cfma(sW[n + c * M], x[c], y);
       const double p = cnorm(y);
       A.P[(static_cast<int64_t>(n) * I + i) * J + t] = p;
+      A.Pt[(static_cast<int64_t>(n) * J + t) * I + i] = p;
       acc[n] = p;
     }
   }
@@ -492,7 +554,10 @@ __global__ void k_scale_apply(IlrmaArgs A, int M) {
     if (q < nP) {
       n = static_cast<int>(q / (I * J));
       const double mu = A.mu[n];
-      if (mu > 0.0 && isfinite(mu)) A.P[q] /= mu * mu;
+      if (mu > 0.0 && isfinite(mu)) {
+        A.P[q] /= mu * mu;
+        A.Pt[q] /= mu * mu;  // same source-major extent, transposed within
+      }
     } else if (q < nP + nT) {
       const int64_t r = q - nP;
       n = static_cast<int>(r / (I * K));
@@ -601,14 +666,10 @@ cudaError_t launch_sphere(cudaStream_t s, int M, const double2* X, int64_t I, in
 
 int64_t ilrma_partials(int64_t I, int64_t J) { return I * ((J + kIlrmaNT - 1) / kIlrmaNT); }
 
-int64_t ilrma_vpart(int64_t I, int64_t J, int K) { return ((I + kVChunk - 1) / kVChunk) * J * 2 * K; }
-
 template <int KMAX>
 static cudaError_t nmf_update(cudaStream_t s, const IlrmaArgs& A, int M) {
-  k_nmf_t<KMAX, kIlrmaNT><<<dim3(static_cast<unsigned>(A.I), M), kIlrmaNT, 0, s>>>(A);
-  const int nchunks = static_cast<int>((A.I + kVChunk - 1) / kVChunk);
-  k_nmf_v<KMAX><<<dim3(static_cast<unsigned>((A.J + 31) / 32), M, nchunks), 256, 0, s>>>(A);
-  k_nmf_v_fin<<<static_cast<unsigned>((A.J * M + 127) / 128), 128, 0, s>>>(A, nchunks, M);
+  k_nmf_t<KMAX><<<static_cast<unsigned>((A.I * M + 3) / 4), 128, 0, s>>>(A, M);
+  k_nmf_v<KMAX><<<static_cast<unsigned>((A.J * M + 3) / 4), 128, 0, s>>>(A, M);
   return cudaGetLastError();
 }
 
@@ -616,7 +677,6 @@ cudaError_t launch_ilrma_nmf(cudaStream_t s, const IlrmaArgs& A, int M) {
   if (A.K <= 4) return nmf_update<4>(s, A, M);
   if (A.K <= 8) return nmf_update<8>(s, A, M);
   if (A.K <= 16) return nmf_update<16>(s, A, M);
-  if (A.K <= 32) return nmf_update<32>(s, A, M);
   return cudaErrorInvalidValue;
 }
 
@@ -632,7 +692,10 @@ cudaError_t launch_ilrma_powers(cudaStream_t s, const IlrmaArgs& A, int M) {
 cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M) {
   cudaError_t e = dispatch_mics(M, [&](auto mm) {
     constexpr int MM = decltype(mm)::value;
-    k_ip_cov<MM, kIlrmaNT><<<dim3(static_cast<unsigned>(A.I), MM), kIlrmaNT, 0, s>>>(A);
+    if constexpr (MM * (MM + 1) <= 32)
+      k_ip_cov_warp<MM><<<static_cast<unsigned>((A.I * MM + 3) / 4), 128, 0, s>>>(A);
+    else
+      k_ip_cov<MM, kIlrmaNT><<<dim3(static_cast<unsigned>(A.I), MM), kIlrmaNT, 0, s>>>(A);
     constexpr int tpb = lu_tpb<MM>();
     k_ip_solve<MM><<<static_cast<unsigned>((A.I + tpb - 1) / tpb), tpb, 0, s>>>(A);
     return cudaGetLastError();

@@ -78,18 +78,16 @@ struct IlrmaArgs {
   double* T;         // [n][I x K col-major]
   double* V;         // [n][K x J col-major]
   double* P;         // [n][bin][t]
+  double* Pt;        // [n][t][bin] (the same powers, transposed for the V update)
   double* partial;   // [n][ilrma_partials(I, J)]
   double* mu;        // [n]
-  double* vpart;     // [n][ilrma_vpart(I, J, K)]
   double2* ucov;     // [bin][n][M*M] IP weighted covariances
   unsigned long long* err;
 };
 int64_t ilrma_partials(int64_t I, int64_t J);
-// V-update partial sums per source: chunks x J x 2K doubles
-int64_t ilrma_vpart(int64_t I, int64_t J, int K);
 cudaError_t launch_sphere(cudaStream_t s, int M, const double2* X, int64_t I, int64_t J, double2* Q, double2* Xw);
 cudaError_t launch_ilrma_powers(cudaStream_t s, const IlrmaArgs& A, int M);
-cudaError_t launch_ilrma_nmf(cudaStream_t s, const IlrmaArgs& A, int M);     // K <= 32
+cudaError_t launch_ilrma_nmf(cudaStream_t s, const IlrmaArgs& A, int M);     // K <= 16
 cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M);  // IP sweep + powers + scaling
 cudaError_t launch_ilrma_inverse(cudaStream_t s, const IlrmaArgs& A, int M);
 // W = W_ilrma Q, Am = W^{-1} per bin (A.W holds W_ilrma)

@@ -491,6 +491,144 @@ __global__ void __launch_bounds__(lu_tpb<M>()) k_ip_solve(IlrmaArgs A) {
   for (int k = 0; k < M * M; ++k) A.W[i * M * M + k] = W[k];
 }
 
+// Pass 2, warp form for M <= 5: one warp per bin, lane l < M*M holding entry
+// (l % M, l / M) -- column-major, so the lane index is Eigen's pivot tie-break
+// order. The same FullPivLU pivot / rank rules and row updates as k_ip_solve,
+// with the pivot search a warp (max |a|^2, min lane) reduction and the row /
+// column swaps and eliminations lane shuffles.
+__device__ __forceinline__ double2 shfl2(double2 v, int src) {
+  return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+template <int M>
+__global__ void __launch_bounds__(128) k_ip_solve_warp(IlrmaArgs A) {
+  static_assert(M * M <= 32, "warp form needs M*M <= 32");
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x) >> 5;
+  if (i >= A.I) return;
+  const bool act = lane < M * M;
+  const int r = lane % M, c = lane / M;
+  double2 W = act ? A.W[i * M * M + lane] : make_double2(0.0, 0.0);
+  for (int n = 0; n < M; ++n) {
+    const double2 U = act ? A.ucov[(i * M + n) * M * M + lane] : make_double2(0.0, 0.0);
+    // WU(r, c) = sum_k W(r, k) U(k, c)
+    auto form_wu = [&](double load) {
+      double2 s = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        const double2 w = shfl2(W, act ? r + k * M : 0), u = shfl2(U, act ? k + c * M : 0);
+        s = cfma(w, u, s);
+      }
+      if (r == c) s.x += load;
+      return act ? s : make_double2(0.0, 0.0);
+    };
+    double2 a = form_wu(0.0);
+    double nrm = cnorm(a);
+#pragma unroll
+    for (int m = 16; m > 0; m >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, m);
+    int rowp[M], colp[M], nonzero = M;
+    double maxpivot = 0.0;
+    auto factor = [&]() {
+      nonzero = M;
+      maxpivot = 0.0;
+      bool done = false;
+#pragma unroll
+      for (int k = 0; k < M; ++k) {
+        // pivot: max |a|^2 over the corner r, c >= k; ties -> lowest lane
+        double v = (act && r >= k && c >= k && !done) ? cnorm(a) : -1.0;
+        int l = lane;
+#pragma unroll
+        for (int m = 16; m > 0; m >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, v, m);
+          const int ol = __shfl_xor_sync(0xffffffffu, l, m);
+          if (ov > v || (ov == v && ol < l)) {
+            v = ov;
+            l = ol;
+          }
+        }
+        if (!done && v == 0.0) {
+          nonzero = k;
+          done = true;
+        }
+        const int br = done ? k : l % M, bc = done ? k : l / M;
+        rowp[k] = br;
+        colp[k] = bc;
+        if (done) continue;
+        maxpivot = fmax(maxpivot, sqrt(v));
+        // swap rows k and br, then columns k and bc
+        int src = lane;
+        if (r == k) src = br + c * M;
+        else if (r == br) src = k + c * M;
+        a = shfl2(a, act ? src : lane);
+        src = lane;
+        if (c == k) src = r + bc * M;
+        else if (c == bc) src = r + k * M;
+        a = shfl2(a, act ? src : lane);
+        const double2 piv = shfl2(a, k + k * M);
+        if (act && c == k && r > k) a = cdiv(a, piv);
+        const double2 lrk = shfl2(a, act ? r + k * M : 0);  // L(r, k) after the division
+        const double2 ukc = shfl2(a, act ? k + c * M : 0);  // U(k, c)
+        if (act && r > k && c > k) a = csub(a, cmul(lrk, ukc));
+      }
+    };
+    factor();
+    const double thr = M * 2.220446049250313e-16 * maxpivot;
+    auto rank_ok = [&]() {
+      const bool big = act && r == c && r < nonzero && hypot(a.x, a.y) > thr;
+      return __popc(__ballot_sync(0xffffffffu, big)) == M;
+    };
+    bool ok = rank_ok();
+    if (!ok) {  // diagonal-loading retry (ilrma.hpp:205-211)
+      a = form_wu(1e-8 * fmax(sqrt(nrm), 1e-30));
+      factor();
+      ok = rank_ok();
+    }
+    if (!ok) {
+      if (lane == 0) report_error(A.err, i * A.J, kErrIlrmaSpatial);
+      return;  // the bin keeps its W
+    }
+    // solve (W U) w = e_n with the factors: lanes 0..M-1 hold y
+    double2 y = make_double2(lane == n ? 1.0 : 0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < M; ++k) {  // row transpositions
+      const double2 yk = shfl2(y, k), yb = shfl2(y, rowp[k]);
+      if (lane == k) y = yb;
+      else if (lane == rowp[k]) y = yk;
+    }
+#pragma unroll
+    for (int q = 0; q < M; ++q) {  // forward (unit lower)
+      const double2 yq = shfl2(y, q);
+      const double2 lrq = shfl2(a, lane < M ? lane + q * M : 0);
+      if (lane > q && lane < M) y = csub(y, cmul(lrq, yq));
+    }
+#pragma unroll
+    for (int q = M - 1; q >= 0; --q) {  // backward (upper)
+      const double2 uqq = shfl2(a, q + q * M);
+      if (lane == q) y = cdiv(y, uqq);
+      const double2 yq = shfl2(y, q);
+      const double2 urq = shfl2(a, lane < M ? lane + q * M : 0);
+      if (lane < q) y = csub(y, cmul(urq, yq));
+    }
+#pragma unroll
+    for (int k = M - 1; k >= 0; --k) {  // column transpositions
+      const double2 yk = shfl2(y, k), yb = shfl2(y, colp[k]);
+      if (lane == k) y = yb;
+      else if (lane == colp[k]) y = yk;
+    }
+    // q = w^H U w; lane (r, c) forms U(r, c) w(c), rows summed in c order
+    const double2 wc = shfl2(y, act ? c : 0);
+    double2 t = act ? cmul(U, wc) : make_double2(0.0, 0.0);
+    double2 uw = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int cc = 0; cc < M; ++cc) uw = cadd(uw, shfl2(t, act ? r + cc * M : 0));  // lane (r, *): (U w)_r
+    double2 qv = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int rr = 0; rr < M; ++rr) qv = cfmac(shfl2(y, rr), shfl2(uw, rr), qv);
+    const double sc = sqrt(fmax(qv.x, 1e-300));
+    if (act && r == n) W = cconj(make_double2(wc.x / sc, wc.y / sc));
+  }
+  if (act) A.W[i * M * M + lane] = W;
+}
+
 // ---- demixed powers, scale normalisation, final inverse --------------------------
 // P[n][i][t] = |(W_i x_it)_n|^2; partial[n][cta] = this CTA's sum (grid: bins x chunks)
 template <int M, int NT>
@@ -696,8 +834,12 @@ cudaError_t launch_ilrma_ip_scale(cudaStream_t s, const IlrmaArgs& A, int M) {
       k_ip_cov_warp<MM><<<static_cast<unsigned>((A.I * MM + 3) / 4), 128, 0, s>>>(A);
     else
       k_ip_cov<MM, kIlrmaNT><<<dim3(static_cast<unsigned>(A.I), MM), kIlrmaNT, 0, s>>>(A);
-    constexpr int tpb = lu_tpb<MM>();
-    k_ip_solve<MM><<<static_cast<unsigned>((A.I + tpb - 1) / tpb), tpb, 0, s>>>(A);
+    if constexpr (MM * MM <= 32) {
+      k_ip_solve_warp<MM><<<static_cast<unsigned>((A.I + 3) / 4), 128, 0, s>>>(A);
+    } else {
+      constexpr int tpb = lu_tpb<MM>();
+      k_ip_solve<MM><<<static_cast<unsigned>((A.I + tpb - 1) / tpb), tpb, 0, s>>>(A);
+    }
     return cudaGetLastError();
   });
   if (e != cudaSuccess) return e;

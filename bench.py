@@ -325,6 +325,7 @@ def run_gpu(args):
                 "avg_launch_ms": k2_avg,
                 "peak_source": "measured live: DFMA probe (rcscm_gpu_probe_fp64) on this GPU; MEASURED_PEAKS.json "
                                "has no FP64 figure",
+                "frac_basis": "of measured (FP64 pipe; the kernel is neither HBM- nor tensor-bound)",
                 "nominal_peak": NOMINAL_FP64_TFLOPS,
                 "frac_of_nominal": achieved / NOMINAL_FP64_TFLOPS}
 
@@ -423,7 +424,8 @@ def stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, 
 
     def entry(ms, bps, n):
         gbs = bps * n / (ms * 1e-3) / 1e9
-        return {"ms": ms, "bytes_per_slot": bps, "slots": n, "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm}
+        return {"ms": ms, "bytes_per_slot": bps, "slots": n, "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm,
+                "frac_basis": "of measured (MEASURED_PEAKS.json hbm_gbs)"}
 
     ctx.session_run(C.STAGE_PRECOMPUTE, 0, hyper)
     out = {"k_pre": entry(cold(ctx, C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S),

@@ -1,0 +1,153 @@
+// capi_internal.h -- shared internals of the C ABI translation units (capi.cu:
+// the reference entry points, solvers and session; capi_pipeline.cu: STFT,
+// sphering, ILRMA and the device cmd_extract chain). Not a public header.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/rcscm_gpu.h"
+#include "launch.h"
+
+using namespace rcscm;
+
+namespace rcscm_capi {
+
+extern thread_local std::string g_last_error;
+
+struct ApiError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw ApiError{code, msg}; }
+
+#define CK(expr)                                                                                      \
+  do {                                                                                                \
+    cudaError_t e_ = (expr);                                                                          \
+    if (e_ != cudaSuccess) fail(RCSCM_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// Grow-only device buffer.
+struct DBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t n) {
+    const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+    if (bytes > cap) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      cap = 0;
+      CK(cudaMalloc(&p, bytes));
+      cap = bytes;
+    }
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+constexpr int kMaxChunks = 16;
+
+inline void check_mics(int M) {
+  if (!mics_supported(M)) fail(RCSCM_UNSUPPORTED, "mics = " + std::to_string(M) + " is not supported (1..8 or 16)");
+}
+
+}  // namespace rcscm_capi
+
+using rcscm_capi::DBuf;
+using rcscm_capi::fail;
+
+struct rcscm_gpu_ctx {
+  int device = 0;
+  int precision = RCSCM_C128;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int64_t launches = 0;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t aux[2] = {nullptr, nullptr};  // copy / compute streams of the pipelined entry points
+  cudaEvent_t evx[19] = {};                       // kMaxChunks + 3
+  // device buffers
+  DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
+  DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
+  DBuf gam;  // Algorithm 1 scratch (gamma per slot)
+  // STFT: waveform, window table, frames, half spectra, Spectrogram
+  DBuf st_x, st_w, st_f, st_spec, st_X;
+  // ILRMA: whitened x, W, A, T, V, powers, partial sums, mu
+  DBuf il_X, il_W, il_A, il_T, il_V, il_P, il_part, il_mu, il_Pt, il_ucov;
+  // extract pipeline: whitening Q, folded W / A, target powers, output waveform,
+  // objective trace
+  DBuf ex_Q, ex_W, ex_A, ex_pow, ex_out, ex_obj;
+  StftPlan stft_plan;
+  // complex64 (FP32) mode copies of the slot arrays
+  DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef, rh0f, ru0f;
+  bool f32_params_current = false;  // session: FP32 r_h / r_u hold the latest iterate
+  // session geometry
+  bool s_loaded = false, s_setup = false, s_pre = false;
+  // RESET is applied lazily: the next ACCEL reads params0 directly (no copy
+  // pass); any other consumer of the iterate materialises it first.
+  bool s_reset_pending = false;
+  int64_t sB = 0, sI = 0, sJ = 0;
+  int sM = 0, sK = 0, sn_h = 0;
+
+  // Every kernel launch goes through here: the error is surfaced as
+  // RCSCM_CUDA_ERROR and the launch counter (rcscm_gpu_launch_count) advances.
+  void launched(cudaError_t e, int n = 1) {
+    if (e != cudaSuccess) fail(RCSCM_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
+    launches += n;
+  }
+};
+
+namespace rcscm_capi {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RCSCM_OK;
+  } catch (const ApiError& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RCSCM_CUDA_ERROR;
+  }
+}
+
+
+// helpers defined in capi.cu
+void h2d(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes);
+void d2h(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes);
+void d2d(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes);
+void sync(rcscm_gpu_ctx* c);
+void reset_err(rcscm_gpu_ctx* c);
+void check_err(rcscm_gpu_ctx* c, int64_t J);
+DevProblem problem(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M);
+bool f32(const rcscm_gpu_ctx* c);
+void params_from_f32(rcscm_gpu_ctx* c, size_t S);
+Accel1Args accel1_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int iters, const rcscm_hyper& h, double eps,
+                       double gamma_fault);
+// MAP objective (dev_out: leave the value in that device slot, no host round trip)
+double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h, double* dev_out = nullptr);
+double objective_fast(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h,
+                      double* dev_out = nullptr);
+// session_load from host (H2D) or device (D2D) buffers
+void session_load_impl(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M, int K, int n_h, const void* X,
+                       const void* W, const void* A, const void* T, const void* V, cudaMemcpyKind kind);
+
+}  // namespace rcscm_capi

@@ -213,6 +213,10 @@ typedef struct {
   int64_t bins, frames;
   double* objective;                  /* caller buffer, >= iters + 1 entries, or NULL */
   int n_objective;
+  double* iter_seconds;               /* caller buffer, >= iters entries, or NULL: CUDA-event
+                                         time of each solver iteration, objective excluded
+                                         (solver_accel.hpp:205,227); without compute_objective
+                                         the iterations run as one launch and share its time */
 } rcscm_extract_result;
 int rcscm_gpu_extract(rcscm_gpu_ctx* ctx, const rcscm_extract_opts* opts,
                       const double* samples, int64_t num_samples, int M,

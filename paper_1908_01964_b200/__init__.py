@@ -25,4 +25,4 @@ from .api import (  # noqa: F401
     run_algorithm2,
     run_naive,
 )
-from . import synth  # noqa: F401
+from . import records, synth  # noqa: F401

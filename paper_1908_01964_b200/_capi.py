@@ -109,6 +109,7 @@ class CExtractResult(ctypes.Structure):
         ("frames", ctypes.c_int64),
         ("objective", _dp),
         ("n_objective", ctypes.c_int),
+        ("iter_seconds", _dp),
     ]
 
 

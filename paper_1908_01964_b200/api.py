@@ -375,7 +375,8 @@ class GpuContext:
         """STFT -> sphere -> ILRMA -> fold -> target index -> build_noise_scm ->
         init_params -> solver -> Wiener image / noise -> WOLA synthesis, all on the
         device. samples (M, len) -> dict(target, noise (M, len), target_index,
-        objective, n_iters)."""
+        objective, n_iters, iter_seconds); records.write_trace takes the last two
+        as cmd_extract's trace.jsonl."""
         hyper = hyper or Hyperparams()
         x = np.asarray(samples, np.float64)
         M, n = x.shape
@@ -385,12 +386,14 @@ class GpuContext:
                            {"naive": 0, "accel1": 1, "accel2": 2}[backend], int(iters), hyper.alpha, hyper.beta,
                            float(eps_var), float(rel_obj_tol), int(bool(compute_objective)))
         obj = np.zeros(max(iters, 0) + 1)
-        r = C.CExtractResult(0, 0, 0, 0, _p(obj), 0)
+        secs = np.zeros(max(iters, 1))
+        r = C.CExtractResult(0, 0, 0, 0, _p(obj), 0, _p(secs))
         tgt = np.zeros((n, M))
         noi = np.zeros((n, M))
         _raise(self._lib.rcscm_gpu_extract(self._h, ctypes.byref(o), _p(xt), n, M, _p(tgt), _p(noi), ctypes.byref(r)))
         return {"target": np.ascontiguousarray(tgt.T), "noise": np.ascontiguousarray(noi.T),
                 "target_index": r.target_index, "objective": obj[:r.n_objective].tolist(), "n_iters": r.n_iters,
+                "iter_seconds": secs[:r.n_iters].tolist(),
                 "bins": r.bins, "frames": r.frames}
 
     # ---- device-resident session ---------------------------------------------

@@ -281,9 +281,25 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
     if (want_obj && o->backend == 2) c->launched(launch_logpdet(c->stream, problem(c, 1, I, J, M)));
     if (want_obj) objv.push_back(eval());
     const int step = want_obj ? 1 : o->iters;
+    // per-step CUDA events for iter_seconds (solver_accel.hpp:205,227: objective excluded)
+    const bool want_secs = res && res->iter_seconds && o->iters > 0;
+    struct Events {  // destroyed on every exit path, including fail()
+      std::vector<cudaEvent_t> v;
+      ~Events() {
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
+      }
+    } evs;
+    std::vector<int> ev_n;
+    auto event = [&] {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      evs.v.push_back(e);
+      CK(cudaEventRecord(e, c->stream));
+    };
     int done = 0;
     while (done < o->iters) {
       const int n = std::min(step, o->iters - done);
+      if (want_secs) event();
       if (o->backend == 2) {
         rc = rcscm_gpu_session_run(c, RCSCM_STAGE_ACCEL, n, &h, o->eps_var);
         if (rc != RCSCM_OK) fail(rc, rcscm_gpu_last_error());
@@ -295,6 +311,10 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
         c->launched(launch_accel1(c->stream, M, accel1_args(c, I, J, n, h, o->eps_var, 0.0)));
       }
       done += n;
+      if (want_secs) {
+        event();
+        ev_n.push_back(n);
+      }
       if (want_obj) {
         objv.push_back(eval());
         const double prev = objv[objv.size() - 2], cur = objv.back();
@@ -337,6 +357,12 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
       if (res->objective && want_obj)
         std::memcpy(res->objective, objv.data(), objv.size() * sizeof(double));
       res->n_objective = static_cast<int>(objv.size());
+      int k = 0;
+      for (size_t q = 0; q < ev_n.size(); ++q) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, evs.v[2 * q], evs.v[2 * q + 1]));
+        for (int r = 0; r < ev_n[q]; ++r) res->iter_seconds[k++] = 1e-3 * ms / ev_n[q];
+      }
     }
   });
 }

@@ -57,6 +57,7 @@ def test_gpu_extract_matches_oracle(O, gpu, M, n, K, ilrma_iters, iters):
     assert float(np.max(np.abs(g["target"] - tw)) / np.max(np.abs(tw))) <= bar
     assert float(np.max(np.abs(g["noise"] - nw)) / np.max(np.abs(nw))) <= bar
     assert len(g["objective"]) == iters + 1
+    assert len(g["iter_seconds"]) == g["n_iters"] == iters and min(g["iter_seconds"]) > 0
     dobj = max(abs(a - b) for a, b in zip(obj, objp))
     assert np.allclose(g["objective"], obj, rtol=max(1e-8, 50 * dobj / max(abs(obj[-1]), 1e-300)), atol=0)
     # x = target image + noise (wiener.hpp:46-53) survives the linear synthesis

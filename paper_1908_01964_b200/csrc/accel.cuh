@@ -87,6 +87,14 @@ struct AccelArgs {
   double2* sigma_bx_w;
   double2* tau_ax_w;
   double* tau_xx_w;
+  // per-iteration MAP objective (TRAJ variants, obj_part != null): after
+  // iteration it, CTA b stores its slots' sum of the O(1) objective terms
+  // (k_objective_fast's formula) at obj_part[it * gridDim.x + b]
+  double* obj_part;
+  const double* logpdet;  // [bin] log pdet R'
+  double alpha, beta;
+  int mics;
+  unsigned long long* err;
 };
 
 // std::max(v, eps) of the reference (returns v unless v < eps) for eps > 0,
@@ -195,6 +203,7 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
   constexpr bool F32 = sizeof(T) == 4;
   constexpr int kMaxWarps = 256 / 32;
   __shared__ __align__(16) double red[2][kMaxWarps];  // zero-padded warp partials
+  __shared__ double ored[TRAJ ? kMaxWarps : 1];        // objective warp partials (TRAJ)
   // cluster exchange: cl_vals[buf][r] receives rank r's CTA partial, cl_bar[buf]
   // counts the CL arrivals (double-buffered by iteration parity)
   __shared__ __align__(16) double cl_vals[2][16];
@@ -522,16 +531,50 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       }
       K2_PROBE(5, ru[0]);
       if constexpr (TRAJ) {
+        if (P.traj_r_h) {
 #pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-          if (valid[k]) {
-            const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
-            const int64_t o = static_cast<int64_t>(it) * P.nb * J + base + t;
-            P.traj_r_h[o] = rh[k];
-            P.traj_r_u[o] = ru[k];
+          for (int k = 0; k < SPT; ++k) {
+            if (valid[k]) {
+              const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+              const int64_t o = static_cast<int64_t>(it) * P.nb * J + base + t;
+              P.traj_r_h[o] = rh[k];
+              P.traj_r_u[o] = ru[k];
+            }
+          }
+          if (rank == 0 && tid == 0) P.traj_lambda[static_cast<int64_t>(it) * P.nb + bin] = lam;
+        }
+        if (P.obj_part) {
+          // model.hpp:129-157 through the scalar expansion (k_objective_fast):
+          // log det R_x = M log pi + log pdet R' + log lambda + (M-1) log r_u + log D,
+          // x^H R_x^-1 x = (rho_xx - (r_h / D) |rho_ax|^2) / r_u, D = r_u + r_h rho_aa;
+          // rho_* with the new lambda (rax now holds rho_ax, xd / M the rho_xx parts)
+          const int Mi = P.mics;
+          const double cbin = Mi * log(3.14159265358979323846) + P.logpdet[bin] + log(lam);
+          double v = 0.0;
+#pragma unroll
+          for (int k = 0; k < SPT; ++k) {
+            if (FULL || valid[k]) {
+              const CT xd = get_xd(k);
+              const double rhk = static_cast<double>(rh[k]), ruk = static_cast<double>(ru[k]);
+              const double rxx = Mi * fma(static_cast<double>(xd.y), il, static_cast<double>(xd.x));
+              const double D = fma(rhk, raa, ruk);
+              const double logdet = cbin + (Mi - 1) * log(ruk) + log(D);
+              const double quad = (rxx - rhk / D * static_cast<double>(cnorm(rax[k]))) / ruk;
+              const double val = -logdet - quad - (P.alpha + 1.0) * log(rhk) - P.beta / rhk;
+              if (!isfinite(val))
+                report_error(P.err, base + t0 + static_cast<int64_t>(k) * NT + tid, kErrObjectiveNonFinite);
+              v += val;
+            }
+          }
+          v = warp_sum(v);
+          if (lane == 0) ored[warp] = v;
+          __syncthreads();
+          if (tid == 0) {
+            double sum = 0.0;
+            for (int w = 0; w < NT / 32; ++w) sum += ored[w];
+            P.obj_part[static_cast<int64_t>(it) * gridDim.x + blockIdx.x] = sum;
           }
         }
-        if (rank == 0 && tid == 0) P.traj_lambda[static_cast<int64_t>(it) * P.nb + bin] = lam;
       }
     }
   };

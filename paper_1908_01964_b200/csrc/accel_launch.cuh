@@ -55,7 +55,7 @@ cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt
 
 template <int CL>
 cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
-  const bool traj = A.traj_r_h != nullptr;
+  const bool traj = A.traj_r_h != nullptr || A.obj_part != nullptr;  // per-iteration recording
   if (g.f32) {  // complex64 mode: direct form, registers only
     if constexpr (CL == 1) {
       if (g.full && g.minb && g.nt <= 128) return launch_accel_spt<CL, true, false, 0, 3, true, float>(s, A, g.nt, g.spt);

@@ -62,6 +62,30 @@ struct DBuf {
   }
 };
 
+// Page-locked host staging (grown on demand): waveform copies at full DMA rate
+// instead of the driver's pageable path.
+struct HBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  template <class T>
+  T* get(size_t n) {
+    const size_t bytes = std::max<size_t>(n * sizeof(T), 16);
+    if (bytes > cap) {
+      if (p) cudaFreeHost(p);
+      p = nullptr;
+      cap = 0;
+      CK(cudaMallocHost(&p, bytes));
+      cap = bytes;
+    }
+    return static_cast<T*>(p);
+  }
+  void release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
 constexpr int kMaxChunks = 16;
 
 inline void check_mics(int M) {
@@ -71,6 +95,7 @@ inline void check_mics(int M) {
 }  // namespace rcscm_capi
 
 using rcscm_capi::DBuf;
+using rcscm_capi::HBuf;
 using rcscm_capi::fail;
 
 struct rcscm_gpu_ctx {
@@ -86,6 +111,7 @@ struct rcscm_gpu_ctx {
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
   DBuf gam;  // Algorithm 1 scratch (gamma per slot)
+  DBuf obj_part;  // K2's per-iteration, per-CTA objective partials
   // STFT: waveform, window table, frames, half spectra, Spectrogram
   DBuf st_x, st_w, st_f, st_spec, st_X;
   // ILRMA: whitened x, W, A, T, V, powers, partial sums, mu
@@ -93,7 +119,13 @@ struct rcscm_gpu_ctx {
   // extract pipeline: whitening Q, folded W / A, target powers, output waveform,
   // objective trace
   DBuf ex_Q, ex_W, ex_A, ex_pow, ex_out, ex_obj;
+  HBuf ex_pin;  // pinned staging of the waveforms in and out
   StftPlan stft_plan;
+  // ILRMA sweeps replayed as one CUDA graph, re-captured when the shape, the
+  // buffers or the sweep count change (key: IlrmaArgs fields, M, iters)
+  cudaGraphExec_t il_graph = nullptr;
+  std::vector<int64_t> il_graph_key;
+  int il_graph_launches = 0;
   // complex64 (FP32) mode copies of the slot arrays
   DBuf Xf, sbxf, taxf, txxf, rhf, ruf, dryf, imagef, rh0f, ru0f;
   bool f32_params_current = false;  // session: FP32 r_h / r_u hold the latest iterate
@@ -146,6 +178,13 @@ Accel1Args accel1_args(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int iters, const
 double objective(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h, double* dev_out = nullptr);
 double objective_fast(rcscm_gpu_ctx* c, int64_t nb, int64_t J, int M, const rcscm_hyper& h,
                       double* dev_out = nullptr);
+// Algorithm 2 for `iters` iterations with the objective after each iteration
+// evaluated inside K2 into dobj[1..iters] (dobj[0]: the caller's initial value);
+// optional trajectory buffers ([it][bin][t], [it][bin]). One K2 launch + one
+// row reduction; complex128 only.
+void run_accel_obj(rcscm_gpu_ctx* c, int64_t I, int64_t J, int M, int iters, const rcscm_hyper& h, double eps,
+                   double gamma_fault, double* dobj, double* trh = nullptr, double* tru = nullptr,
+                   double* trl = nullptr);
 // session_load from host (H2D) or device (D2D) buffers
 void session_load_impl(rcscm_gpu_ctx* c, int64_t B, int64_t I, int64_t J, int M, int K, int n_h, const void* X,
                        const void* W, const void* A, const void* T, const void* V, cudaMemcpyKind kind);

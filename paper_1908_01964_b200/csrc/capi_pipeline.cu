@@ -2,9 +2,50 @@
 // STFT analysis / WOLA synthesis (stft.hpp), sphering and ILRMA (ilrma.hpp) and
 // the whole cmd_extract chain on the device (tools/rcscm.cpp:158-221). Kernels:
 // stft.cu, ilrma.cu; the SCM stages reuse the session of capi.cu.
+#include <thread>
+
 #include "capi_internal.h"
 
 using namespace rcscm_capi;
+
+namespace {
+
+// Replays the ~7 (iters + 5) launches of the ILRMA sweeps as one CUDA graph:
+// launch overhead, not kernel time, dominated them at the reference's sizes.
+template <typename F>
+static void ilrma_graph_launch(rcscm_gpu_ctx* c, const IlrmaArgs& a, int M, int iters, F&& sweeps) {
+  const std::vector<int64_t> key{a.I, a.J, a.K, M, iters, reinterpret_cast<int64_t>(a.X),
+                                 reinterpret_cast<int64_t>(a.W), reinterpret_cast<int64_t>(a.A),
+                                 reinterpret_cast<int64_t>(a.T), reinterpret_cast<int64_t>(a.V),
+                                 reinterpret_cast<int64_t>(a.P), reinterpret_cast<int64_t>(a.Pt),
+                                 reinterpret_cast<int64_t>(a.partial), reinterpret_cast<int64_t>(a.mu),
+                                 reinterpret_cast<int64_t>(a.ucov), reinterpret_cast<int64_t>(a.err)};
+  if (!c->il_graph || key != c->il_graph_key) {
+    if (c->il_graph) cudaGraphExecDestroy(c->il_graph);
+    c->il_graph = nullptr;
+    const int64_t before = c->launches;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+    cudaGraph_t g = nullptr;
+    try {
+      sweeps();
+    } catch (...) {
+      cudaStreamEndCapture(c->stream, &g);
+      if (g) cudaGraphDestroy(g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(c->stream, &g));
+    const cudaError_t ie = cudaGraphInstantiate(&c->il_graph, g, 0);
+    cudaGraphDestroy(g);
+    CK(ie);
+    c->il_graph_key = key;
+    c->il_graph_launches = static_cast<int>(c->launches - before);
+  } else {
+    c->launches += c->il_graph_launches;
+  }
+  CK(cudaGraphLaunch(c->il_graph, c->stream));
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -178,13 +219,21 @@ static IlrmaArgs ilrma_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64
   h2d(c, a.T, hT.data(), hT.size() * sizeof(double));
   h2d(c, a.V, hV.data(), hV.size() * sizeof(double));
   reset_err(c);
-  c->launched(launch_ilrma_powers(c->stream, a, M));
-  for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
-  for (int it = 0; it < iters; ++it) {
-    c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
-    c->launched(launch_ilrma_ip_scale(c->stream, a, M), 5);
+  auto sweeps = [&] {
+    c->launched(launch_ilrma_powers(c->stream, a, M));
+    for (int pass = 0; pass < 30; ++pass) c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
+    for (int it = 0; it < iters; ++it) {
+      c->launched(launch_ilrma_nmf(c->stream, a, M), 2);
+      c->launched(launch_ilrma_ip_scale(c->stream, a, M), 5);
+    }
+    c->launched(launch_ilrma_inverse(c->stream, a, M));
+  };
+  const char* e = std::getenv("RCSCM_ILRMA_GRAPH");
+  if (c->stream == nullptr || (e && std::atoi(e) == 0)) {
+    sweeps();  // the legacy default stream cannot be captured
+  } else {
+    ilrma_graph_launch(c, a, M, iters, sweeps);
   }
-  c->launched(launch_ilrma_inverse(c->stream, a, M));
   check_err(c, J > 0 ? J : 1);
   return a;
 }
@@ -222,8 +271,11 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
     check_mics(M);
     const rcscm_hyper h{o->alpha, o->beta};
     // 1. STFT (stft.hpp:50-88)
-    double* dx = c->st_x.get<double>(static_cast<size_t>(num_samples) * M);
-    h2d(c, dx, samples, static_cast<size_t>(num_samples) * M * sizeof(double));
+    const size_t nw = static_cast<size_t>(num_samples) * M;  // samples per waveform
+    double* pin = c->ex_pin.get<double>(2 * nw);  // [target | noise] on the way out
+    std::memcpy(pin, samples, nw * sizeof(double));
+    double* dx = c->st_x.get<double>(nw);
+    h2d(c, dx, pin, nw * sizeof(double));
     int win = 0, hop = 0;
     int64_t J = 0, I = 0;
     stft_analyze_dev(c, dx, num_samples, M, o->sample_rate, o->win_ms, o->hop_ms, &win, &hop, &J, &I);
@@ -297,6 +349,18 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
       CK(cudaEventRecord(e, c->stream));
     };
     int done = 0;
+    if (obj_dev && o->backend == 2 && !f32(c) && o->iters > 0) {
+      // no early stop: every iteration and its objective in one K2 launch
+      if (want_secs) event();
+      run_accel_obj(c, I, J, M, o->iters, h, o->eps_var, 0.0, dobj);
+      if (want_secs) {
+        event();
+        ev_n.push_back(o->iters);
+      }
+      done = o->iters;
+      nobj = o->iters + 1;
+      objv.resize(nobj);
+    }
     while (done < o->iters) {
       const int n = std::min(step, o->iters - done);
       if (want_secs) event();
@@ -338,17 +402,26 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
     Wa.image = c->image.get<double2>(S * M);
     Wa.noise = c->noise.get<double2>(S * M);
     c->launched(launch_wiener(c->stream, M, Wa, true, true));
-    double* dout = c->ex_out.get<double>(static_cast<size_t>(num_samples) * M);
-    if (target) {
-      stft_synth_dev(c, Wa.image, I, J, M, win, hop, num_samples, dout);
-      d2h(c, target, dout, static_cast<size_t>(num_samples) * M * sizeof(double));
-    }
-    if (noise) {
-      sync(c);
-      stft_synth_dev(c, Wa.noise, I, J, M, win, hop, num_samples, dout);
-      d2h(c, noise, dout, static_cast<size_t>(num_samples) * M * sizeof(double));
+    // both waveforms synthesised into one device buffer, one D2H into the
+    // pinned stage, then host copies into the caller's buffers
+    double* dout = c->ex_out.get<double>(2 * nw);
+    if (target) stft_synth_dev(c, Wa.image, I, J, M, win, hop, num_samples, dout);
+    if (noise) stft_synth_dev(c, Wa.noise, I, J, M, win, hop, num_samples, dout + nw);
+    if (target && noise) {
+      d2h(c, pin, dout, 2 * nw * sizeof(double));
+    } else if (target || noise) {
+      d2h(c, target ? pin : pin + nw, target ? dout : dout + nw, nw * sizeof(double));
     }
     sync(c);
+    if (target && noise) {
+      std::thread th([&] { std::memcpy(noise, pin + nw, nw * sizeof(double)); });
+      std::memcpy(target, pin, nw * sizeof(double));
+      th.join();
+    } else if (target) {
+      std::memcpy(target, pin, nw * sizeof(double));
+    } else if (noise) {
+      std::memcpy(noise, pin + nw, nw * sizeof(double));
+    }
     if (res) {
       res->target_index = n_h;
       res->n_iters = done;

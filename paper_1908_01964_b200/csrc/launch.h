@@ -56,6 +56,7 @@ cudaError_t launch_objective_fast(cudaStream_t s, ObjFastArgs O, int64_t* np);
 // objective partial sums (np = grid size written to *np) and the final sum
 cudaError_t launch_objective(cudaStream_t s, int M, ObjArgs O, int64_t* np);
 cudaError_t launch_sum_partials(cudaStream_t s, const double* partial, int64_t n, double* out);
+cudaError_t launch_sum_rows(cudaStream_t s, const double* partial, int rows, int64_t n, double* out);
 // reference I x J column-major (leading dimension ld, 0 = I) <-> device [bin][t]
 // (B blocks of I bins)
 cudaError_t launch_to_bt(cudaStream_t s, const double* src, double* dst, int64_t B, int64_t I, int64_t J,

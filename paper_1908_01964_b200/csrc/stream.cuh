@@ -286,6 +286,23 @@ static __global__ void k_sum_partials(const double* partial, int64_t n, double* 
   }
 }
 
+// Row totals of a rows x n partial array (K2's per-iteration objective
+// partials): block r sums row r in k_sum_partials' fixed order.
+static __global__ void k_sum_rows(const double* partial, int64_t n, double* out) {
+  __shared__ double red[32];
+  const double* row = partial + static_cast<int64_t>(blockIdx.x) * n;
+  double s = 0.0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s += row[k];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += red[w];
+    out[blockIdx.x] = tot;
+  }
+}
+
 // Reference I x J column-major (element (i, t) at i + t*ld, ld >= I) -> device
 // [i][t] (element at i*J + t), per utterance block z of I bins (source block
 // stride ld*J). 32 x 32 smem tiles.

@@ -52,6 +52,12 @@ cudaError_t launch_sum_partials(cudaStream_t s, const double* partial, int64_t n
   return cudaGetLastError();
 }
 
+cudaError_t launch_sum_rows(cudaStream_t s, const double* partial, int rows, int64_t n, double* out) {
+  if (rows <= 0) return cudaSuccess;
+  k_sum_rows<<<rows, 1024, 0, s>>>(partial, n, out);
+  return cudaGetLastError();
+}
+
 template <class T, bool TO_BT>
 static cudaError_t transpose(cudaStream_t s, const T* src, T* dst, int64_t B, int64_t I, int64_t J, int64_t ld) {
   if (B * I * J == 0) return cudaSuccess;

@@ -300,6 +300,27 @@ def test_objective_and_monotone(O, gpu):  # test_solver_accel.cpp:320-332, test_
             assert obj[k] >= obj[k - 1] - 1e-7 * abs(obj[k - 1])
 
 
+@pytest.mark.parametrize("cfg,I,J,iters", [(0, 16, 320, 100), (1, 8, 640, 60), (4, 3, 4096, 30), (2, 2, 20000, 20)])
+def test_objective_in_kernel(O, gpu, cfg, I, J, iters):
+    """compute_objective without an early stop evaluates the objective inside
+    K2 after every iteration (per-CTA partials; J = 4096 / 20000 run as
+    clusters): equal to the oracle's per-iteration map_objective within 1e-9,
+    to the per-iteration launch path (rel_obj_tol > 0 that never fires) within
+    1e-12, and the parameters and trajectory bitwise equal to a run without
+    the objective."""
+    u, inp, p0 = _synthetic(O, cfg, I, J)
+    res = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=iters, compute_objective=True, record_trajectory=True))
+    oo = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=iters, compute_objective=True))
+    assert len(res.objective) == iters + 1 and len(res.iter_seconds) == iters
+    assert np.allclose(res.objective, oo.objective, rtol=1e-9, atol=0)
+    step = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=iters, compute_objective=True, rel_obj_tol=1e-300))
+    assert np.allclose(res.objective, step.objective, rtol=1e-12, atol=0)
+    plain = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=iters, record_trajectory=True))
+    for f in ("r_h", "r_u", "lam"):
+        assert np.array_equal(getattr(res.params, f), getattr(plain.params, f)), f
+        assert np.array_equal(getattr(res.trajectory[-1], f), getattr(plain.trajectory[-1], f)), f
+
+
 def test_early_stop(O, gpu):  # test_solver_naive.cpp:209-218
     inp, p, X = O.make_verify_instance(2, 6, 2, 10)
     res = gpu.run_naive(inp, p, _hyper(), X, _opts(iters=500, compute_objective=True, rel_obj_tol=1e-6))

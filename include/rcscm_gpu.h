@@ -197,7 +197,8 @@ int rcscm_gpu_run_ilrma(rcscm_gpu_ctx* ctx, int64_t I, int64_t J, int M, int K,
  * -> solver (backend 0 naive, 1 Algorithm 1, 2 Algorithm 2; optional objective
  * per iteration with the rel_obj_tol early stop) -> extract_target / extract_noise
  * -> WOLA synthesis, with every intermediate resident in HBM. samples, target and
- * noise are M x num_samples col-major (Waveform::samples); target / noise may be NULL. */
+ * noise are M x num_samples col-major (Waveform::samples) or channel rows
+ * (samples_layout); target / noise may be NULL. */
 typedef struct {
   double sample_rate, win_ms, hop_ms; /* 16000, 64, 32 in cmd_extract */
   int nmf_bases, ilrma_iters;         /* RunConfig defaults 10, 50 */
@@ -207,6 +208,9 @@ typedef struct {
   int iters;
   double alpha, beta, eps_var, rel_obj_tol;
   int compute_objective;              /* cmd_extract sets it */
+  int samples_layout;                 /* 0: samples / target / noise M x num_samples col-major
+                                         (Waveform::samples); 1: one contiguous row of
+                                         num_samples per channel (numpy (M, n) C order) */
 } rcscm_extract_opts;
 typedef struct {
   int target_index, n_iters;

@@ -98,6 +98,7 @@ class CExtractOpts(ctypes.Structure):
         ("eps_var", ctypes.c_double),
         ("rel_obj_tol", ctypes.c_double),
         ("compute_objective", ctypes.c_int),
+        ("samples_layout", ctypes.c_int),
     ]
 
 

@@ -371,27 +371,32 @@ class GpuContext:
     def extract(self, samples, sample_rate: float = 16000.0, nmf_bases: int = 10, ilrma_iters: int = 50,
                 seed: int = 0, target_index: int = -1, backend: str = "accel2", iters: int = 100,
                 hyper: Optional["Hyperparams"] = None, eps_var: float = 1e-12, compute_objective: bool = True,
-                rel_obj_tol: float = 0.0, win_ms: float = 64.0, hop_ms: float = 32.0):
+                rel_obj_tol: float = 0.0, win_ms: float = 64.0, hop_ms: float = 32.0, layout: str = "rows"):
         """STFT -> sphere -> ILRMA -> fold -> target index -> build_noise_scm ->
         init_params -> solver -> Wiener image / noise -> WOLA synthesis, all on the
         device. samples (M, len) -> dict(target, noise (M, len), target_index,
         objective, n_iters, iter_seconds); records.write_trace takes the last two
         as cmd_extract's trace.jsonl."""
         hyper = hyper or Hyperparams()
+        # layout "rows": channel rows as numpy holds them (samples_layout 1, no
+        # transposes); "interleaved": the reference's Waveform::samples order (0)
+        inter = {"rows": False, "interleaved": True}[layout]
         x = np.asarray(samples, np.float64)
         M, n = x.shape
-        xt = np.ascontiguousarray(x.T)
+        x = np.ascontiguousarray(x.T if inter else x)
         o = C.CExtractOpts(float(sample_rate), float(win_ms), float(hop_ms), int(nmf_bases), int(ilrma_iters),
                            int(seed) & (2**64 - 1), int(target_index),
                            {"naive": 0, "accel1": 1, "accel2": 2}[backend], int(iters), hyper.alpha, hyper.beta,
-                           float(eps_var), float(rel_obj_tol), int(bool(compute_objective)))
+                           float(eps_var), float(rel_obj_tol), int(bool(compute_objective)), 0 if inter else 1)
         obj = np.zeros(max(iters, 0) + 1)
         secs = np.zeros(max(iters, 1))
         r = C.CExtractResult(0, 0, 0, 0, _p(obj), 0, _p(secs))
-        tgt = np.zeros((n, M))
-        noi = np.zeros((n, M))
-        _raise(self._lib.rcscm_gpu_extract(self._h, ctypes.byref(o), _p(xt), n, M, _p(tgt), _p(noi), ctypes.byref(r)))
-        return {"target": np.ascontiguousarray(tgt.T), "noise": np.ascontiguousarray(noi.T),
+        tgt = np.empty((n, M) if inter else (M, n))
+        noi = np.empty((n, M) if inter else (M, n))
+        _raise(self._lib.rcscm_gpu_extract(self._h, ctypes.byref(o), _p(x), n, M, _p(tgt), _p(noi), ctypes.byref(r)))
+        if inter:
+            tgt, noi = np.ascontiguousarray(tgt.T), np.ascontiguousarray(noi.T)
+        return {"target": tgt, "noise": noi,
                 "target_index": r.target_index, "objective": obj[:r.n_objective].tolist(), "n_iters": r.n_iters,
                 "iter_seconds": secs[:r.n_iters].tolist(),
                 "bins": r.bins, "frames": r.frames}

@@ -79,7 +79,8 @@ int rcscm_gpu_stft_shape(int64_t num_samples, double sample_rate, double win_ms,
 
 // device STFT of the device waveform dx (M x len) into c->st_X ([bin][frame][mic])
 static void stft_analyze_dev(rcscm_gpu_ctx* c, const double* dx, int64_t len, int M, double sample_rate,
-                             double win_ms, double hop_ms, int* win_o, int* hop_o, int64_t* J_o, int64_t* B_o) {
+                             double win_ms, double hop_ms, int* win_o, int* hop_o, int64_t* J_o, int64_t* B_o,
+                             bool planar = false) {
   int win = 0, hop = 0;
   stft_params(sample_rate, win_ms, hop_ms, &win, &hop);
   const int64_t J = (len + (win - hop) + hop - 1) / hop, B = win / 2 + 1, rows = J * M;
@@ -89,7 +90,7 @@ static void stft_analyze_dev(rcscm_gpu_ctx* c, const double* dx, int64_t len, in
   double2* dX = c->st_X.get<double2>(static_cast<size_t>(B * rows));
   c->launched(launch_stft_analyze(c->stream, c->stft_plan, dx, len, M, win, hop, J, dw,
                                   c->st_f.get<double>(static_cast<size_t>(rows) * win),
-                                  c->st_spec.get<double2>(static_cast<size_t>(rows * B)), dX),
+                                  c->st_spec.get<double2>(static_cast<size_t>(rows * B)), dX, planar),
               3);
   *win_o = win;
   *hop_o = hop;
@@ -99,7 +100,7 @@ static void stft_analyze_dev(rcscm_gpu_ctx* c, const double* dx, int64_t len, in
 
 // device WOLA synthesis of dX ([bin][frame][mic], I = win/2 + 1 bins) into dout (M x len)
 static void stft_synth_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64_t J, int M, int win, int hop,
-                           int64_t len, double* dout) {
+                           int64_t len, double* dout, bool planar = false) {
   const std::vector<double> w = hamming(win);
   std::vector<double> denom(hop, 0.0), dual(win);
   for (int k = 0; k < win; ++k) denom[k % hop] += w[k] * w[k];
@@ -109,7 +110,7 @@ static void stft_synth_dev(rcscm_gpu_ctx* c, const double2* dX, int64_t I, int64
   const int64_t rows = J * M;
   c->launched(launch_stft_synthesize(c->stream, c->stft_plan, dX, I, J, M, win, hop, len, dd,
                                      c->st_spec.get<double2>(static_cast<size_t>(rows * I)),
-                                     c->st_f.get<double>(static_cast<size_t>(rows) * win), dout),
+                                     c->st_f.get<double>(static_cast<size_t>(rows) * win), dout, planar),
               4);
 }
 
@@ -268,6 +269,7 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
     if (num_samples <= 0 || M <= 0) fail(RCSCM_INVALID_INPUT, "stft_analyze: empty waveform");
     if (o->iters < 0) fail(RCSCM_INVALID_INPUT, "run_accelerated: iters must be >= 0");
     if (o->backend < 0 || o->backend > 2) fail(RCSCM_INVALID_INPUT, "extract: unknown backend");
+    if (o->samples_layout != 0 && o->samples_layout != 1) fail(RCSCM_INVALID_INPUT, "extract: unknown samples_layout");
     check_mics(M);
     const rcscm_hyper h{o->alpha, o->beta};
     // 1. STFT (stft.hpp:50-88)
@@ -278,7 +280,8 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
     h2d(c, dx, pin, nw * sizeof(double));
     int win = 0, hop = 0;
     int64_t J = 0, I = 0;
-    stft_analyze_dev(c, dx, num_samples, M, o->sample_rate, o->win_ms, o->hop_ms, &win, &hop, &J, &I);
+    const bool planar = o->samples_layout == 1;
+    stft_analyze_dev(c, dx, num_samples, M, o->sample_rate, o->win_ms, o->hop_ms, &win, &hop, &J, &I, planar);
     const size_t S = static_cast<size_t>(I * J);
     const double2* dX = c->st_X.as<double2>();
     // 2. sphering + ILRMA in the whitened domain (ilrma.hpp:53-73, :145-240)
@@ -405,8 +408,8 @@ int rcscm_gpu_extract(rcscm_gpu_ctx* c, const rcscm_extract_opts* o, const doubl
     // both waveforms synthesised into one device buffer, one D2H into the
     // pinned stage, then host copies into the caller's buffers
     double* dout = c->ex_out.get<double>(2 * nw);
-    if (target) stft_synth_dev(c, Wa.image, I, J, M, win, hop, num_samples, dout);
-    if (noise) stft_synth_dev(c, Wa.noise, I, J, M, win, hop, num_samples, dout + nw);
+    if (target) stft_synth_dev(c, Wa.image, I, J, M, win, hop, num_samples, dout, planar);
+    if (noise) stft_synth_dev(c, Wa.noise, I, J, M, win, hop, num_samples, dout + nw, planar);
     if (target && noise) {
       d2h(c, pin, dout, 2 * nw * sizeof(double));
     } else if (target || noise) {

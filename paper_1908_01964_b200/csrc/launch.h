@@ -109,15 +109,16 @@ struct StftPlan {
   void reset();
   cudaError_t ensure(int win, int64_t batch, cudaStream_t s);
 };
-// x: (ch, p) at ch + p*M; window[win]; scratch frames[J*M*win], spec[J*M*(win/2+1)];
-// X out: [bin][frame][mic] (stft.hpp:50-88)
+// x: (ch, p) at ch + p*M (planar: ch*len + p); window[win]; scratch
+// frames[J*M*win], spec[J*M*(win/2+1)]; X out: [bin][frame][mic] (stft.hpp:50-88)
 cudaError_t launch_stft_analyze(cudaStream_t s, StftPlan& plan, const double* x, int64_t len, int M, int win,
                                 int hop, int64_t J, const double* window, double* frames, double2* spec,
-                                double2* X);
-// X: [bin][frame][mic], B bins; dual_n = WOLA dual window / win; out (ch, p) at ch + p*M (stft.hpp:92-129)
+                                double2* X, bool planar = false);
+// X: [bin][frame][mic], B bins; dual_n = WOLA dual window / win; out (ch, p) at
+// ch + p*M (planar: ch*len + p) (stft.hpp:92-129)
 cudaError_t launch_stft_synthesize(cudaStream_t s, StftPlan& plan, const double2* X, int64_t B, int64_t J, int M,
                                    int win, int hop, int64_t len, const double* dual_n, double2* spec,
-                                   double* frames, double* out);
+                                   double* frames, double* out, bool planar = false);
 cudaError_t launch_fp32_probe(cudaStream_t s, int blocks, int iters, double* out);
 
 // complex64 (FP32) mode

@@ -16,15 +16,17 @@
 
 namespace rcscm {
 
-// F[(j*M + ch)*win + k] = x(ch, j*hop - pad + k) * w[k] (0 outside [0, len))
+// F[(j*M + ch)*win + k] = x(ch, j*hop - pad + k) * w[k] (0 outside [0, len));
+// x(ch, p) at ch + p*M (Waveform::samples, M x len col-major) or, planar, at
+// ch*len + p (one contiguous row per channel)
 __global__ void k_stft_frames(const double* __restrict__ x, int64_t len, int M, int win, int hop, int64_t J,
-                              const double* __restrict__ w, double* __restrict__ F) {
+                              const double* __restrict__ w, double* __restrict__ F, bool planar) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t r = blockIdx.y;
   if (k >= win || r >= J * M) return;
   const int64_t j = r / M, ch = r % M;
   const int64_t p = j * hop - (win - hop) + k;
-  F[r * win + k] = (p >= 0 && p < len) ? x[ch + p * M] * w[k] : 0.0;
+  F[r * win + k] = (p >= 0 && p < len) ? x[planar ? ch * len + p : ch + p * M] * w[k] : 0.0;
 }
 
 // Half-spectrum input of the inverse transform: the imaginary parts of DC and
@@ -42,10 +44,10 @@ __global__ void k_stft_clear_edges(double2* Z, int64_t rows, int64_t B, bool nyq
 // (stft.hpp:118-125; the 1/win is the inverse DFT's normalisation, exact for
 // power-of-two win, folded into the dual-window table on the host).
 __global__ void k_stft_ola(const double* __restrict__ F, int64_t len, int M, int win, int hop, int64_t J,
-                           const double* __restrict__ dual_n, double* __restrict__ out) {
-  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // = ch + p*M
+                           const double* __restrict__ dual_n, double* __restrict__ out, bool planar) {
+  const int64_t q = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;  // ch + p*M, or ch*len + p
   if (q >= len * M) return;
-  const int64_t p = q / M, ch = q % M;
+  const int64_t p = planar ? q % len : q / M, ch = planar ? q / len : q % M;
   const int64_t pad = win - hop;
   // frames j with j*hop - pad <= p < j*hop - pad + win
   int64_t j0 = p + pad - win + 1;
@@ -100,13 +102,13 @@ cudaError_t StftPlan::ensure(int win, int64_t b, cudaStream_t s) {
 
 cudaError_t launch_stft_analyze(cudaStream_t s, StftPlan& plan, const double* x, int64_t len, int M, int win,
                                 int hop, int64_t J, const double* window, double* frames, double2* spec,
-                                double2* X) {
+                                double2* X, bool planar) {
   const int64_t rows = J * M, B = win / 2 + 1;
   if (rows == 0) return cudaSuccess;
   cudaError_t e = plan.ensure(win, rows, s);
   if (e != cudaSuccess) return e;
   k_stft_frames<<<dim3((win + 255) / 256, static_cast<unsigned>(rows)), 256, 0, s>>>(x, len, M, win, hop, J, window,
-                                                                                  frames);
+                                                                                  frames, planar);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   e = cufft_status(cufftExecD2Z(static_cast<cufftHandle>(plan.fwd), frames, reinterpret_cast<cufftDoubleComplex*>(spec)));
   if (e != cudaSuccess) return e;
@@ -116,7 +118,7 @@ cudaError_t launch_stft_analyze(cudaStream_t s, StftPlan& plan, const double* x,
 
 cudaError_t launch_stft_synthesize(cudaStream_t s, StftPlan& plan, const double2* X, int64_t B, int64_t J, int M,
                                    int win, int hop, int64_t len, const double* dual_n, double2* spec,
-                                   double* frames, double* out) {
+                                   double* frames, double* out, bool planar) {
   const int64_t rows = J * M;
   if (len * M == 0) return cudaSuccess;
   cudaError_t e = plan.ensure(win, rows, s);
@@ -126,7 +128,7 @@ cudaError_t launch_stft_synthesize(cudaStream_t s, StftPlan& plan, const double2
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   e = cufft_status(cufftExecZ2D(static_cast<cufftHandle>(plan.inv), reinterpret_cast<cufftDoubleComplex*>(spec), frames));
   if (e != cudaSuccess) return e;
-  k_stft_ola<<<static_cast<unsigned>((len * M + 255) / 256), 256, 0, s>>>(frames, len, M, win, hop, J, dual_n, out);
+  k_stft_ola<<<static_cast<unsigned>((len * M + 255) / 256), 256, 0, s>>>(frames, len, M, win, hop, J, dual_n, out, planar);
   return cudaGetLastError();
 }
 

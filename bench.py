@@ -430,6 +430,29 @@ def stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, 
     ctx.session_run(C.STAGE_PRECOMPUTE, 0, hyper)
     out = {"k_pre": entry(cold(ctx, C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S),
            "k_wiener": entry(cold(ctx, C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S)}
+
+    def copy_cold(nbytes, reps=7):
+        # torch's device copy moving the same bytes (half read, half written),
+        # timed like the kernels: what a plain stream achieves at this size
+        n = max(int(nbytes // 8), 1)
+        src = torch.ones(n, dtype=torch.float32, device=f"cuda:{local}")
+        dst = torch.empty_like(src)
+        ts = []
+        for r in range(reps + 1):
+            flush()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(tstream)
+            with torch.cuda.stream(tstream):
+                dst.copy_(src)
+            e1.record(tstream)
+            e1.synchronize()
+            if r:
+                ts.append(e0.elapsed_time(e1))
+        return statistics.median(ts)
+
+    for name, bps in (("copy_same_bytes_as_k_pre", BYTES_PRE.get(M, 0)), ("copy_same_bytes_as_k_wiener",
+                                                                           BYTES_WIENER.get(M, 0))):
+        out[name] = entry(copy_cold(bps * S), bps, S)
     nb = 8
     # the single-utterance launch in steady state: 8 contexts, each holding its own
     # copy of the utterance (0.5 GB in all, > L2), launched back to back after one
@@ -471,7 +494,9 @@ def stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, 
     out["note"] = ("k_pre / k_wiener: one launch alone after an L2 flush (launch latency included); *_steady: "
                    "the same single-utterance launch, 8 back to back on distinct copies after one flush (cold "
                    "data, latency overlapped); *_batch8: one launch over 8 utterances; algorithmic bytes (K1: "
-                   "read x, write sigma_bx, tau_ax, tau_xx; K4: read sigma_bx, tau_ax, r_h, r_u, write dry + image)")
+                   "read x, write sigma_bx, tau_ax, tau_xx; K4: read sigma_bx, tau_ax, r_h, r_u, write dry + image); "
+                   "copy_same_bytes_as_*: torch's device copy moving the same bytes, timed the same way (the "
+                   "bandwidth a plain stream reaches at this size)")
     return out
 
 

@@ -431,11 +431,13 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   AccelCfg g = choose_accel_cfg(J);
   if (!g.cl) return false;
   if (accel_fusable(g, M) && opt->iters > 0) g.prem = M;  // one kernel per chunk: precompute fused into K2
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < 4; ++k)
     if (!c->aux[k]) CK(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
-  for (int k = 0; k < kMaxChunks + 3; ++k)
+  for (int k = 0; k < kMaxChunks + 6; ++k)
     if (!c->evx[k]) CK(cudaEventCreateWithFlags(&c->evx[k], cudaEventDisableTiming));
-  cudaStream_t cp = c->aux[0], cs = c->aux[1];
+  // H2D alternates between two copy streams (two DMA engines run concurrently;
+  // one alone reaches about half of the PCIe rate); K2 runs on cs per chunk
+  cudaStream_t cpy[2] = {c->aux[0], c->aux[2]}, cs = c->aux[1];
   alloc_problem(c, I, J, M);
   const size_t S = static_cast<size_t>(I * J);
   double* t1 = c->tmp.get<double>(S);
@@ -443,26 +445,41 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   reset_err(c);
   CK(cudaEventRecord(c->ev0, c->stream));
   CK(cudaEventRecord(c->evx[0], c->stream));
-  CK(cudaStreamWaitEvent(cp, c->evx[0], 0));
-  CK(cudaStreamWaitEvent(cs, c->evx[0], 0));
-  auto up = [&](void* dst, const void* src, size_t bytes) {
-    if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cp));
+  for (cudaStream_t q : {cpy[0], cpy[1], cs}) CK(cudaStreamWaitEvent(q, c->evx[0], 0));
+  auto up = [&](int e, void* dst, const void* src, size_t bytes) {
+    if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cpy[e]));
   };
-  up(t1, p0->r_h, S * sizeof(double));
-  up(t2, p0->r_u, S * sizeof(double));
-  up(c->lam.p, p0->lambda, I * sizeof(double));
-  up(c->a.p, in->a, I * M * sizeof(double2));
-  up(c->b.p, in->b, I * M * sizeof(double2));
-  up(c->Rpp.p, in->R_prime_pinv, I * M * M * sizeof(double2));
-  CK(cudaEventRecord(c->evx[1], cp));
+  // r_h0 / r_u0 (I x J col-major: every chunk needs all of both) first, one per engine
+  up(0, t1, p0->r_h, S * sizeof(double));
+  up(1, t2, p0->r_u, S * sizeof(double));
+  up(0, c->lam.p, p0->lambda, I * sizeof(double));
+  up(0, c->a.p, in->a, I * M * sizeof(double2));
+  up(1, c->b.p, in->b, I * M * sizeof(double2));
+  up(1, c->Rpp.p, in->R_prime_pinv, I * M * M * sizeof(double2));
+  CK(cudaEventRecord(c->evx[1], cpy[0]));
+  CK(cudaEventRecord(c->evx[kMaxChunks + 3], cpy[1]));
   for (int ch = 0; ch < nch; ++ch) {
     const int64_t i0 = I * ch / nch, i1 = I * (ch + 1) / nch;
-    up(c->X.as<double2>() + i0 * J * M, X + 2 * i0 * J * M, (i1 - i0) * J * M * sizeof(double2));
-    CK(cudaEventRecord(c->evx[3 + ch], cp));
+    up(ch & 1, c->X.as<double2>() + i0 * J * M, X + 2 * i0 * J * M, (i1 - i0) * J * M * sizeof(double2));
+    CK(cudaEventRecord(c->evx[3 + ch], cpy[ch & 1]));
   }
   const DevProblem full = problem(c, 1, I, J, M);
   const AccelArgs afull = accel_args(c, I, J, M, opt->iters, *hyper, opt->eps_var, opt->gamma_fault);
   CK(cudaStreamWaitEvent(cs, c->evx[1], 0));
+  CK(cudaStreamWaitEvent(cs, c->evx[kMaxChunks + 3], 0));
+  // output segments (RCSCM_D2H_SEGS; default one per chunk, measured fastest on
+  // config 1: 1.41 -> 1.25 ms per call): groups of consecutive chunks
+  const char* e_sg = std::getenv("RCSCM_D2H_SEGS");
+  const int nseg = std::max(1, std::min(nch, e_sg ? std::atoi(e_sg) : nch));
+  auto seg_of = [&](int ch) { return ch * nseg / nch; };
+  auto seg_first = [&](int sg) {  // first chunk of segment sg
+    int ch = 0;
+    while (seg_of(ch) < sg) ++ch;
+    return ch;
+  };
+  cudaStream_t cd = c->aux[3];
+  CK(cudaStreamWaitEvent(cd, c->evx[0], 0));
+  int64_t d_done = 0;  // bins already sent back
   for (int ch = 0; ch < nch; ++ch) {
     const int64_t i0 = I * ch / nch, i1 = I * (ch + 1) / nch, Ic = i1 - i0;
     if (Ic == 0) continue;
@@ -501,12 +518,33 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
     if (opt->iters > 0) c->launched(launch_accel(cs, A, g));
     c->launched(launch_to_ij(cs, c->rh.as<double>() + off, t1 + i0, 1, Ic, J, I));
     c->launched(launch_to_ij(cs, c->ru.as<double>() + off, t2 + i0, 1, Ic, J, I));
+    // the output is I x J col-major, so a bin range is a strided row block: all
+    // but the last segment go out as 2D copies on their own stream while the
+    // remaining chunks upload and compute (PCIe is full duplex)
+    const int sg = seg_of(ch);
+    if (nseg > 1 && sg < nseg - 1 && seg_of(ch + 1) != sg) {
+      const int64_t s0 = I * seg_first(sg) / nch;
+      CK(cudaEventRecord(c->evx[kMaxChunks + 4], cs));
+      CK(cudaStreamWaitEvent(cd, c->evx[kMaxChunks + 4], 0));
+      for (auto pr : {std::make_pair(out->r_h, t1), std::make_pair(out->r_u, t2)})
+        CK(cudaMemcpy2DAsync(pr.first + s0, I * sizeof(double), pr.second + s0, I * sizeof(double),
+                             (i1 - s0) * sizeof(double), J, cudaMemcpyDeviceToHost, cd));
+      d_done = i1;
+    }
   }
-  CK(cudaMemcpyAsync(out->r_h, t1, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
-  CK(cudaMemcpyAsync(out->r_u, t2, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  if (d_done == 0) {
+    CK(cudaMemcpyAsync(out->r_h, t1, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
+    CK(cudaMemcpyAsync(out->r_u, t2, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
+  } else {
+    for (auto pr : {std::make_pair(out->r_h, t1), std::make_pair(out->r_u, t2)})
+      CK(cudaMemcpy2DAsync(pr.first + d_done, I * sizeof(double), pr.second + d_done, I * sizeof(double),
+                           (I - d_done) * sizeof(double), J, cudaMemcpyDeviceToHost, cs));
+  }
   CK(cudaMemcpyAsync(out->lambda, c->lam.p, I * sizeof(double), cudaMemcpyDeviceToHost, cs));
   CK(cudaEventRecord(c->evx[2], cs));
   CK(cudaStreamWaitEvent(c->stream, c->evx[2], 0));
+  CK(cudaEventRecord(c->evx[kMaxChunks + 5], cd));
+  CK(cudaStreamWaitEvent(c->stream, c->evx[kMaxChunks + 5], 0));
   CK(cudaEventRecord(c->ev1, c->stream));
   check_err(c, J);
   float ms = 0.f;
@@ -785,7 +823,7 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
   if (c->il_graph) cudaGraphExecDestroy(c->il_graph);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
-  for (int k = 0; k < 2; ++k)
+  for (int k = 0; k < 4; ++k)
     if (c->aux[k]) cudaStreamDestroy(c->aux[k]);
   for (cudaEvent_t e : c->evx)
     if (e) cudaEventDestroy(e);

@@ -105,8 +105,10 @@ struct rcscm_gpu_ctx {
   bool own_stream = false;
   int64_t launches = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaStream_t aux[2] = {nullptr, nullptr};  // copy / compute streams of the pipelined entry points
-  cudaEvent_t evx[19] = {};                       // kMaxChunks + 3
+  // two copy streams (one DMA engine each: a single H2D stream reaches half the
+  // PCIe rate on B200 hosts) and a compute stream for the pipelined entry points
+  cudaStream_t aux[4] = {nullptr, nullptr, nullptr, nullptr};  // + a D2H stream
+  cudaEvent_t evx[22] = {};  // kMaxChunks + 6
   // device buffers
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;

@@ -434,18 +434,19 @@ def test_fused_precompute_bitwise(O, gpu, monkeypatch, cfg, I, J):
 
 
 def test_pipelined_entry_point_bitwise(O, gpu, monkeypatch):
-    """The copy/compute-pipelined run_algorithm2 (bins in chunks on two
-    streams) equals the single-shot path bitwise."""
-    from paper_1908_01964_b200 import synth
-
+    """The copy/compute-pipelined run_algorithm2 (bins in chunks, uploads on
+    two copy streams, the output sent back in 2D row-block segments while later
+    chunks run) equals the single-shot path bitwise, for any segment count."""
     u, inp, p0 = _synthetic(O, 1, 300, 64)
     monkeypatch.setenv("RCSCM_PIPELINE_CHUNKS", "1")
     single = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=20)).params
-    monkeypatch.setenv("RCSCM_PIPELINE_CHUNKS", "5")
-    piped = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=20)).params
-    assert np.array_equal(single.r_h, piped.r_h)
-    assert np.array_equal(single.r_u, piped.r_u)
-    assert np.array_equal(single.lam, piped.lam)
+    for chunks, segs in (("5", "1"), ("5", "2"), ("5", "5"), ("7", "3")):
+        monkeypatch.setenv("RCSCM_PIPELINE_CHUNKS", chunks)
+        monkeypatch.setenv("RCSCM_D2H_SEGS", segs)
+        piped = gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=20)).params
+        assert np.array_equal(single.r_h, piped.r_h), (chunks, segs)
+        assert np.array_equal(single.r_u, piped.r_u), (chunks, segs)
+        assert np.array_equal(single.lam, piped.lam), (chunks, segs)
 
 
 # ---- complex64 (FP32) mode: relative-L2 <= 1e-4 on the output ----------------------

@@ -34,7 +34,7 @@ pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
 Xp = pin(u.X.view(np.float64)); ap = pin(inp.a.view(np.float64)); bp = pin(inp.b.view(np.float64))
 rpp = pin(np.ascontiguousarray(inp.R_prime_pinv.transpose(0, 2, 1)).view(np.float64))
 rh0 = pin(p0.r_h.T); ru0 = pin(p0.r_u.T); l0 = pin(p0.lam)
-rh = torch.empty(I * J, dtype=torch.float64).pin_memory(); ru = torch.empty_like(rh); lam = torch.empty(I, dtype=torch.float64).pin_memory()
+rh = torch.empty(I * J, dtype=torch.float64).pin_memory(); ru = torch.empty(I * J, dtype=torch.float64).pin_memory(); lam = torch.empty(I, dtype=torch.float64).pin_memory()
 dp = lambda t: ctypes.cast(t.data_ptr(), C._dp)
 ci = C.CInputs(I, J, M, 0, dp(ap), None, dp(rpp), dp(bp))
 cp = C.CParams(dp(rh0), dp(ru0), dp(l0)); co = C.CParams(dp(rh), dp(ru), dp(lam))

@@ -62,6 +62,17 @@ typedef struct {
   int device;    /* CUDA device ordinal */
   int precision; /* RCSCM_C128 (reference-exact) or RCSCM_C64 (FP32 mode) */
   void* stream;  /* cudaStream_t to launch on; NULL = context-owned stream */
+  /* Optional device list: with num_devices > 1 the solver entry
+   * points (run_naive / run_algorithm1 / run_algorithm2 without objective or
+   * trajectory) and extract_target / extract_noise shard contiguous, balanced
+   * bin ranges over devices[0..num_devices) -- one host thread and stream per
+   * device, inputs sliced straight from the caller's buffers, each range's
+   * results copied back into its own (strided, for I x J col-major arrays)
+   * slice of the caller's outputs. No collective: bins are independent, and
+   * results are bitwise equal to the single-device call. devices[0] replaces
+   * `device`; `stream` applies to devices[0] only. NULL / 0 / 1: one device. */
+  const int* devices;
+  int num_devices;
 } rcscm_gpu_config;
 
 /* model.hpp:16-25 RcscmInputs (host pointers, reference layout). */

@@ -112,11 +112,17 @@ struct ExtractionResult {  // wiener.hpp:11-14
   std::vector<cplx> dry;  // (i, t) at i + t*I
 };
 
-// One CUDA device + stream (rcscm_gpu_ctx). Not thread-safe; one per thread.
+// One CUDA device + stream (rcscm_gpu_ctx), or bins sharded over a device list
+// (one stream and host thread per device). Not thread-safe; one per thread.
 class Context {
  public:
   explicit Context(int device = 0, void* stream = nullptr) {
-    rcscm_gpu_config cfg{device, RCSCM_C128, stream};
+    rcscm_gpu_config cfg{device, RCSCM_C128, stream, nullptr, 0};
+    check(rcscm_gpu_create(&cfg, &ctx_));
+  }
+  explicit Context(const std::vector<int>& devices) {
+    rcscm_gpu_config cfg{devices.empty() ? 0 : devices[0], RCSCM_C128, nullptr, devices.data(),
+                         static_cast<int>(devices.size())};
     check(rcscm_gpu_create(&cfg, &ctx_));
   }
   ~Context() { rcscm_gpu_destroy(ctx_); }

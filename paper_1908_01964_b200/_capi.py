@@ -34,7 +34,8 @@ _i64 = ctypes.c_int64
 
 
 class GpuConfig(ctypes.Structure):
-    _fields_ = [("device", ctypes.c_int), ("precision", ctypes.c_int), ("stream", ctypes.c_void_p)]
+    _fields_ = [("device", ctypes.c_int), ("precision", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("devices", ctypes.POINTER(ctypes.c_int)), ("num_devices", ctypes.c_int)]
 
 
 class CInputs(ctypes.Structure):

@@ -166,12 +166,17 @@ def _c_params_in(p: RcscmParams, held: _Held) -> C.CParams:
 
 
 class GpuContext:
-    """One rcscm_gpu_ctx (one CUDA device, one stream)."""
+    """One rcscm_gpu_ctx: one CUDA device and stream, or (devices=[...]) bins
+    sharded over several devices, one stream and host thread each."""
 
-    def __init__(self, device: int = 0, precision: str = "c128", stream: Optional[int] = None):
+    def __init__(self, device: int = 0, precision: str = "c128", stream: Optional[int] = None,
+                 devices: Optional[List[int]] = None):
         lib = C.load()
-        cfg = C.GpuConfig(int(device), C.RCSCM_C128 if precision == "c128" else C.RCSCM_C64,
-                          ctypes.c_void_p(stream) if stream else None)
+        devs = (ctypes.c_int * len(devices))(*[int(d) for d in devices]) if devices else None
+        cfg = C.GpuConfig(int(devices[0]) if devices else int(device),
+                          C.RCSCM_C128 if precision == "c128" else C.RCSCM_C64,
+                          ctypes.c_void_p(stream) if stream else None, devs, len(devices) if devices else 0)
+        self._devs = devs  # keep the list alive for the call
         h = ctypes.c_void_p()
         _raise(lib.rcscm_gpu_create(ctypes.byref(cfg), ctypes.byref(h)))
         self._h = h

@@ -6,6 +6,8 @@
 // device's bin-major layout, the CUDA kernels, and the way back. There is no
 // CPU fallback: every numeric step runs in the kernels launched through
 // launch.h (setup_launch.cu, accel_launch.cu, naive_launch.cu, stream_launch.cu).
+#include <thread>
+
 #include "capi_internal.h"
 
 using namespace rcscm_capi;
@@ -24,6 +26,16 @@ void d2d(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes) {
   if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, c->stream));
 }
 void sync(rcscm_gpu_ctx* c) { CK(cudaStreamSynchronize(c->stream)); }
+void h2d_ij(rcscm_gpu_ctx* c, void* dst, const void* src, int64_t I, int64_t J, size_t esz) {
+  const int64_t ld = c->ldh > I ? c->ldh : I;
+  if (ld == I) return h2d(c, dst, src, static_cast<size_t>(I * J) * esz);
+  if (I * J) CK(cudaMemcpy2DAsync(dst, I * esz, src, ld * esz, I * esz, J, cudaMemcpyHostToDevice, c->stream));
+}
+void d2h_ij(rcscm_gpu_ctx* c, void* dst, const void* src, int64_t I, int64_t J, size_t esz) {
+  const int64_t ld = c->ldh > I ? c->ldh : I;
+  if (ld == I) return d2h(c, dst, src, static_cast<size_t>(I * J) * esz);
+  if (I * J && dst) CK(cudaMemcpy2DAsync(dst, ld * esz, src, I * esz, I * esz, J, cudaMemcpyDeviceToHost, c->stream));
+}
 
 void reset_err(rcscm_gpu_ctx* c) {
   unsigned long long* e = c->err.get<unsigned long long>(1);
@@ -83,6 +95,8 @@ void check_err(rcscm_gpu_ctx* c, int64_t J) {
   unsigned long long key = ~0ull;
   CK(cudaMemcpyAsync(&key, c->err.as<unsigned long long>(), sizeof(key), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
+  if (key != ~0ull && c->bin_offset && J > 0)  // a bin range of a sharded call: global slot
+    key = (((key >> 8) + static_cast<unsigned long long>(c->bin_offset * J)) << 8) | (key & 0xFFull);
   std::string msg;
   const int rc = decode_err(key, J, &msg);
   if (rc != RCSCM_OK) fail(rc, msg);
@@ -387,8 +401,8 @@ void upload_model(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* 
   if (p) {
     double* t1 = c->tmp.get<double>(S);
     double* t2 = c->tmp2.get<double>(S);
-    h2d(c, t1, p->r_h, S * sizeof(double));
-    h2d(c, t2, p->r_u, S * sizeof(double));
+    h2d_ij(c, t1, p->r_h, I, J, sizeof(double));
+    h2d_ij(c, t2, p->r_u, I, J, sizeof(double));
     c->launched(launch_to_bt(c->stream, t1, c->rh.as<double>(), 1, I, J));
     c->launched(launch_to_bt(c->stream, t2, c->ru.as<double>(), 1, I, J));
     h2d(c, c->lam.p, p->lambda, I * sizeof(double));
@@ -401,8 +415,8 @@ void download_params(rcscm_gpu_ctx* c, int64_t I, int64_t J, rcscm_params* out) 
   double* t2 = c->tmp2.get<double>(S);
   c->launched(launch_to_ij(c->stream, c->rh.as<double>(), t1, 1, I, J));
   c->launched(launch_to_ij(c->stream, c->ru.as<double>(), t2, 1, I, J));
-  d2h(c, out->r_h, t1, S * sizeof(double));
-  d2h(c, out->r_u, t2, S * sizeof(double));
+  d2h_ij(c, out->r_h, t1, I, J, sizeof(double));
+  d2h_ij(c, out->r_u, t2, I, J, sizeof(double));
   d2h(c, out->lambda, c->lam.p, I * sizeof(double));
 }
 
@@ -449,9 +463,15 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   auto up = [&](int e, void* dst, const void* src, size_t bytes) {
     if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, cpy[e]));
   };
+  const int64_t ldh = c->ldh > I ? c->ldh : I;  // host leading dimension of r_h / r_u
+  auto up_ij = [&](int e, double* dst, const double* src) {
+    if (ldh == I) return up(e, dst, src, S * sizeof(double));
+    CK(cudaMemcpy2DAsync(dst, I * sizeof(double), src, ldh * sizeof(double), I * sizeof(double), J,
+                         cudaMemcpyHostToDevice, cpy[e]));
+  };
   // r_h0 / r_u0 (I x J col-major: every chunk needs all of both) first, one per engine
-  up(0, t1, p0->r_h, S * sizeof(double));
-  up(1, t2, p0->r_u, S * sizeof(double));
+  up_ij(0, t1, p0->r_h);
+  up_ij(1, t2, p0->r_u);
   up(0, c->lam.p, p0->lambda, I * sizeof(double));
   up(0, c->a.p, in->a, I * M * sizeof(double2));
   up(1, c->b.p, in->b, I * M * sizeof(double2));
@@ -527,17 +547,17 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
       CK(cudaEventRecord(c->evx[kMaxChunks + 4], cs));
       CK(cudaStreamWaitEvent(cd, c->evx[kMaxChunks + 4], 0));
       for (auto pr : {std::make_pair(out->r_h, t1), std::make_pair(out->r_u, t2)})
-        CK(cudaMemcpy2DAsync(pr.first + s0, I * sizeof(double), pr.second + s0, I * sizeof(double),
+        CK(cudaMemcpy2DAsync(pr.first + s0, ldh * sizeof(double), pr.second + s0, I * sizeof(double),
                              (i1 - s0) * sizeof(double), J, cudaMemcpyDeviceToHost, cd));
       d_done = i1;
     }
   }
-  if (d_done == 0) {
+  if (d_done == 0 && ldh == I) {
     CK(cudaMemcpyAsync(out->r_h, t1, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
     CK(cudaMemcpyAsync(out->r_u, t2, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
   } else {
     for (auto pr : {std::make_pair(out->r_h, t1), std::make_pair(out->r_u, t2)})
-      CK(cudaMemcpy2DAsync(pr.first + d_done, I * sizeof(double), pr.second + d_done, I * sizeof(double),
+      CK(cudaMemcpy2DAsync(pr.first + d_done, ldh * sizeof(double), pr.second + d_done, I * sizeof(double),
                            (I - d_done) * sizeof(double), J, cudaMemcpyDeviceToHost, cs));
   }
   CK(cudaMemcpyAsync(out->lambda, c->lam.p, I * sizeof(double), cudaMemcpyDeviceToHost, cs));
@@ -734,7 +754,7 @@ void extract_impl(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* 
       c->launched(launch_f2d(c->stream, c->dryf.as<float>(), reinterpret_cast<double*>(dd), 2 * S));
       double2* t = c->tmp.get<double2>(S);
       c->launched(launch_to_ij_c(c->stream, dd, t, 1, I, J));
-      d2h(c, dry, t, S * sizeof(double2));
+      d2h_ij(c, dry, t, I, J, sizeof(double2));
     }
     if (image) {
       double2* im = c->image.get<double2>(S * M);
@@ -761,11 +781,107 @@ void extract_impl(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* 
   if (dry) {
     double2* t = c->tmp.get<double2>(S);
     c->launched(launch_to_ij_c(c->stream, Wa.dry, t, 1, I, J));
-    d2h(c, dry, t, S * sizeof(double2));
+    d2h_ij(c, dry, t, I, J, sizeof(double2));
   }
   if (image) d2h(c, image, Wa.image, S * M * sizeof(double2));
   if (noise) d2h(c, noise, Wa.noise, S * M * sizeof(double2));
   sync(c);
+}
+
+// ---- multi-device: contiguous bin ranges, one host thread per device ---------------
+// Runs body(ctx, d, lo, hi) for device d's balanced bin range [lo, hi) of I bins
+// on its own thread, with the context's ldh / bin_offset set for the range; the
+// first failing range (in device order) is rethrown on the caller's thread.
+template <class F>
+void run_sharded(rcscm_gpu_ctx* c, int64_t I, F&& body) {
+  std::vector<rcscm_gpu_ctx*> ctxs{c};
+  ctxs.insert(ctxs.end(), c->peers.begin(), c->peers.end());
+  const int64_t D = static_cast<int64_t>(ctxs.size());
+  std::vector<ApiError> errs(ctxs.size(), ApiError{RCSCM_OK, ""});
+  std::vector<std::thread> th;
+  for (int64_t d = 0; d < D; ++d) {
+    const int64_t lo = I * d / D, hi = I * (d + 1) / D;
+    if (hi == lo) continue;
+    th.emplace_back([&, d, lo, hi] {
+      rcscm_gpu_ctx* x = ctxs[d];
+      try {
+        CK(cudaSetDevice(x->device));
+        x->ldh = I;
+        x->bin_offset = lo;
+        struct Reset {
+          rcscm_gpu_ctx* x;
+          ~Reset() { x->ldh = x->bin_offset = 0; }
+        } reset{x};
+        body(x, d, lo, hi);
+      } catch (const ApiError& e) {
+        errs[d] = e;
+      } catch (const std::exception& e) {
+        errs[d] = ApiError{RCSCM_CUDA_ERROR, e.what()};
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  CK(cudaSetDevice(c->device));
+  for (const ApiError& e : errs)
+    if (e.code != RCSCM_OK) fail(e.code, e.msg);
+}
+
+// rcscm_inputs / X views of bins [lo, hi)
+rcscm_inputs slice_inputs(const rcscm_inputs* in, int64_t lo, int64_t hi) {
+  rcscm_inputs v = *in;
+  const int64_t M = in->mics;
+  v.num_bins = hi - lo;
+  v.a = in->a ? in->a + 2 * lo * M : nullptr;
+  v.b = in->b ? in->b + 2 * lo * M : nullptr;
+  v.R_prime = in->R_prime ? in->R_prime + 2 * lo * M * M : nullptr;
+  v.R_prime_pinv = in->R_prime_pinv ? in->R_prime_pinv + 2 * lo * M * M : nullptr;
+  return v;
+}
+
+void run_solver_sharded(rcscm_gpu_ctx* c, Backend backend, const rcscm_inputs* in, const rcscm_params* p0,
+                        const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt, rcscm_params* out,
+                        rcscm_result* extra) {
+  const char* who = backend == kNaive ? "run_naive" : "run_accelerated";
+  validate_opts(opt, who);
+  validate_inputs(in, backend != kAccel2, backend == kAccel2);
+  if (!p0 || !out || !hyper || !X) fail(RCSCM_INVALID_INPUT, std::string(who) + ": NULL argument");
+  if (opt->compute_objective || opt->record_trajectory)
+    fail(RCSCM_UNSUPPORTED, std::string(who) + ": compute_objective / record_trajectory run on one device");
+  const int64_t I = in->num_bins, J = in->frames, M = in->mics;
+  const int n = std::max(opt->iters, 0);
+  std::vector<std::vector<double>> secs(1 + c->peers.size(), std::vector<double>(n, 0.0));
+  run_sharded(c, I, [&](rcscm_gpu_ctx* x, int64_t d, int64_t lo, int64_t hi) {
+    const rcscm_inputs v = slice_inputs(in, lo, hi);
+    const rcscm_params pin{p0->r_h + lo, p0->r_u + lo, p0->lambda + lo};
+    rcscm_params pout{out->r_h + lo, out->r_u + lo, out->lambda + lo};
+    int nit = 0;
+    rcscm_result r{nullptr, nullptr, secs[d].data(), &nit, nullptr, nullptr, nullptr};
+    run_solver(x, backend, &v, &pin, hyper, X + 2 * lo * J * M, opt, &pout, &r);
+  });
+  if (extra) {
+    if (extra->n_objective) *extra->n_objective = 0;
+    if (extra->iter_seconds)  // the devices run concurrently: the slowest one's time
+      for (int k = 0; k < n; ++k) {
+        double m = 0.0;
+        for (const auto& v : secs) m = std::max(m, v[k]);
+        extra->iter_seconds[k] = m;
+      }
+    if (extra->n_iters) *extra->n_iters = n;
+  }
+}
+
+void extract_sharded(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p, const double* X, double* image,
+                     double* dry, double* noise) {
+  if (!p || !X) fail(RCSCM_INVALID_INPUT, "extract: NULL argument");
+  validate_inputs(in, false, true);
+  const int64_t I = in->num_bins, J = in->frames, M = in->mics;
+  run_sharded(c, I, [&](rcscm_gpu_ctx* x, int64_t, int64_t lo, int64_t hi) {
+    const rcscm_inputs v = slice_inputs(in, lo, hi);
+    const rcscm_params pv{p->r_h + lo, p->r_u + lo, p->lambda + lo};
+    const size_t o = static_cast<size_t>(2 * lo * J * M);
+    extract_impl(x, &v, &pv, X + o, image ? image + o : nullptr, dry ? dry + 2 * lo : nullptr,
+                 noise ? noise + o : nullptr);
+  });
 }
 
 }  // namespace rcscm_capi
@@ -777,38 +893,62 @@ extern "C" {
 
 const char* rcscm_gpu_last_error(void) { return g_last_error.c_str(); }
 
-int rcscm_gpu_create(const rcscm_gpu_config* cfg, rcscm_gpu_ctx** out) {
-  return guarded([&] {
-    if (!out) fail(RCSCM_INVALID_INPUT, "out must not be NULL");
-    *out = nullptr;
-    rcscm_gpu_config d{0, RCSCM_C128, nullptr};
-    if (cfg) d = *cfg;
-    if (d.precision != RCSCM_C128 && d.precision != RCSCM_C64) fail(RCSCM_INVALID_INPUT, "precision must be RCSCM_C128 or RCSCM_C64");
-    int n = 0;
-    CK(cudaGetDeviceCount(&n));
-    if (d.device < 0 || d.device >= n) fail(RCSCM_INVALID_INPUT, "device ordinal out of range");
-    CK(cudaSetDevice(d.device));
-    cudaDeviceProp prop;
-    CK(cudaGetDeviceProperties(&prop, d.device));
-    if (prop.major != 10)
-      fail(RCSCM_UNSUPPORTED, std::string("this build targets sm_100a (B200); device is ") + prop.name);
-    auto* c = new rcscm_gpu_ctx();
-    c->device = d.device;
-    c->precision = d.precision;
-    if (d.stream) {
-      c->stream = static_cast<cudaStream_t>(d.stream);
+// One context on `device` (stream: the caller's, or a context-owned one).
+static rcscm_gpu_ctx* make_ctx(int device, int precision, void* stream) {
+  int n = 0;
+  CK(cudaGetDeviceCount(&n));
+  if (device < 0 || device >= n) fail(RCSCM_INVALID_INPUT, "device ordinal out of range");
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    fail(RCSCM_UNSUPPORTED, std::string("this build targets sm_100a (B200); device is ") + prop.name);
+  auto* c = new rcscm_gpu_ctx();
+  c->device = device;
+  c->precision = precision;
+  try {
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
     } else {
       CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
       c->own_stream = true;
     }
     CK(cudaEventCreate(&c->ev0));
     CK(cudaEventCreate(&c->ev1));
+  } catch (...) {
+    rcscm_gpu_destroy(c);
+    throw;
+  }
+  return c;
+}
+
+int rcscm_gpu_create(const rcscm_gpu_config* cfg, rcscm_gpu_ctx** out) {
+  return guarded([&] {
+    if (!out) fail(RCSCM_INVALID_INPUT, "out must not be NULL");
+    *out = nullptr;
+    rcscm_gpu_config d{0, RCSCM_C128, nullptr, nullptr, 0};
+    if (cfg) d = *cfg;
+    if (d.precision != RCSCM_C128 && d.precision != RCSCM_C64) fail(RCSCM_INVALID_INPUT, "precision must be RCSCM_C128 or RCSCM_C64");
+    if (d.num_devices < 0 || (d.num_devices > 1 && !d.devices))
+      fail(RCSCM_INVALID_INPUT, "create: devices must list num_devices ordinals");
+    const int nd = d.num_devices > 1 ? d.num_devices : 1;
+    const int dev0 = (d.num_devices >= 1 && d.devices) ? d.devices[0] : d.device;
+    rcscm_gpu_ctx* c = make_ctx(dev0, d.precision, d.stream);
+    try {
+      for (int k = 1; k < nd; ++k) c->peers.push_back(make_ctx(d.devices[k], d.precision, nullptr));
+    } catch (...) {
+      rcscm_gpu_destroy(c);
+      throw;
+    }
+    CK(cudaSetDevice(dev0));
     *out = c;
   });
 }
 
 void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
   if (!c) return;
+  for (rcscm_gpu_ctx* p : c->peers) rcscm_gpu_destroy(p);
+  c->peers.clear();
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (DBuf* b : {&c->X, &c->W, &c->A, &c->T, &c->V, &c->a, &c->b, &c->Rp, &c->Rpp, &c->power, &c->sab, &c->taa,
@@ -831,7 +971,12 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
   delete c;
 }
 
-int64_t rcscm_gpu_launch_count(const rcscm_gpu_ctx* c) { return c ? c->launches : 0; }
+int64_t rcscm_gpu_launch_count(const rcscm_gpu_ctx* c) {
+  if (!c) return 0;
+  int64_t n = c->launches;
+  for (const rcscm_gpu_ctx* p : c->peers) n += p->launches;
+  return n;
+}
 
 void* rcscm_gpu_stream(rcscm_gpu_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
 
@@ -914,6 +1059,7 @@ int rcscm_gpu_run_naive(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_pa
                         rcscm_result* extra) {
   return guarded([&] {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
+    if (!c->peers.empty()) return run_solver_sharded(c, kNaive, in, params0, hyper, X, opt, out, extra);
     run_solver(c, kNaive, in, params0, hyper, X, opt, out, extra);
   });
 }
@@ -923,6 +1069,7 @@ int rcscm_gpu_run_algorithm2(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcs
                              rcscm_params* out, rcscm_result* extra) {
   return guarded([&] {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
+    if (!c->peers.empty()) return run_solver_sharded(c, kAccel2, in, params0, hyper, X, opt, out, extra);
     run_solver(c, kAccel2, in, params0, hyper, X, opt, out, extra);
   });
 }
@@ -932,19 +1079,24 @@ int rcscm_gpu_run_algorithm1(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcs
                              rcscm_params* out, rcscm_result* extra) {
   return guarded([&] {
     if (!c) fail(RCSCM_INVALID_INPUT, "ctx must not be NULL");
+    if (!c->peers.empty()) return run_solver_sharded(c, kAccel1, in, params0, hyper, X, opt, out, extra);
     run_solver(c, kAccel1, in, params0, hyper, X, opt, out, extra);
   });
 }
 
 int rcscm_gpu_extract_target(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p, const double* X,
                              double* image, double* dry) {
-  return guarded([&] { extract_impl(c, in, p, X, image, dry, nullptr); });
+  return guarded([&] {
+    if (c && !c->peers.empty()) return extract_sharded(c, in, p, X, image, dry, nullptr);
+    extract_impl(c, in, p, X, image, dry, nullptr);
+  });
 }
 
 int rcscm_gpu_extract_noise(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p, const double* X,
                             double* noise) {
   return guarded([&] {
     if (!noise) fail(RCSCM_INVALID_INPUT, "extract_noise: noise must not be NULL");
+    if (c && !c->peers.empty()) return extract_sharded(c, in, p, X, nullptr, nullptr, noise);
     extract_impl(c, in, p, X, nullptr, nullptr, noise);
   });
 }

@@ -138,6 +138,12 @@ struct rcscm_gpu_ctx {
   bool s_reset_pending = false;
   int64_t sB = 0, sI = 0, sJ = 0;
   int sM = 0, sK = 0, sn_h = 0;
+  // multi-device: the contexts of devices[1..] (this one is devices[0]); while a
+  // context serves one bin range of a sharded call, ldh is the caller's I (the
+  // leading dimension of its I x J col-major host arrays) and bin_offset the
+  // range's first bin (error messages report global bins)
+  std::vector<rcscm_gpu_ctx*> peers;
+  int64_t ldh = 0, bin_offset = 0;
 
   // Every kernel launch goes through here: the error is surfaced as
   // RCSCM_CUDA_ERROR and the launch counter (rcscm_gpu_launch_count) advances.
@@ -168,6 +174,10 @@ int guarded(F&& f) {
 void h2d(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes);
 void d2h(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes);
 void d2d(rcscm_gpu_ctx* c, void* dst, const void* src, size_t bytes);
+// I x J col-major host array (leading dimension c->ldh when serving a bin range
+// of a wider array) <-> contiguous I x J device array, element size esz
+void h2d_ij(rcscm_gpu_ctx* c, void* dst, const void* src, int64_t I, int64_t J, size_t esz);
+void d2h_ij(rcscm_gpu_ctx* c, void* dst, const void* src, int64_t I, int64_t J, size_t esz);
 void sync(rcscm_gpu_ctx* c);
 void reset_err(rcscm_gpu_ctx* c);
 void check_err(rcscm_gpu_ctx* c, int64_t J);

@@ -68,7 +68,30 @@ int main() {
     ref += w.samples[k] * w.samples[k];
   }
   const bool ok5 = S.bins == 513 && S.frames == 33 && r.num_samples == w.num_samples && std::sqrt(err / ref) < 1e-8;
-  std::printf("shim_check: naive r_h %.17g (want %.17g) accel==naive %d wiener %d throws %d alg1 %d stft %d\n",
-              naive.params.r_h[0], want, ok2, ok3, threw, ok4, ok5);
-  return (ok1 && ok2 && ok3 && threw && ok4 && ok5) ? 0 : 1;
+  // a device list (here device 0 twice): bins sharded over two contexts, the
+  // result bitwise equal to one device -- 3 bins of the scalar case
+  Context multi(std::vector<int>{0, 0});
+  RcscmInputs in3 = in;
+  in3.bins = 3;
+  in3.a.assign(3, cplx(1.0, 0.0));
+  in3.b.assign(3, cplx(1.0, 0.0));
+  in3.R_prime.assign(3, cplx(0.0, 0.0));
+  in3.R_prime_pinv.assign(3, cplx(0.0, 0.0));
+  RcscmParams q0 = p0;
+  q0.bins = 3;
+  q0.r_h = {1.0, 2.0, 0.5};
+  q0.r_u = {1.0, 0.7, 1.5};
+  q0.lambda = {2.0, 1.0, 3.0};
+  Spectrogram X3 = X;
+  X3.bins = 3;
+  X3.data = {cplx(3.0, 0.0), cplx(1.0, -2.0), cplx(0.5, 0.25)};
+  opt.iters = 4;
+  const SolverResult one = run_algorithm2(ctx, in3, q0, Hyperparams{}, X3, opt);
+  const SolverResult two = run_algorithm2(multi, in3, q0, Hyperparams{}, X3, opt);
+  const bool ok6 = one.params.r_h == two.params.r_h && one.params.r_u == two.params.r_u &&
+                   one.params.lambda == two.params.lambda;
+  std::printf("shim_check: naive r_h %.17g (want %.17g) accel==naive %d wiener %d throws %d alg1 %d stft %d "
+              "devices %d\n",
+              naive.params.r_h[0], want, ok2, ok3, threw, ok4, ok5, ok6);
+  return (ok1 && ok2 && ok3 && threw && ok4 && ok5 && ok6) ? 0 : 1;
 }

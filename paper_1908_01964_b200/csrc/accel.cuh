@@ -16,7 +16,7 @@
 // the way out. With PREM = M the sigma / tau forms are computed from x in the
 // prologue (the precompute fused into the kernel). The only cross-slot
 // dependency -- lambda's sum over frames -- is a fixed-order tree: in-thread
-// pairwise sum, a warp total (one DMMA + a 3-level xor butterfly), a
+// pairwise sum, a warp total (one DMMA + a 2-level xor butterfly), a
 // zero-padded 4/8-way block tree (+ a DSMEM exchange across the cluster), so
 // results are deterministic and independent of how the bins are sharded.
 //
@@ -108,26 +108,29 @@ __device__ __forceinline__ double floor_eps(double v, double eps) {
 }
 
 // Sum of the 32 lanes' values, returned in every lane: one DMMA m8n8k4 with
-// B = 1 leaves in lane l the sum of its 4-lane group (fixed internal order;
-// multiplications by 1 are exact), then a 3-level xor butterfly over the 8
-// group sums. Every lane ends with the same bits: each butterfly level adds
-// the same two operands in both partner lanes and IEEE addition commutes.
-// Measured on B200 at 3 CTAs/SM (tools/k2_probe.cu): 4 % faster per launch
-// than the all-DMMA tree (DMMA, shuffle transpose, two DMMAs), whose three
-// tensor-pipe ops per warp-iteration contend under load, and than a 5-level
-// shuffle butterfly (longer latency).
-__device__ __forceinline__ double dmma_ones(double a) {
-  double d0;
-  [[maybe_unused]] double d1;
+// A = 1 and the values as B (lane l holds B[l % 4][l / 4]) leaves in lane l
+// the sums of the 4-lane groups 2(l % 4) and 2(l % 4) + 1 (D columns; fixed
+// internal order, multiplications by 1 exact); their sum and a 2-level xor
+// butterfly finish it. Every lane ends with the same bits -- each level adds
+// the same two operands in both partner lanes and IEEE addition commutes --
+// and the tree ((G0+G1)+(G2+G3))+((G4+G5)+(G6+G7)) over the group sums G is the
+// one of the earlier A = values form (DMMA + 3-level butterfly), so results are
+// bitwise unchanged with one shuffle level (two SHFL + one DADD of latency per
+// iteration) fewer on the lambda chain: config 1 0.174 -> 0.170 ms, a lone bin
+// 43 -> 41 us (B200). A second A = 1 DMMA in place of the butterfly (lane l
+// holds the pair sum P_{l % 4}, so every D element is P0 + P1 + P2 + P3) cuts
+// the lone bin to 39 us but is no faster at 3 CTAs/SM and 1 % slower on config
+// 3: tensor-pipe ops of co-resident warps contend under load, as with the
+// earlier all-DMMA tree (DMMA, shuffle transpose, two DMMAs); a 5-level
+// shuffle butterfly is slower through latency.
+__device__ __forceinline__ double warp_total(double v) {
+  double d0, d1;
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};"
       : "=d"(d0), "=d"(d1)
-      : "d"(a), "d"(1.0), "d"(0.0), "d"(0.0));
-  return d0;
-}
-__device__ __forceinline__ double warp_total(double v) {
-  double s = dmma_ones(v);  // lane l: sum of lanes 4*(l/4) .. +3
-#pragma unroll
-  for (int m = 4; m < 32; m <<= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+      : "d"(1.0), "d"(v), "d"(0.0), "d"(0.0));
+  double s = d0 + d1;  // G(2j) + G(2j+1), j = lane % 4
+  s += __shfl_xor_sync(0xffffffffu, s, 1);
+  s += __shfl_xor_sync(0xffffffffu, s, 2);
   return s;
 }
 

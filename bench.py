@@ -59,9 +59,13 @@ class ClockSampler:
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device):
+    def __init__(self, device, lead_in=None):
         self.device = device
         self.proc = None
+        # lead_in(seconds): keeps the GPU under load while nvidia-smi starts (an
+        # idle lead-in lets the clocks drop: measured on B200, the first K2 steps
+        # after 0.3 s of idle run up to 15 % slow and take ~6 steps to recover)
+        self.lead_in = lead_in
 
     def __enter__(self):
         try:
@@ -70,7 +74,10 @@ class ClockSampler:
                  "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except (OSError, FileNotFoundError):
             self.proc = None
-        time.sleep(0.3)
+        if self.lead_in is not None:
+            self.lead_in(0.3)
+        else:
+            time.sleep(0.3)
         return self
 
     def __exit__(self, *exc):
@@ -277,11 +284,19 @@ def run_gpu(args):
     ctx.session_check()
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    launches0 = ctx.launch_count
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize(dev)
-    with ClockSampler(local) as clk:
+    def lead_in(seconds):  # untimed steps while the clock sampler starts
+        t_end = time.perf_counter() + seconds
+        while time.perf_counter() < t_end:
+            for _ in range(20):
+                flush()
+                ctx.session_run(step_stages, iters, hyper)
+            torch.cuda.synchronize(dev)
+
+    with ClockSampler(local, lead_in) as clk:
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        launches0 = ctx.launch_count
         for k in range(args.steps):
             flush()  # L2 flush between steps (outside the events)
             e0, e1 = ev[k]
@@ -382,6 +397,8 @@ def run_gpu(args):
                        "step": "run_algorithm2 on resident inputs: params0, sigma/tau precompute fused into the "
                                "prologue of K2, 100 on-chip iterations (one kernel)",
                        "l2": "flushed between steps (256 MiB write, outside the timed events)",
+                       "clock_lead_in": "0.3 s of untimed steps while nvidia-smi starts, so the timed steps "
+                                        "do not start from an idle GPU",
                        "parallelism": f"bins sharded by utterance, {world} GPU(s), no collective in the loop"},
             "gpu_launches": launches,
             "breakdown_ms": {"fused_k2": k2_avg},

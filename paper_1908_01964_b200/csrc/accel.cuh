@@ -63,6 +63,10 @@ struct AccelArgs {
   double* lambda;           // [bin]    out
   const double* r_h_in;     // [bin][t] initial iterate (may alias r_h)
   const double* r_u_in;
+  // ld_p > 0: r_h / r_u (in and out, complex128) are the reference's I x J
+  // column-major arrays instead -- slot (bin, t) at bin + t * ld_p -- so a
+  // chunk of bins reads and writes the caller's layout without transposes
+  int64_t ld_p;
   const double* lambda_in;  // [bin]
   double* traj_r_h;         // optional [it][bin][t]
   double* traj_r_u;
@@ -221,6 +225,8 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
   const int64_t t0 = rank * Jc;
   const int64_t t_end = min(J, t0 + Jc);
   const int64_t base = bin * J;
+  const int64_t ldp = P.ld_p;
+  auto pslot = [&](int64_t t) { return ldp ? bin + t * ldp : base + t; };  // r_h / r_u index
   const double inv_M = P.inv_M;
   // shared planes ([k][tid], conflict-free): tax, (txx, dd) packed, and for
   // SMEMC 1 also cc
@@ -323,8 +329,9 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       tk = P.tau_ax_f[s];
       xk = P.tau_xx_f[s] * invMT;
     } else if constexpr (PREM > 0) {
-      rh[k] = P.r_h_in[s];
-      ru[k] = P.r_u_in[s];
+      const int64_t sp = pslot(valid[k] ? t : t0);
+      rh[k] = P.r_h_in[sp];
+      ru[k] = P.r_u_in[sp];
       double2 xv[PREM];
 #pragma unroll
       for (int m = 0; m < PREM; ++m) {
@@ -339,8 +346,9 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       }
       xk = txx * invMT;
     } else {
-      rh[k] = P.r_h_in[s];
-      ru[k] = P.r_u_in[s];
+      const int64_t sp = pslot(valid[k] ? t : t0);
+      rh[k] = P.r_h_in[sp];
+      ru[k] = P.r_u_in[sp];
       sb = P.sigma_bx[s];
       tk = P.tau_ax[s];
       xk = P.tau_xx[s] * invMT;
@@ -590,8 +598,8 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
         P.r_h_f[base + t] = rh[k];
         P.r_u_f[base + t] = ru[k];
       } else {
-        P.r_h[base + t] = rh[k];
-        P.r_u[base + t] = ru[k];
+        P.r_h[pslot(t)] = rh[k];
+        P.r_u[pslot(t)] = ru[k];
       }
     }
   }

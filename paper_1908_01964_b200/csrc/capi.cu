@@ -428,11 +428,13 @@ void validate_opts(const rcscm_solver_opts* opt, const char* who) {
 // Copy/compute-overlapped run_algorithm2 (no objective, no trajectory). A copy
 // stream uploads the small per-bin inputs and the whole r_h / r_u / lambda
 // (contiguous), then x chunk by chunk of bins; the compute stream waits for each
-// x chunk and runs transpose -> sigma/tau -> K2 -> transpose back on that chunk
-// while the next chunk is still in flight; one device->host copy of the results
-// follows. Chunks own disjoint slices of the bin-major device buffers and the
-// per-bin arithmetic is unchanged, so the result is bitwise identical to the
-// single-shot path. Returns false when the problem is too small to split.
+// x chunk and runs K2 with the sigma / tau precompute fused and r_h / r_u read
+// and written in place in the caller's I x J column-major layout (other K2
+// variants: transpose -> sigma/tau -> K2 -> transpose back) on that chunk while
+// the next chunk is still in flight; each chunk's results go back as 2D row
+// blocks on a D2H stream. Chunks own disjoint bin ranges of every buffer and
+// the per-bin arithmetic is unchanged, so the result is bitwise identical to
+// the single-shot path. Returns false when the problem is too small to split.
 bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p0,
                          const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt,
                          rcscm_params* out, std::vector<double>* secs) {
@@ -500,13 +502,25 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   cudaStream_t cd = c->aux[3];
   CK(cudaStreamWaitEvent(cd, c->evx[0], 0));
   int64_t d_done = 0;  // bins already sent back
+  auto send_rows = [&](cudaStream_t q, int64_t b0, int64_t b1) {  // bins [b0, b1) of r_h / r_u to the caller
+    if (b1 <= b0) return;
+    for (auto pr : {std::make_pair(out->r_h, t1), std::make_pair(out->r_u, t2)})
+      CK(cudaMemcpy2DAsync(pr.first + b0, ldh * sizeof(double), pr.second + b0, I * sizeof(double),
+                           (b1 - b0) * sizeof(double), J, cudaMemcpyDeviceToHost, q));
+  };
   for (int ch = 0; ch < nch; ++ch) {
     const int64_t i0 = I * ch / nch, i1 = I * (ch + 1) / nch, Ic = i1 - i0;
     if (Ic == 0) continue;
     const size_t off = static_cast<size_t>(i0 * J);
     CK(cudaStreamWaitEvent(cs, c->evx[3 + ch], 0));
-    c->launched(launch_to_bt(cs, t1 + i0, c->rh.as<double>() + off, 1, Ic, J, I));
-    c->launched(launch_to_bt(cs, t2 + i0, c->ru.as<double>() + off, 1, Ic, J, I));
+    // the fused K2 reads and writes r_h / r_u in the caller's I x J column-major
+    // layout (ld_p = I) in place in t1 / t2; other variants go through the
+    // bin-major arrays with transposes around them
+    const bool colmajor = g.prem != 0;
+    if (!colmajor) {
+      c->launched(launch_to_bt(cs, t1 + i0, c->rh.as<double>() + off, 1, Ic, J, I));
+      c->launched(launch_to_bt(cs, t2 + i0, c->ru.as<double>() + off, 1, Ic, J, I));
+    }
     DevProblem P = full;
     P.nb = Ic;
     P.I = Ic;
@@ -529,15 +543,25 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
     A.sigma_bx += off;
     A.tau_ax += off;
     A.tau_xx += off;
-    A.r_h += off;
-    A.r_u += off;
     A.lambda += i0;
-    A.r_h_in += off;
-    A.r_u_in += off;
     A.lambda_in += i0;
+    if (colmajor) {
+      A.r_h = t1 + i0;
+      A.r_u = t2 + i0;
+      A.r_h_in = A.r_h;
+      A.r_u_in = A.r_u;
+      A.ld_p = I;
+    } else {
+      A.r_h += off;
+      A.r_u += off;
+      A.r_h_in += off;
+      A.r_u_in += off;
+    }
     if (opt->iters > 0) c->launched(launch_accel(cs, A, g));
-    c->launched(launch_to_ij(cs, c->rh.as<double>() + off, t1 + i0, 1, Ic, J, I));
-    c->launched(launch_to_ij(cs, c->ru.as<double>() + off, t2 + i0, 1, Ic, J, I));
+    if (!colmajor) {
+      c->launched(launch_to_ij(cs, c->rh.as<double>() + off, t1 + i0, 1, Ic, J, I));
+      c->launched(launch_to_ij(cs, c->ru.as<double>() + off, t2 + i0, 1, Ic, J, I));
+    }
     // the output is I x J col-major, so a bin range is a strided row block: all
     // but the last segment go out as 2D copies on their own stream while the
     // remaining chunks upload and compute (PCIe is full duplex)
@@ -546,9 +570,7 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
       const int64_t s0 = I * seg_first(sg) / nch;
       CK(cudaEventRecord(c->evx[kMaxChunks + 4], cs));
       CK(cudaStreamWaitEvent(cd, c->evx[kMaxChunks + 4], 0));
-      for (auto pr : {std::make_pair(out->r_h, t1), std::make_pair(out->r_u, t2)})
-        CK(cudaMemcpy2DAsync(pr.first + s0, ldh * sizeof(double), pr.second + s0, I * sizeof(double),
-                             (i1 - s0) * sizeof(double), J, cudaMemcpyDeviceToHost, cd));
+      send_rows(cd, s0, i1);
       d_done = i1;
     }
   }
@@ -556,9 +578,7 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
     CK(cudaMemcpyAsync(out->r_h, t1, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
     CK(cudaMemcpyAsync(out->r_u, t2, S * sizeof(double), cudaMemcpyDeviceToHost, cs));
   } else {
-    for (auto pr : {std::make_pair(out->r_h, t1), std::make_pair(out->r_u, t2)})
-      CK(cudaMemcpy2DAsync(pr.first + d_done, ldh * sizeof(double), pr.second + d_done, I * sizeof(double),
-                           (I - d_done) * sizeof(double), J, cudaMemcpyDeviceToHost, cs));
+    send_rows(cs, d_done, I);
   }
   CK(cudaMemcpyAsync(out->lambda, c->lam.p, I * sizeof(double), cudaMemcpyDeviceToHost, cs));
   CK(cudaEventRecord(c->evx[2], cs));

@@ -42,10 +42,13 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
         best_waste = waste;
         // FULL needs every CTA of the cluster to own exactly nt * spt frames
         const bool full = (waste == 0) && (jc * cl == J);
-        // shared-memory constants where the cluster needs several CTAs per SM
-        // to hide its exchange (CL >= 4); 2-CTA clusters keep everything in
-        // registers (measured on B200: J = 4096 19 % faster, J = 20000 the reverse)
-        const int smem = smem_env >= 0 ? smem_env : (cl >= 4 ? 1 : 0);
+        // shared-memory constants for every cluster: the register file then
+        // holds two CTAs per SM, whose per-iteration cluster exchanges overlap
+        // (measured on B200, config 4, J = 4096 as 2 x 256 x 8: 2.98 ms against
+        // 3.34 ms with the constants in registers at one CTA per SM; 4 x 128 x 8
+        // 3.01, 8 x 64 x 8 3.56; config 2, J = 20000 as 16 x 256 x 5: 2.99 ms
+        // against 5.37)
+        const int smem = smem_env >= 0 ? smem_env : (cl >= 2 ? 1 : 0);
         const int minb = minb_env >= 0 ? minb_env : (smem == 0 ? 3 : 4);
         best = AccelCfg{cl, static_cast<int>(nt), spt, full, f32 ? 0 : smem, minb, direct, f32};
       }

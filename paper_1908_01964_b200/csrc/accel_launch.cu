@@ -29,6 +29,10 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
     // runs 33 % faster as 2 CTAs x 8 slots/thread than as 4 x 4)
     const int max_spt = (cl >= 2 || f32) ? 8 : 6;
     if (jc > 256LL * (force_spt ? force_spt : max_spt)) continue;
+    // complex64 clusters (constants always in registers): CTAs of <= 128 threads,
+    // so two CTAs of different clusters share an SM (measured on B200, config 4
+    // c64: 4 x 128 x 8 2.18 ms against 2 x 256 x 8 2.35 ms)
+    if (f32 && !force_cl && cl >= 2 && cl < 16 && jc > 128LL * max_spt) continue;
     int64_t best_waste = -1;
     for (int spt = 1; spt <= 8; ++spt) {
       if (spt == 7) continue;  // not instantiated
@@ -50,7 +54,11 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
         // against 5.37)
         const int smem = smem_env >= 0 ? smem_env : (cl >= 2 ? 1 : 0);
         const int minb = minb_env >= 0 ? minb_env : (smem == 0 ? 3 : 4);
-        best = AccelCfg{cl, static_cast<int>(nt), spt, full, f32 ? 0 : smem, minb, direct, f32};
+        // complex64: shared-memory constants only for clusters of 8+ (instantiated
+        // there; measured on B200, config 2 c64 as 16 x 160 x 8: 2.17 ms against
+        // 4.40 ms with the constants in registers)
+        const int smem_t = f32 ? (cl >= 8 ? (smem_env >= 0 ? smem_env : 1) : 0) : smem;
+        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem_t, minb, direct, f32};
       }
     }
     if (best.cl) return best;

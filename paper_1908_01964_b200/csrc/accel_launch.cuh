@@ -56,9 +56,15 @@ cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt
 template <int CL>
 cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
   const bool traj = A.traj_r_h != nullptr || A.obj_part != nullptr;  // per-iteration recording
-  if (g.f32) {  // complex64 mode: direct form, registers only
+  if (g.f32) {  // complex64 mode: direct form; shared-memory constants for large clusters
     if constexpr (CL == 1) {
       if (g.full && g.minb && g.nt <= 128) return launch_accel_spt<CL, true, false, 0, 3, true, float>(s, A, g.nt, g.spt);
+    }
+    if constexpr (CL >= 8) {
+      if (g.smem) {
+        if (g.full) return launch_accel_spt<CL, true, false, 1, 0, true, float>(s, A, g.nt, g.spt);
+        return launch_accel_spt<CL, false, false, 1, 0, true, float>(s, A, g.nt, g.spt);
+      }
     }
     if (g.full) return launch_accel_spt<CL, true, false, 0, 0, true, float>(s, A, g.nt, g.spt);
     return launch_accel_spt<CL, false, false, 0, 0, true, float>(s, A, g.nt, g.spt);

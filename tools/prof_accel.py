@@ -26,7 +26,7 @@ ctx.session_load(X, W, A, T, V, 0)
 ctx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
 h = Hyperparams()
 ev = []
-for r in range(a.reps):
+for r in range(a.reps + 5):  # the first 5 are warm-up (clocks ramp after an idle GPU)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE, 0, h)
     e0.record(s)
@@ -42,7 +42,7 @@ for r in range(a.reps):
     ev.append((e0, e1))
 torch.cuda.synchronize()
 ctx.session_check()
-ms = min(e0.elapsed_time(e1) for e0, e1 in ev)
+ms = min(e0.elapsed_time(e1) for e0, e1 in ev[5:])
 B, I, J, M = X.shape
 it = 1 if a.wiener else (c["naive_iters"] if a.naive else c["iters"])
 print(f"{'c64' if a.c64 else 'c128'} cfg{a.cfg} B={B} I={I} J={J} {'wiener' if a.wiener else ('naive' if a.naive else 'accel')} spt={os.environ.get('RCSCM_ACCEL_SPT','auto')} "

@@ -374,12 +374,12 @@ def run_gpu(args):
     c64 = c64_measure(local, tstream, X, W, A, T, V, iters, hyper, S, args, torch, C)
 
     # e2e through the C ABI with pinned host buffers (reference layout)
-    e2e = e2e_measure(ctx, u, iters, hyper, args, torch)
+    e2e = e2e_measure(ctx, u, iters, hyper, args, torch, world, dev)
 
     out = None
     if rank == 0:
         clocks = clk.summary()
-        cpu = cpu_baseline(u, c) if world == 1 or rank == 0 else None
+        cpu = cpu_baseline(u, c) if world == 1 else None  # rank 0 at N = 1 only
         out = {
             "metric": "TF-slot updates/s (I*J*iters/s), accelerated rule (Algorithm 2)",
             "value": value,
@@ -551,8 +551,11 @@ def c64_measure(local, tstream, X, W, A, T, V, iters, hyper, S, args, torch, C):
             "note": "same step with x, sigma/tau and the slot arithmetic in single precision; lambda in double"}
 
 
-def e2e_measure(ctx, u, iters, hyper, args, torch):
-    """rcscm_gpu_run_algorithm2 with pinned host inputs/outputs (reference layout)."""
+def e2e_measure(ctx, u, iters, hyper, args, torch, world=1, dev=None):
+    """rcscm_gpu_run_algorithm2 with pinned host inputs/outputs (reference layout).
+    With N ranks each rank runs its own utterance; the whole-job value is
+    N x I*J*iters over the slowest rank's mean call time, and the byte counts are
+    summed over ranks."""
     import paper_1908_01964_b200._capi as C
 
     lib = C.load()
@@ -591,6 +594,10 @@ def e2e_measure(ctx, u, iters, hyper, args, torch):
     # ramp; measured on B200, tools/e2e_bench_check.py)
     for _ in range(max(args.warmup, 10)):
         call()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
     ts = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
@@ -599,11 +606,18 @@ def e2e_measure(ctx, u, iters, hyper, args, torch):
     if os.environ.get("RCSCM_E2E_VERBOSE"):
         print("e2e per call (ms):", " ".join(f"{t * 1e3:.3f}" for t in ts), file=sys.stderr)
     dt = sum(ts) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
     h2d = (Xp.numel() + ap.numel() + bp.numel() + rpp.numel() + rh0.numel() + ru0.numel() + l0.numel()) * 8
     d2h = (rh.numel() + ru.numel() + lam.numel()) * 8
-    return {"value": I * J * iters / dt, "unit": "TF-slot updates/s", "h2d_bytes_per_step": h2d,
-            "d2h_bytes_per_step": d2h, "ms_per_step": dt * 1e3,
-            "path": "rcscm_gpu_run_algorithm2 (C ABI, synchronous) with pinned host buffers, host wall clock"}
+    return {"value": world * I * J * iters / dt, "unit": "TF-slot updates/s", "h2d_bytes_per_step": world * h2d,
+            "d2h_bytes_per_step": world * d2h, "ms_per_step": dt * 1e3,
+            "path": "rcscm_gpu_run_algorithm2 (C ABI, synchronous) with pinned host buffers, host wall clock"
+                    + (f"; {world} ranks, one utterance each, slowest rank's time" if world > 1 else "")}
 
 
 def main():

@@ -529,3 +529,22 @@ def test_session_reset_replays(O, gpu, gpu64, prec):
         o = O.run("naive", inp, o0, u.X, O.SolverOptions(iters=2)).params
         assert np.allclose(nv["lam"][1], o.lam, rtol=1e-8, atol=0)
     g.session_check()
+
+
+@pytest.mark.parametrize("cfg,I,J,cl", [(4, 6, 4096, "2"), (4, 6, 4096, "4"), (2, 2, 20000, "16")])
+def test_cluster_constant_placement_bitwise(O, gpu, monkeypatch, cfg, I, J, cl):
+    """A cluster shape gives the same bits whether the per-slot constants live in
+    registers or in shared memory (the default for clusters): placement changes
+    residency, not arithmetic. Both agree with the oracle's lambda within 1e-9."""
+    u, inp, p0 = _synthetic(O, cfg, I, J)
+    monkeypatch.setenv("RCSCM_ACCEL_CL", cl)
+    runs = []
+    for smem in ("0", "1"):
+        monkeypatch.setenv("RCSCM_ACCEL_SMEM", smem)
+        runs.append(gpu.run_algorithm2(inp, p0, _hyper(), u.X, _opts(iters=10)).params)
+    assert np.array_equal(runs[0].r_h, runs[1].r_h)
+    assert np.array_equal(runs[0].r_u, runs[1].r_u)
+    assert np.array_equal(runs[0].lam, runs[1].lam)
+    o = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=10)).params
+    rel = np.abs(runs[1].lam - o.lam) / np.maximum(np.maximum(np.abs(runs[1].lam), np.abs(o.lam)), 1e-12)
+    assert rel.max() <= 1e-9, rel.max()

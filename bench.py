@@ -252,10 +252,10 @@ def run_gpu(args):
     import paper_1908_01964_b200._capi as C
 
     rank, world, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
     c = workload_config()
     u = synth.make_config(CFG, utterances=1, seed_base=1000 * CFG + rank)[0]
     X, W, A, T, V = synth.stack([u])

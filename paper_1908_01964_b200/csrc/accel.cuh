@@ -243,15 +243,27 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
   // (whose dependent loads and barrier then overlap it) when it fits registers
   constexpr bool XPRE = PREM > 0 && SPT * PREM <= 20;
   double2 xpre[XPRE ? SPT : 1][XPRE ? PREM : 1];
+  // ... and so are its initial r_h / r_u, the bin's a and lambda: no global load
+  // waits behind the prologue's barrier (a barrier orders every later load)
+  double rhpre[XPRE ? SPT : 1], rupre[XPRE ? SPT : 1];
+  double2 apre[PM];
   if constexpr (XPRE) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
       const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
-      const int64_t s = base + ((FULL || t < t_end) ? t : t0);
+      const int64_t tt = (FULL || t < t_end) ? t : t0;
+      const int64_t s = base + tt;
 #pragma unroll
       for (int m = 0; m < PREM; ++m) xpre[k][m] = __ldg(P.X + s * PREM + m);
+      rhpre[k] = __ldg(P.r_h_in + pslot(tt));
+      rupre[k] = __ldg(P.r_u_in + pslot(tt));
     }
   }
+  if constexpr (PREM > 0) {
+#pragma unroll
+    for (int k = 0; k < PREM; ++k) apre[k] = __ldg(P.a_in + bin * PREM + k);
+  }
+  double lam = P.lambda_in[bin];
   if constexpr (PREM > 0) {
     // per-bin prologue of K1 (k_pre): R'^+, b and R'^+ a in shared memory;
     // sigma_ab = a^H b and tau_aa = max(Re a^H R'^+ a, 0) in every thread
@@ -259,13 +271,15 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
     if (tid < PREM) {
       pb[tid] = P.b_in[bin * PREM + tid];
       double2 s = make_double2(0.0, 0.0);
-      for (int k = 0; k < PREM; ++k) s = cfma(P.Rpp_in[bin * PREM * PREM + tid + k * PREM], P.a_in[bin * PREM + k], s);
+#pragma unroll
+      for (int k = 0; k < PREM; ++k) s = cfma(P.Rpp_in[bin * PREM * PREM + tid + k * PREM], apre[k], s);
       pp[tid] = s;
     }
     __syncthreads();
     double2 ab = make_double2(0.0, 0.0), aa = make_double2(0.0, 0.0);
+#pragma unroll
     for (int k = 0; k < PREM; ++k) {
-      const double2 ak = P.a_in[bin * PREM + k];
+      const double2 ak = apre[k];
       ab = cfmac(ak, pb[k], ab);
       aa = cfmac(ak, pp[k], aa);
     }
@@ -280,7 +294,6 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
     taa = P.tau_aa[bin];
   }
   const double s2 = cnorm(sab);  // |sigma_ab|^2
-  double lam = P.lambda_in[bin];
   double il = 1.0 / lam;
   double raa = fma(s2, il, taa);  // rho_aa (solver_accel.hpp:122)
   // Scaled residual: with the per-slot constant c = s_ab s_bx / |s_ab|^2 (s_bx
@@ -329,9 +342,14 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       tk = P.tau_ax_f[s];
       xk = P.tau_xx_f[s] * invMT;
     } else if constexpr (PREM > 0) {
-      const int64_t sp = pslot(valid[k] ? t : t0);
-      rh[k] = P.r_h_in[sp];
-      ru[k] = P.r_u_in[sp];
+      if constexpr (XPRE) {
+        rh[k] = rhpre[k];
+        ru[k] = rupre[k];
+      } else {
+        const int64_t sp = pslot(valid[k] ? t : t0);
+        rh[k] = P.r_h_in[sp];
+        ru[k] = P.r_u_in[sp];
+      }
       double2 xv[PREM];
 #pragma unroll
       for (int m = 0; m < PREM; ++m) {

@@ -69,13 +69,14 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
 bool accel_fusable(const AccelCfg& g, int M) {
   const char* e = std::getenv("RCSCM_FUSE_PRE");
   if (e && std::atoi(e) == 0) return false;
-  return (M == 2 || M == 4 || M == 8) && g.cl == 1 && g.full && !g.f32 && g.smem == 0 && g.minb == 3 && g.direct &&
-         g.nt <= 128;
+  if (!(M == 2 || M == 4 || M == 8) || g.f32 || !g.direct) return false;
+  // the tuned single-CTA shape, or a cluster with its constants in shared memory
+  return (g.cl == 1 && g.full && g.smem == 0 && g.minb == 3 && g.nt <= 128) || (g.cl >= 2 && g.smem == 1);
 }
 
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
   if (A.nb * A.J == 0) return cudaSuccess;
-  if (g.prem) return launch_accel_fused(s, A, g);
+  if (g.prem && g.cl == 1) return launch_accel_fused(s, A, g);
   switch (g.cl) {
     case 1: return launch_accel_cl1(s, A, g);
     case 2: return launch_accel_cl2(s, A, g);

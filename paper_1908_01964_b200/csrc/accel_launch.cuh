@@ -53,8 +53,26 @@ cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt
   }
 }
 
+// Clusters with the sigma / tau precompute fused into the prologue (PREM = M),
+// constants in shared memory, direct form.
+template <int CL, int PREM>
+cudaError_t launch_accel_fused_cl_m(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
+  if (g.full) return launch_accel_spt<CL, true, false, 1, 0, true, double, PREM>(s, A, g.nt, g.spt);
+  return launch_accel_spt<CL, false, false, 1, 0, true, double, PREM>(s, A, g.nt, g.spt);
+}
+
 template <int CL>
 cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
+  if constexpr (CL >= 2) {
+    if (g.prem) {
+      switch (g.prem) {
+        case 2: return launch_accel_fused_cl_m<CL, 2>(s, A, g);
+        case 4: return launch_accel_fused_cl_m<CL, 4>(s, A, g);
+        case 8: return launch_accel_fused_cl_m<CL, 8>(s, A, g);
+        default: return cudaErrorInvalidValue;
+      }
+    }
+  }
   const bool traj = A.traj_r_h != nullptr || A.obj_part != nullptr;  // per-iteration recording
   if (g.f32) {  // complex64 mode: direct form; shared-memory constants for large clusters
     if constexpr (CL == 1) {

@@ -407,11 +407,11 @@ def test_session_pipeline_matches_entry_points(O, gpu):
         assert output_rel_err(out["image"][k], oimg) <= 1e-6
 
 
-@pytest.mark.parametrize("cfg,I,J", [(0, 24, 320), (1, 16, 640), (4, 6, 640)])
+@pytest.mark.parametrize("cfg,I,J", [(0, 24, 320), (1, 16, 640), (4, 6, 640), (4, 4, 4096), (2, 2, 20000)])
 def test_fused_precompute_bitwise(O, gpu, monkeypatch, cfg, I, J):
     """K2 with the sigma / tau precompute fused into its prologue (one kernel for
     PRECOMPUTE | ACCEL) equals K1 + K2 bitwise, including the forms it keeps for
-    the Wiener stage; M = 2, 4, 8."""
+    the Wiener stage; M = 2, 4, 8, single-CTA bins and clusters (J = 4096, 20000)."""
     from paper_1908_01964_b200 import synth
     import paper_1908_01964_b200._capi as C
 

@@ -465,6 +465,20 @@ def test_pipelined_entry_point_bitwise(O, gpu, monkeypatch):
         assert np.array_equal(single.lam, piped.lam), (chunks, segs)
 
 
+def test_pipelined_cluster_bitwise(O, gpu, monkeypatch):
+    """The pipelined run_algorithm2 on a cluster shape (J = 4096, M = 8: 2-CTA
+    clusters with the fused precompute reading and writing r_h / r_u in the
+    caller's column-major layout) equals the single-shot path bitwise."""
+    inp, p0, X = O.make_verify_instance(256, 4096, 8, 77)
+    monkeypatch.setenv("RCSCM_PIPELINE_CHUNKS", "1")
+    single = gpu.run_algorithm2(inp, p0, _hyper(), X, _opts(iters=8)).params
+    monkeypatch.setenv("RCSCM_PIPELINE_CHUNKS", "3")
+    piped = gpu.run_algorithm2(inp, p0, _hyper(), X, _opts(iters=8)).params
+    assert np.array_equal(single.r_h, piped.r_h)
+    assert np.array_equal(single.r_u, piped.r_u)
+    assert np.array_equal(single.lam, piped.lam)
+
+
 # ---- complex64 (FP32) mode: relative-L2 <= 1e-4 on the output ----------------------
 def _rel_l2(got, ref):
     got = np.asarray(got)

@@ -92,9 +92,12 @@ int decode_err(unsigned long long key, int64_t J, std::string* msg) {
 }
 
 void check_err(rcscm_gpu_ctx* c, int64_t J) {
-  unsigned long long key = ~0ull;
-  CK(cudaMemcpyAsync(&key, c->err.as<unsigned long long>(), sizeof(key), cudaMemcpyDeviceToHost, c->stream));
+  // into a page-locked word: a direct DMA instead of the driver's pageable staging
+  unsigned long long* hk = c->err_pin.get<unsigned long long>(1);
+  *hk = ~0ull;
+  CK(cudaMemcpyAsync(hk, c->err.as<unsigned long long>(), sizeof(*hk), cudaMemcpyDeviceToHost, c->stream));
   sync(c);
+  unsigned long long key = *hk;
   if (key != ~0ull && c->bin_offset && J > 0)  // a bin range of a sharded call: global slot
     key = (((key >> 8) + static_cast<unsigned long long>(c->bin_offset * J)) << 8) | (key & 0xFFull);
   std::string msg;
@@ -980,6 +983,7 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
                   &c->ex_Q, &c->ex_W, &c->ex_A, &c->ex_pow, &c->ex_out, &c->ex_obj})
     b->release();
   c->ex_pin.release();
+  c->err_pin.release();
   if (c->il_graph) cudaGraphExecDestroy(c->il_graph);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);

@@ -122,6 +122,7 @@ struct rcscm_gpu_ctx {
   // objective trace
   DBuf ex_Q, ex_W, ex_A, ex_pow, ex_out, ex_obj;
   HBuf ex_pin;  // pinned staging of the waveforms in and out
+  HBuf err_pin;  // pinned landing word of the device error word (check_err)
   StftPlan stft_plan;
   // ILRMA sweeps replayed as one CUDA graph, re-captured when the shape, the
   // buffers or the sweep count change (key: IlrmaArgs fields, M, iters)

@@ -6,6 +6,8 @@
 // device's bin-major layout, the CUDA kernels, and the way back. There is no
 // CPU fallback: every numeric step runs in the kernels launched through
 // launch.h (setup_launch.cu, accel_launch.cu, naive_launch.cu, stream_launch.cu).
+#include <chrono>
+#include <cstdio>
 #include <thread>
 
 #include "capi_internal.h"
@@ -461,6 +463,7 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   const size_t S = static_cast<size_t>(I * J);
   double* t1 = c->tmp.get<double>(S);
   double* t2 = c->tmp2.get<double>(S);
+  const auto th0 = std::chrono::steady_clock::now();  // RCSCM_DEBUG_TIMING: host enqueue time
   reset_err(c);
   CK(cudaEventRecord(c->ev0, c->stream));
   CK(cudaEventRecord(c->evx[0], c->stream));
@@ -589,9 +592,14 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   CK(cudaEventRecord(c->evx[kMaxChunks + 5], cd));
   CK(cudaStreamWaitEvent(c->stream, c->evx[kMaxChunks + 5], 0));
   CK(cudaEventRecord(c->ev1, c->stream));
+  const auto th1 = std::chrono::steady_clock::now();
   check_err(c, J);
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+  if (std::getenv("RCSCM_DEBUG_TIMING"))
+    std::fprintf(stderr, "run_accel_pipelined: host enqueue %.1f us, device %.1f us, total %.1f us\n",
+                 std::chrono::duration<double, std::micro>(th1 - th0).count(), ms * 1e3,
+                 std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - th0).count());
   // end-to-end per iteration (copies overlapped with compute)
   secs->assign(opt->iters, opt->iters ? (ms * 1e-3) / opt->iters : 0.0);
   return true;

@@ -10,6 +10,8 @@
  *   rcscm_gpu_run_naive         replaces  run_naive             solver_naive.hpp:412-450
  *   rcscm_gpu_run_algorithm1    replaces  run_algorithm1        solver_accel.hpp:245-250
  *   rcscm_gpu_run_algorithm2    replaces  run_algorithm2        solver_accel.hpp:254-258
+ *   rcscm_gpu_run_accel         stage 1 / 2 -> run_algorithm1 / 2 (one accelerated symbol)
+ *   rcscm_gpu_build_inputs      build_noise_scm + init_params     model.hpp:58-124
  *   rcscm_gpu_extract_target    replaces  extract_target        wiener.hpp:19-43
  *   rcscm_gpu_extract_noise     replaces  extract_noise         wiener.hpp:46-53
  *   rcscm_gpu_stft_analyze      replaces  stft_analyze          stft.hpp:50-88
@@ -165,6 +167,20 @@ int rcscm_gpu_run_algorithm2(rcscm_gpu_ctx* ctx, const rcscm_inputs* in,
                              const rcscm_params* params0, const rcscm_hyper* hyper,
                              const double* X, const rcscm_solver_opts* opt,
                              rcscm_params* out, rcscm_result* extra);
+/* solver_accel.hpp:246-258 by stage: 1 = run_algorithm1, 2 = run_algorithm2 (the
+ * accelerated entry as one symbol; any other stage is RCSCM_INVALID_INPUT). */
+int rcscm_gpu_run_accel(rcscm_gpu_ctx* ctx, int stage, const rcscm_inputs* in,
+                        const rcscm_params* params0, const rcscm_hyper* hyper,
+                        const double* X, const rcscm_solver_opts* opt,
+                        rcscm_params* out, rcscm_result* extra);
+/* model.hpp:58-124 in one call: build_noise_scm (a, R', R'^+, b into the caller's
+ * buffers, as rcscm_gpu_build_noise_scm) then init_params (params0 into out, T, V =
+ * NmfModel::T[n_h], V[n_h], K = rank); the same results as the two calls. */
+int rcscm_gpu_build_inputs(rcscm_gpu_ctx* ctx, int64_t I, int64_t J, int M,
+                           const double* X, const double* W, const double* A,
+                           int n_h, double rank_tol, int K, const double* T,
+                           const double* V, double* a, double* R_prime,
+                           double* R_prime_pinv, double* b, rcscm_params* out);
 /* wiener.hpp:19-43 (image [i][t][m] and/or dry I x J col-major; either may be NULL) */
 int rcscm_gpu_extract_target(rcscm_gpu_ctx* ctx, const rcscm_inputs* in,
                              const rcscm_params* p, const double* X, double* image,

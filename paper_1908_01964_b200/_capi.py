@@ -149,6 +149,12 @@ SIGNATURES = {
     "rcscm_gpu_run_algorithm2": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams),
                                                 ctypes.POINTER(CHyper), _dp, ctypes.POINTER(COpts),
                                                 ctypes.POINTER(CParams), ctypes.POINTER(CResult)]),
+    "rcscm_gpu_run_accel": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.POINTER(CInputs), ctypes.POINTER(CParams),
+                                           ctypes.POINTER(CHyper), _dp, ctypes.POINTER(COpts),
+                                           ctypes.POINTER(CParams), ctypes.POINTER(CResult)]),
+    "rcscm_gpu_build_inputs": (ctypes.c_int, [_vp, _i64, _i64, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int,
+                                              ctypes.c_double, ctypes.c_int, _dp, _dp, _dp, _dp, _dp, _dp,
+                                              ctypes.POINTER(CParams)]),
     "rcscm_gpu_extract_target": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams), _dp, _dp,
                                                 _dp]),
     "rcscm_gpu_extract_noise": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.POINTER(CParams), _dp, _dp]),

@@ -289,6 +289,32 @@ class GpuContext:
     def run_algorithm2(self, inputs, params0, hyper, X, opt=None) -> SolverResult:
         return self._run(self._lib.rcscm_gpu_run_algorithm2, inputs, params0, hyper, X, opt)
 
+    def run_accel(self, stage: int, inputs, params0, hyper, X, opt=None) -> SolverResult:
+        """rcscm_gpu_run_accel: stage 1 / 2 = run_algorithm1 / run_algorithm2."""
+        lib, st = self._lib, int(stage)
+        return self._run(lambda h, *rest: lib.rcscm_gpu_run_accel(h, st, *rest), inputs, params0, hyper, X, opt)
+
+    def build_inputs(self, W, A, X, n_h: int, T, V, rank_tol: float = 1e-10):
+        """rcscm_gpu_build_inputs: build_noise_scm then init_params in one call
+        (model.hpp:58-124); returns (RcscmInputs, RcscmParams)."""
+        X = _cz(X)
+        I, J, M = X.shape
+        T = np.asarray(T, np.float64)
+        V = np.asarray(V, np.float64)
+        a = np.zeros((I, M), np.complex128)
+        b = np.zeros((I, M), np.complex128)
+        rp = np.zeros((I, M, M), np.complex128)
+        rpp = np.zeros((I, M, M), np.complex128)
+        rh = np.zeros(I * J)
+        ru = np.zeros(I * J)
+        lam = np.zeros(I)
+        out = C.CParams(_p(rh), _p(ru), _p(lam))
+        _raise(self._lib.rcscm_gpu_build_inputs(self._h, I, J, M, _p(X), _p(_mats(W)), _p(_mats(A)), int(n_h),
+                                                float(rank_tol), T.shape[1], _p(_ij(T)), _p(_ij(V)), _p(a), _p(rp),
+                                                _p(rpp), _p(b), ctypes.byref(out)))
+        inputs = RcscmInputs(a, rp.transpose(0, 2, 1).copy(), rpp.transpose(0, 2, 1).copy(), b, int(n_h))
+        return inputs, RcscmParams(_from_ij(rh, I, J), _from_ij(ru, I, J), lam)
+
     def extract_target(self, inputs: RcscmInputs, p: RcscmParams, X) -> ExtractionResult:
         X = _cz(X)
         I, J, M = X.shape

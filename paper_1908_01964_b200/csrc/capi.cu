@@ -1116,6 +1116,23 @@ int rcscm_gpu_run_algorithm1(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcs
   });
 }
 
+int rcscm_gpu_run_accel(rcscm_gpu_ctx* c, int stage, const rcscm_inputs* in, const rcscm_params* params0,
+                        const rcscm_hyper* hyper, const double* X, const rcscm_solver_opts* opt, rcscm_params* out,
+                        rcscm_result* extra) {
+  if (stage == 1) return rcscm_gpu_run_algorithm1(c, in, params0, hyper, X, opt, out, extra);
+  if (stage == 2) return rcscm_gpu_run_algorithm2(c, in, params0, hyper, X, opt, out, extra);
+  return guarded([&] { fail(RCSCM_INVALID_INPUT, "run_accel: stage must be 1 or 2, got " + std::to_string(stage)); });
+}
+
+int rcscm_gpu_build_inputs(rcscm_gpu_ctx* c, int64_t I, int64_t J, int M, const double* X, const double* W,
+                           const double* A, int n_h, double rank_tol, int K, const double* T, const double* V,
+                           double* a, double* R_prime, double* R_prime_pinv, double* b, rcscm_params* out) {
+  const int rc = rcscm_gpu_build_noise_scm(c, I, J, M, X, W, A, n_h, rank_tol, a, R_prime, R_prime_pinv, b);
+  if (rc != RCSCM_OK) return rc;
+  const rcscm_inputs in{I, J, M, n_h, a, R_prime, R_prime_pinv, b};
+  return rcscm_gpu_init_params(c, &in, K, X, W, A, T, V, out);
+}
+
 int rcscm_gpu_extract_target(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_params* p, const double* X,
                              double* image, double* dry) {
   return guarded([&] {

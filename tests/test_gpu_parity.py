@@ -578,3 +578,26 @@ def test_cluster_constant_placement_bitwise(O, gpu, monkeypatch, cfg, I, J, cl):
     o = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=10)).params
     rel = np.abs(runs[1].lam - o.lam) / np.maximum(np.maximum(np.abs(runs[1].lam), np.abs(o.lam)), 1e-12)
     assert rel.max() <= 1e-9, rel.max()
+
+
+def test_build_inputs_and_run_accel_entry_points(O, gpu):
+    """rcscm_gpu_build_inputs == build_noise_scm + init_params and
+    rcscm_gpu_run_accel(stage) == run_algorithm1 / run_algorithm2, bitwise; a stage
+    other than 1 or 2 is InvalidInputError."""
+    from paper_1908_01964_b200 import synth
+    from paper_1908_01964_b200.api import InvalidInputError
+
+    u = synth.make_config(1, utterances=1, I=12, J=64)[0]
+    inp, p0 = gpu.build_inputs(u.W, u.A, u.X, 0, u.T, u.V)
+    ref_inp = gpu.build_noise_scm(u.W, u.A, u.X, 0)
+    ref_p0 = gpu.init_params(ref_inp, u.T, u.V, u.W, u.A, u.X)
+    for k in ("a", "R_prime", "R_prime_pinv", "b"):
+        assert np.array_equal(getattr(inp, k), getattr(ref_inp, k)), k
+    for k in ("r_h", "r_u", "lam"):
+        assert np.array_equal(getattr(p0, k), getattr(ref_p0, k)), k
+    for stage, fn in ((1, gpu.run_algorithm1), (2, gpu.run_algorithm2)):
+        a = gpu.run_accel(stage, inp, p0, _hyper(), u.X, _opts(iters=7)).params
+        b = fn(inp, p0, _hyper(), u.X, _opts(iters=7)).params
+        assert np.array_equal(a.r_h, b.r_h) and np.array_equal(a.r_u, b.r_u) and np.array_equal(a.lam, b.lam)
+    with pytest.raises(InvalidInputError, match="stage must be 1 or 2"):
+        gpu.run_accel(3, inp, p0, _hyper(), u.X, _opts(iters=1))

@@ -1,22 +1,31 @@
 #!/usr/bin/env python
 """Benchmark of the rcscm hot path on B200 (one JSON line on rank 0).
 
-Workload (BASELINE.json configs[1], the single-GPU config the metric is quoted
-on): one utterance, M = 4 mics, I = 1025 bins, J = 640 frames, 100 iterations of
-the accelerated rule (Algorithm 2, solver_accel.hpp:254), complex128. Synthetic
-inputs from the BASELINE recipe (paper_1908_01964_b200/synth.py), seed
-1000 * 1 + rank, generated once on the host.
+Headline workload: BASELINE.json configs[3], the largest configuration that fits
+one GPU -- 256 independent utterances, each M = 4 mics, I = 513 bins, J = 320
+frames (42.0 M time-frequency slots, x = 2.69 GB complex128), 100 iterations of
+the accelerated rule (Algorithm 2, solver_accel.hpp:254). Synthetic inputs from
+the BASELINE recipe (paper_1908_01964_b200/synth.py), utterance u drawn with
+seed 3000 + u, generated once on the host; both arms use the same seeds and
+print the same `config` dict.
 
-A step = run_algorithm2 on the device with its inputs resident in HBM: one
-fused K2 launch (restore params0, the sigma/tau precompute in its prologue,
-100 on-chip iterations). K1 and K4 are timed alone (cold L2) as extras.
-value  = B * I * J * iters * n_gpus / (max-over-ranks device time per step).
+A step = run_algorithm2 over the whole batch with its inputs resident in HBM:
+one fused K2 launch (restore params0, the sigma/tau precompute in its prologue,
+100 on-chip iterations per bin).
+value  = 256 * I * J * iters / (max-over-ranks device time per step).
+With N GPUs (torchrun) the 256 utterances are split into contiguous balanced
+ranges, one per rank (strong scaling: total work fixed; no collective in the
+solve, the timing MAX is the only NCCL traffic).
 e2e    = the same metric through the C ABI entry point rcscm_gpu_run_algorithm2
-         with pinned host buffers in the reference layout (H2D of X, inputs and
-         params0, D2H of r_h, r_u, lambda inside the timed region).
-naive  = the naive rule (solver_naive.hpp:412) on the same resident inputs.
---impl reference runs the oracle port (the reference's CPU algorithm,
-restated in oracle/; the reference itself needs Eigen and cannot be built here).
+         with page-locked host buffers in the reference layout: each rank's
+         utterances as one call (bins flattened), H2D of X, a, b, R'^+ and
+         params0 and D2H of r_h, r_u, lambda inside the timed region.
+extras (N = 1): every other BASELINE config (C0, C1, C2, C4 in complex128 and
+complex64, C3 in complex64), the naive rule, the Wiener output after the solve,
+and the K1 / K4 stream kernels -- each with its own roofline.
+--impl reference runs the oracle port (the reference's CPU algorithm restated in
+oracle/; the reference itself needs Eigen and cannot be built here) on the host
+cores over a bounded sample of the same utterances.
 """
 from __future__ import annotations
 
@@ -34,15 +43,18 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-CFG = 1
+CFG = 3  # BASELINE configs[3]: the largest single-GPU configuration
 FLOPS_ACCEL = 47.0  # canonical flops per slot-iteration
 FLOPS_NAIVE = {2: 341.0, 4: 1804.0, 8: 11052.0}
-# K1 / K4 algorithmic bytes per slot (complex128): SURVEY 8(d). The timed step's
-# K1 is the sigma/tau pass only: read x (16 M) + write sigma_bx, tau_ax, tau_xx (40);
+# K1 / K4 algorithmic bytes per slot (complex128): SURVEY 8(d). The timed K1 is
+# the sigma/tau pass only: read x (16 M) + write sigma_bx, tau_ax, tau_xx (40);
 # SURVEY's 88/120/184 also count the r_h0 / r_u0 writes of the setup pass.
 BYTES_PRE = {2: 72.0, 4: 104.0, 8: 168.0}
 BYTES_WIENER = {2: 96.0, 4: 128.0, 8: 192.0}
 NOMINAL_FP64_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12  # HGX B200 spec class
+NOMINAL_FP32_TFLOPS = 2 * NOMINAL_FP64_TFLOPS
+METRIC = "TF-slot updates/s (I*J*iters/s), accelerated rule (Algorithm 2)"
+UNIT = "TF-slot updates/s"
 
 
 def dist_env():
@@ -50,6 +62,25 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def partition(n, world):
+    """Contiguous balanced ranges (paper_1908_01964_b200.shard.partition)."""
+    from paper_1908_01964_b200.shard import partition as p
+
+    return p(n, world)
+
+
+def headline_config(n_gpus):
+    """The `config` dict both arms print (identical for the same --gpus)."""
+    from paper_1908_01964_b200 import synth
+
+    c = synth.CONFIGS[CFG]
+    return {"workload": c["name"], "M": c["M"], "I": c["I"], "J": c["J"], "utterances": c["B"],
+            "iters": c["iters"], "rule": "accel2 (Algorithm 2, solver_accel.hpp:183-258)",
+            "seeds": f"utterance u: {1000 * CFG} + u", "precision": "complex128",
+            "parallelism": f"{c['B']} utterances in contiguous ranges over {n_gpus} GPU(s), no collective in the solve",
+            "l2": "inputs (x 2.69 GB + state) exceed the 126 MB L2; a 256 MiB write also flushes it between steps"}
 
 
 class ClockSampler:
@@ -123,22 +154,14 @@ def load_peaks():
         return {}
 
 
-def ncu_traffic(kernel_key):
-    """dram bytes per launch from the committed ncu summary (profiles/), or None."""
+def ncu_summary(kernel_key):
+    """The committed ncu summary entry (profiles/ncu_summary.json) or {}."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
-            d = json.load(f)
-        return d.get(kernel_key, {}).get("dram_bytes_per_launch")
+            return json.load(f).get(kernel_key, {})
     except (OSError, ValueError):
-        return None
-
-
-def workload_config():
-    from paper_1908_01964_b200 import synth
-
-    c = synth.CONFIGS[CFG]
-    return c
+        return {}
 
 
 def cpu_model():
@@ -152,434 +175,437 @@ def cpu_model():
     return "unknown"
 
 
-def oracle_problem(u):
+def gen_batch(cfg, lo, hi, I=None, J=None):
+    """Utterances [lo, hi) of BASELINE config `cfg` (seed 1000 cfg + u) stacked as
+    X (n, I, J, M), W, A (n, I, M, M), T (n, I, K), V (n, K, J), written in place
+    (no second copy of x)."""
+    from paper_1908_01964_b200 import synth
+
+    c = synth.CONFIGS[cfg]
+    I, J, M = I or c["I"], J or c["J"], c["M"]
+    n = hi - lo
+    X = np.empty((n, I, J, M), np.complex128)
+    W = np.empty((n, I, M, M), np.complex128)
+    A = np.empty((n, I, M, M), np.complex128)
+    T = np.empty((n, I, 4))
+    V = np.empty((n, 4, J))
+    for k, u in enumerate(range(lo, hi)):
+        ut = synth.make_utterance(M, I, J, c["d"], 1000 * cfg + u)
+        X[k], W[k], A[k], T[k], V[k] = ut.X, ut.W, ut.A, ut.T, ut.V
+    return X, W, A, T, V
+
+
+# ---- the reference arm / cpu_baseline: the oracle on the host cores -------------------
+def oracle_batch(X, W, A, T, V):
+    """Oracle setup (build_noise_scm + init_params per utterance, model.hpp:58-124),
+    concatenated over utterances along the bin axis: every equation of
+    Algorithm 2 is per bin, so one oracle call over the concatenation is the
+    same computation as one call per utterance."""
     from oracle import oracle as O
 
     O.build()
-    inp = O.build_noise_scm(u.W, u.A, u.X, 0)
-    p0 = O.init_params(inp, u.T, u.V, u.W, u.A, u.X)
-    return O, inp, p0
+    ins, ps = [], []
+    for k in range(X.shape[0]):
+        inp = O.build_noise_scm(W[k], A[k], X[k], 0)
+        ins.append(inp)
+        ps.append(O.init_params(inp, T[k], V[k], W[k], A[k], X[k]))
+    cat = lambda f, xs: np.concatenate([getattr(x, f) for x in xs], axis=0)
+    inp = O.Inputs(cat("a", ins), cat("R_prime", ins), cat("R_prime_pinv", ins), cat("b", ins), 0)
+    p0 = O.Params(cat("r_h", ps), cat("r_u", ps), cat("lam", ps))
+    return O, inp, p0, X.reshape(-1, X.shape[2], X.shape[3])
 
 
-def cpu_baseline(u, c, budget_s=10.0, threads=None):
-    """Oracle port of Algorithm 2 on the host cores over a bounded sample of the
-    workload: all I bins, J frames, as many iterations as fit ~budget_s."""
-    O, inp, p0 = oracle_problem(u)
-    threads = threads or os.cpu_count() or 1
-    I, J = u.X.shape[0], u.X.shape[1]
+def oracle_rate(steps, warmup, budget_s, threads):
+    """Times the oracle port of Algorithm 2 (all 100 iterations) on the first n of
+    the headline's utterances, n sized so steps + warmup runs take ~budget_s.
+    Returns (value slot-updates/s, per-step seconds, n, description)."""
+    from paper_1908_01964_b200 import synth
+
+    c = synth.CONFIGS[CFG]
+    iters = c["iters"]
+    X, W, A, T, V = gen_batch(CFG, 0, 1)
+    O, inp, p0, Xf = oracle_batch(X, W, A, T, V)
     t0 = time.perf_counter()
-    O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=2, threads=threads))
-    per_it = max((time.perf_counter() - t0) / 2, 1e-6)
-    iters = int(max(2, min(c["iters"], budget_s / per_it)))
-    # repeat the run until ~budget_s of CPU time has been spent (a 16-thread run
-    # of the full config is ~0.2 s, too short for a stable figure)
-    runs, dt = 0, 0.0
-    while runs < 3 or dt < budget_s:
+    O.run("accel2_binparallel", inp, p0, Xf, O.SolverOptions(iters=iters, threads=threads))
+    per_utt = max(time.perf_counter() - t0, 1e-4)
+    n = int(max(1, min(c["B"], budget_s / max(steps + warmup, 1) / per_utt)))
+    if n > 1:
+        X, W, A, T, V = gen_batch(CFG, 0, n)
+        O, inp, p0, Xf = oracle_batch(X, W, A, T, V)
+    for _ in range(warmup):
+        O.run("accel2_binparallel", inp, p0, Xf, O.SolverOptions(iters=iters, threads=threads))
+    times = []
+    for _ in range(steps):
         t0 = time.perf_counter()
-        O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=iters, threads=threads))
-        dt += time.perf_counter() - t0
-        runs += 1
-        if dt > 3 * budget_s:
-            break
-    # reference-faithful single thread (solver_accel.hpp:183-240 is serial), few iterations
-    it1 = 3
-    r1 = O.run("accel2", inp, p0, u.X, O.SolverOptions(iters=it1 + 3))
-    t_single = statistics.median(r1.iter_seconds[3:]) if len(r1.iter_seconds) > 3 else r1.iter_seconds[-1]
-    return {
-        "value": I * J * iters * runs / dt,
-        "unit": "TF-slot updates/s",
-        "cores": threads,
-        "kind": "port",
-        "sample": f"oracle Algorithm 2, all {I} bins x {J} frames, {iters} iterations (incl. sigma/tau precompute), "
-                  f"{runs} runs ({dt:.1f} s), bins split over {threads} threads; host {cpu_model()}",
-        "single_thread_value": I * J / t_single,
-        "single_thread_sample": "serial restatement of run_algorithm2 (the reference's accel2 is single-threaded), "
-                                "median per-iteration time after 3 warm-ups (metrics.hpp:43-51)",
-    }
+        O.run("accel2_binparallel", inp, p0, Xf, O.SolverOptions(iters=iters, threads=threads))
+        times.append(time.perf_counter() - t0)
+    slot_iters = n * c["I"] * c["J"] * iters
+    value = slot_iters * steps / sum(times)
+    desc = (f"oracle port of Algorithm 2 (solver_accel.hpp:183-240, incl. the sigma/tau precompute), utterances "
+            f"0..{n - 1} of the {c['B']} (seeds {1000 * CFG}..{1000 * CFG + n - 1}, the GPU arm's first {n}), all "
+            f"{iters} iterations, {steps} timed runs after {warmup} warm-up; bins over {threads} threads; per-utterance "
+            f"work is identical so the rate scales linearly to the full batch; host {cpu_model()}")
+    return value, times, n, desc
+
+
+def single_thread_rate():
+    """The reference-faithful serial restatement (solver_accel.hpp:183-240 is
+    single-threaded): median per-iteration time after 3 warm-ups (metrics.hpp:43-51)."""
+    from paper_1908_01964_b200 import synth
+
+    c = synth.CONFIGS[CFG]
+    X, W, A, T, V = gen_batch(CFG, 0, 1)
+    O, inp, p0, Xf = oracle_batch(X, W, A, T, V)
+    r = O.run("accel2", inp, p0, Xf, O.SolverOptions(iters=6))
+    t = statistics.median(r.iter_seconds[3:])
+    return c["I"] * c["J"] / t
 
 
 def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from paper_1908_01964_b200 import synth
-
-    c = workload_config()
-    u = synth.make_config(CFG, utterances=1)[0]
-    O, inp, p0 = oracle_problem(u)
     threads = os.cpu_count() or 1
-    I, J = u.X.shape[0], u.X.shape[1]
-    # size each step as a bounded sample: the full config if it fits ~20 s per step
-    t0 = time.perf_counter()
-    O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=2, threads=threads))
-    per_it = max((time.perf_counter() - t0) / 2, 1e-6)
-    total_budget = 150.0
-    iters = int(max(1, min(c["iters"], total_budget / max(args.steps + args.warmup, 1) / per_it)))
-    for _ in range(args.warmup):
-        O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=iters, threads=threads))
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        O.run("accel2_binparallel", inp, p0, u.X, O.SolverOptions(iters=iters, threads=threads))
-        times.append(time.perf_counter() - t0)
-    tot = sum(times)
-    value = I * J * iters * args.steps / tot
-    sample = (f"oracle port of Algorithm 2 (solver_accel.hpp:183-240) on the full config-1 problem "
-              f"({I} bins x {J} frames), {iters} of {c['iters']} iterations per step, bins over {threads} threads; "
-              f"host {cpu_model()}")
+    value, times, n, desc = oracle_rate(args.steps, args.warmup, 150.0, threads)
     line = {
         "impl": "reference",
-        "metric": "TF-slot updates/s (I*J*iters/s), accelerated rule (Algorithm 2)",
+        "metric": METRIC,
         "value": value,
-        "unit": "TF-slot updates/s",
+        "unit": UNIT,
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / args.steps,
+        "ms_per_step": 1e3 * sum(times) / len(times),
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic (BASELINE recipe, seed 1001)",
-        "config": {"workload": c["name"], "M": c["M"], "I": c["I"], "J": c["J"], "iters_per_step": iters,
-                   "rule": "accel2"},
-        "cpu_baseline": {"value": value, "unit": "TF-slot updates/s", "cores": threads, "kind": "port",
-                         "sample": sample},
-        "e2e": {"value": value, "unit": "TF-slot updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "note": "the reference (C++/Eigen) cannot be built in this image; oracle/ restates its algorithm",
+        "data": "synthetic (BASELINE recipe: sinc-coherent diffuse noise + NMF-variance target, 0 dB)",
+        "config": headline_config(args.gpus),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "note": "the reference (C++/Eigen) cannot be built in this image (Eigen absent); oracle/ restates its "
+                "algorithm line by line; each step is a bounded sample of the headline batch: "
+                f"{n} of {headline_config(args.gpus)['utterances']} utterances, host threads: {threads}",
     }
     print(json.dumps(line), flush=True)
+
+
+# ---- GPU arm -----------------------------------------------------------------------------
+class Dev:
+    """Per-process device handles shared by the measurements."""
+
+    def __init__(self, local, torch):
+        self.torch = torch
+        self.local = local
+        self.dev = torch.device("cuda", local)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=self.dev)
+
+    def flush(self):
+        with self.torch.cuda.stream(self.stream):
+            self.l2.fill_(1.0)
+
+    def event(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+
+def fp_probe(ctx, fp32=False):
+    import paper_1908_01964_b200._capi as C
+
+    tf, ms = ctypes.c_double(), ctypes.c_double()
+    fn = C.load().rcscm_gpu_probe_fp32 if fp32 else C.load().rcscm_gpu_probe_fp64
+    rc = fn(ctx.handle, ctypes.byref(tf), ctypes.byref(ms))
+    return (tf.value, ms.value) if rc == 0 else (None, None)
+
+
+def accel_roofline(ms, slots, iters, M, peak, f32=False, kernel="", ncu_key=None):
+    """FP64 (FP32 in complex64) roofline of one fused K2 launch: 47 flops per
+    slot-iteration + the sigma / tau forms once per slot (b^H x and
+    (R'^+ a)^H x: 8 M each; x^H R'^+ x from the lower triangle: 4 M^2 + 15 M)."""
+    pre = 4.0 * M * M + 15.0 * M
+    flops = FLOPS_ACCEL * slots * iters + pre * slots
+    achieved = flops / (ms * 1e-3) / 1e12
+    nominal = NOMINAL_FP32_TFLOPS if f32 else NOMINAL_FP64_TFLOPS
+    nc = ncu_summary(ncu_key) if ncu_key else {}
+    return {"bound": "fp32" if f32 else "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved / peak if peak else None, "nominal_peak": nominal, "frac_of_nominal": achieved / nominal,
+            "traffic": nc.get("dram_bytes_per_launch"), "kernel": kernel,
+            "flops_per_slot_iter": FLOPS_ACCEL, "slot_iters_per_launch": slots * iters,
+            "precompute_flops_per_slot": pre, "flops_per_launch": flops, "avg_launch_ms": ms,
+            "peak_source": ("measured live on this GPU: " + ("FFMA" if f32 else "DFMA") + " probe (rcscm_gpu_probe_"
+                            + ("fp32" if f32 else "fp64") + "); MEASURED_PEAKS.json has no FP64/FP32 figure"),
+            "ncu": {k: nc.get(k) for k in ("fp64_pipe_inst_pct", "stall_long_sb_per_issue", "duration_ns")} if nc
+            else None}
+
+
+def session_for(d, cfg, lo=0, hi=None, precision="c128", I=None, J=None, data=None):
+    from paper_1908_01964_b200 import GpuContext, synth
+    import paper_1908_01964_b200._capi as C
+
+    c = synth.CONFIGS[cfg]
+    hi = c["B"] if hi is None else hi
+    X, W, A, T, V = data if data is not None else gen_batch(cfg, lo, hi, I, J)
+    ctx = GpuContext(d.local, precision=precision, stream=d.stream.cuda_stream)
+    ctx.session_load(X, W, A, T, V, 0)
+    ctx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
+    ctx.session_check()
+    return ctx, X.shape
+
+
+def time_stages(d, ctx, stages, iters, reps, hyper, pre_stages=0, flush=True):
+    """Mean / min device time (ms) of session_run(stages) over reps after one
+    untimed run; pre_stages run untimed before each (e.g. RESET)."""
+    ctx.session_run(stages | pre_stages, iters, hyper)
+    ts = []
+    for _ in range(reps):
+        if pre_stages:
+            ctx.session_run(pre_stages, 0, hyper)
+        if flush:
+            d.flush()
+        e0, e1 = d.event(), d.event()
+        e0.record(d.stream)
+        ctx.session_run(stages, iters, hyper)
+        e1.record(d.stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ctx.session_check()
+    return statistics.mean(ts), min(ts)
 
 
 def run_gpu(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1908_01964_b200 import GpuContext, Hyperparams, synth
+    from paper_1908_01964_b200 import Hyperparams, synth
     import paper_1908_01964_b200._capi as C
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    d = Dev(local, torch)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    c = workload_config()
-    u = synth.make_config(CFG, utterances=1, seed_base=1000 * CFG + rank)[0]
-    X, W, A, T, V = synth.stack([u])
-    B, I, J, M = X.shape
+        dist.init_process_group("nccl", device_id=d.dev)
+    c = synth.CONFIGS[CFG]
     iters = c["iters"]
-    tstream = torch.cuda.Stream(device=dev)
-    ctx = GpuContext(local, stream=tstream.cuda_stream)
+    lo, hi = partition(c["B"], world)[rank]
     hyper = Hyperparams()
-    ctx.session_load(X, W, A, T, V, 0)
-    ctx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
-    ctx.session_check()
-    l2_flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
-
-    def flush():
-        with torch.cuda.stream(tstream):
-            l2_flush.fill_(1.0)
-
-    # one step = run_algorithm2 on resident inputs: restore params0, sigma / tau
-    # precompute, 100 iterations -- one fused K2 launch (precompute in its prologue)
+    data = gen_batch(CFG, lo, hi)
+    ctx, (B, I, J, M) = session_for(d, CFG, lo, hi, data=data)
     step_stages = C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL
 
-    # warm-up
     for _ in range(args.warmup):
         ctx.session_run(step_stages, iters, hyper)
-    torch.cuda.synchronize(dev)
+    torch.cuda.synchronize(d.dev)
     ctx.session_check()
 
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    ev = [(d.event(), d.event()) for _ in range(args.steps)]
+
     def lead_in(seconds):  # untimed steps while the clock sampler starts
         t_end = time.perf_counter() + seconds
         while time.perf_counter() < t_end:
-            for _ in range(20):
-                flush()
+            for _ in range(4):
+                d.flush()
                 ctx.session_run(step_stages, iters, hyper)
-            torch.cuda.synchronize(dev)
+            torch.cuda.synchronize(d.dev)
 
     with ClockSampler(local, lead_in) as clk:
         if world > 1:
             dist.barrier()
-        torch.cuda.synchronize(dev)
+        torch.cuda.synchronize(d.dev)
         launches0 = ctx.launch_count
         for k in range(args.steps):
-            flush()  # L2 flush between steps (outside the events)
+            d.flush()  # L2 flush between steps (outside the events)
             e0, e1 = ev[k]
-            e0.record(tstream)
+            e0.record(d.stream)
             ctx.session_run(step_stages, iters, hyper)
-            e1.record(tstream)
-        torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
+            e1.record(d.stream)
+        torch.cuda.synchronize(d.dev)
     launches = (ctx.launch_count - launches0) / args.steps
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
-    k2_ms = step_ms  # the step is the single fused K2 launch
     tot_ms = sum(step_ms)
     if world > 1:
-        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        t = torch.tensor([tot_ms], device=d.dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         tot_ms = float(t.item())
+        dist.barrier()
     ctx.session_check()
-    slot_iters = B * I * J * iters
-    value = slot_iters * world * args.steps / (tot_ms * 1e-3)
+    S_all = c["B"] * c["I"] * c["J"]
+    value = S_all * iters * args.steps / (tot_ms * 1e-3)
+    fp64_peak, probe_ms = fp_probe(ctx)
+    k2_avg = sum(step_ms) / len(step_ms)
+    roofline = accel_roofline(k2_avg, B * I * J, iters, M, fp64_peak,
+                              kernel="k_accel<5,1,FULL,-,0,3,DIRECT,double,PREM=4> (K2: sigma/tau precompute fused "
+                                     "into the prologue, then the on-chip Algorithm 2 iterations), this rank's "
+                                     f"{B} utterances x {I} bins", ncu_key="k_accel_c3")
+    roofline["peak_probe"] = {"tflops": fp64_peak, "ms": probe_ms, "sm_mhz_during_bench": None}
+    ctx.close()
 
-    # roofline of K2 (FP64 pipe) against the measured DFMA peak
-    tf = ctypes.c_double()
-    pm = ctypes.c_double()
-    rc = C.load().rcscm_gpu_probe_fp64(ctx.handle, ctypes.byref(tf), ctypes.byref(pm))
-    fp64_peak = tf.value if rc == 0 else NOMINAL_FP64_TFLOPS
-    k2_avg = sum(k2_ms) / len(k2_ms)
-    # algorithmic flops of the fused launch: the sigma / tau forms once per slot
-    # (b^H x and (R'^+ a)^H x: 8 M each; x^H R'^+ x with R'^+ Hermitian: 3 M on the
-    # diagonal + 8 per lower-triangle pair -> 4 M^2 + 15 M) plus 47 per
-    # slot-iteration (SURVEY 8(d))
-    pre_flops = 4.0 * M * M + 15.0 * M
-    launch_flops = FLOPS_ACCEL * slot_iters + pre_flops * B * I * J
-    achieved = launch_flops / (k2_avg * 1e-3) / 1e12
-    roofline = {"bound": "fp64", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": ncu_traffic("k_accel"),
-                "kernel": "k_accel<PREM=M> (K2 with the sigma/tau precompute fused into its prologue, then the "
-                          "on-chip Algorithm 2 iterations)",
-                "flops_per_slot_iter": FLOPS_ACCEL, "slot_iters_per_launch": slot_iters,
-                "precompute_flops_per_slot": pre_flops, "flops_per_launch": launch_flops,
-                "avg_launch_ms": k2_avg,
-                "peak_source": "measured live: DFMA probe (rcscm_gpu_probe_fp64) on this GPU; MEASURED_PEAKS.json "
-                               "has no FP64 figure",
-                "frac_basis": "of measured (FP64 pipe; the kernel is neither HBM- nor tensor-bound)",
-                "nominal_peak": NOMINAL_FP64_TFLOPS,
-                "frac_of_nominal": achieved / NOMINAL_FP64_TFLOPS}
-
-    # secondary kernels: K1 precompute and K4 wiener (HBM), naive rule (FP64)
-    peaks = load_peaks()
-    hbm = peaks.get("hbm_gbs", 6650.0)
-    S = B * I * J
-
-    def timed(stages, n, reps=5):
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ctx.session_run(stages, n, hyper)
-        flush()
-        e0.record(tstream)
-        for _ in range(reps):
-            ctx.session_run(stages, n, hyper)
-        e1.record(tstream)
-        e1.synchronize()
-        return e0.elapsed_time(e1) / reps
-
-    naive_iters = c["naive_iters"]
-    naive_ms = timed(C.STAGE_RESET | C.STAGE_NAIVE, naive_iters, reps=3)
-    ctx.session_check()
-    stream_kernels = stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, torch, C)
-    naive = {"value": S * naive_iters / (naive_ms * 1e-3), "unit": "TF-slot updates/s", "iters": naive_iters,
-             "ms_per_run": naive_ms,
-             "achieved_tflops_canonical": FLOPS_NAIVE.get(M, 0) * S * naive_iters / (naive_ms * 1e-3) / 1e12,
-             "canonical_flops_per_slot_iter": FLOPS_NAIVE.get(M),
-             "accel_over_naive_per_iteration": (naive_ms / naive_iters) / (k2_avg / iters)}
-
-    # complex64 (FP32) mode of the same step, against the measured FP32 peak
-    c64 = c64_measure(local, tstream, X, W, A, T, V, iters, hyper, S, args, torch, C)
-
-    # e2e through the C ABI with pinned host buffers (reference layout)
-    # (a fresh context, as a caller of the C ABI has: no session state, its own stream)
-    e2e_ctx = GpuContext(local)
-    e2e = e2e_measure(e2e_ctx, u, iters, hyper, args, torch, world, dev)
-    e2e_ctx.close()
+    # e2e through the C ABI with pinned host buffers (reference layout), this
+    # rank's utterances as one call
+    e2e = e2e_measure(d, data, iters, hyper, args, world, S_all)
+    del data
 
     out = None
+    extras = None
+    if world == 1:
+        extras = run_extras(d, hyper, args)
     if rank == 0:
         clocks = clk.summary()
-        cpu = cpu_baseline(u, c) if world == 1 else None  # rank 0 at N = 1 only
+        roofline["peak_probe"]["sm_mhz_during_bench"] = clocks.get("sm_mhz")
+        cpu = None
+        if world == 1:  # rank 0 at N = 1 only
+            threads = os.cpu_count() or 1
+            v, times, n, desc = oracle_rate(1, 1, 20.0, threads)
+            cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "port", "sample": desc,
+                   "single_thread_value": single_thread_rate(),
+                   "single_thread_sample": "serial restatement of run_algorithm2 (the reference's accel2 is "
+                                           "single-threaded) on utterance 0: median per-iteration time after 3 "
+                                           "warm-ups (metrics.hpp:43-51)"}
         out = {
-            "metric": "TF-slot updates/s (I*J*iters/s), accelerated rule (Algorithm 2)",
+            "metric": METRIC,
             "value": value,
-            "unit": "TF-slot updates/s",
+            "unit": UNIT,
             "n_gpus": world,
             "steps": args.steps,
             "warmup": args.warmup,
             "ms_per_step": tot_ms / args.steps,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
             "dtype": "f64",
-            "data": "synthetic (BASELINE recipe: sinc-coherent diffuse noise + NMF-variance target, 0 dB; seed 1001+rank)",
-            "config": {"workload": c["name"], "M": M, "I": I, "J": J, "utterances_per_gpu": B, "iters": iters,
-                       "step": "run_algorithm2 on resident inputs: params0, sigma/tau precompute fused into the "
-                               "prologue of K2, 100 on-chip iterations (one kernel)",
-                       "l2": "flushed between steps (256 MiB write, outside the timed events)",
-                       "clock_lead_in": "0.3 s of untimed steps while nvidia-smi starts, so the timed steps "
-                                        "do not start from an idle GPU",
-                       "parallelism": f"bins sharded by utterance, {world} GPU(s), no collective in the loop"},
+            "data": "synthetic (BASELINE recipe: sinc-coherent diffuse noise + NMF-variance target, 0 dB)",
+            "config": headline_config(world),
             "gpu_launches": launches,
-            "breakdown_ms": {"fused_k2": k2_avg},
+            "breakdown_ms": {"fused_k2": k2_avg, "rank0_utterances": B},
             "roofline": roofline,
-            "stream_kernels": stream_kernels,
-            "naive": naive,
-            "c64": c64,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": clocks,
+            "extras": extras,
         }
         print(json.dumps(out), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    ctx.close()
 
 
-def stream_measure(ctx, tstream, flush, hyper, S, M, hbm, X, W, A, T, V, local, torch, C):
-    """K1 (standalone precompute) and K4 (Wiener) against the HBM peak: the
-    bench-utterance launch timed alone after an L2 flush (68 / 84 MB: launch-
-    latency bound), the same launch 8 times back to back on distinct copies
-    (steady state), and one launch over a batch of 8 copies (0.5 / 0.7 GB: the
-    streaming regime the batched configs run in)."""
-    from paper_1908_01964_b200 import GpuContext
-    import numpy as np
+def run_extras(d, hyper, args):
+    """Every other BASELINE config, the naive rule, the Wiener output and the
+    stream kernels, one session at a time (N = 1)."""
+    import paper_1908_01964_b200._capi as C
+    from paper_1908_01964_b200 import synth
 
-    def cold(cx, stages, reps=7):
-        ts = []
-        for r in range(reps + 1):
-            flush()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(tstream)
-            cx.session_run(stages, 0, hyper)
-            e1.record(tstream)
-            e1.synchronize()
-            if r:
-                ts.append(e0.elapsed_time(e1))
-        return statistics.median(ts)
+    torch = d.torch
+    out = {}
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs", 6554.2)
+    reps = max(3, min(args.steps, 10))
+    step = C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL
+    fp64_peak = fp32_peak = None
 
-    def entry(ms, bps, n):
+    def stream_entry(ms, bps, n):
         gbs = bps * n / (ms * 1e-3) / 1e9
-        return {"ms": ms, "bytes_per_slot": bps, "slots": n, "achieved_gbs": gbs, "peak_gbs": hbm, "frac": gbs / hbm,
-                "frac_basis": "of measured (MEASURED_PEAKS.json hbm_gbs)"}
+        return {"ms": ms, "bytes_per_slot": bps, "slots": n, "achieved_gbs": gbs, "peak_gbs": hbm,
+                "frac": gbs / hbm, "frac_basis": "of measured (MEASURED_PEAKS.json hbm_gbs)"}
 
-    ctx.session_run(C.STAGE_PRECOMPUTE, 0, hyper)
-    out = {"k_pre": entry(cold(ctx, C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S),
-           "k_wiener": entry(cold(ctx, C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S)}
+    for cfg in (0, 1, 2, 4):
+        c = synth.CONFIGS[cfg]
+        ctx, (B, I, J, M) = session_for(d, cfg)
+        if fp64_peak is None:
+            fp64_peak, _ = fp_probe(ctx)
+        S = B * I * J
+        mean, best = time_stages(d, ctx, step, c["iters"], reps, hyper)
+        e = {"workload": c["name"], "iters": c["iters"], "ms_per_step": mean, "ms_min": best,
+             "value": S * c["iters"] / (mean * 1e-3), "unit": UNIT,
+             "roofline": accel_roofline(mean, S, c["iters"], M, fp64_peak, kernel="fused K2 (k_accel, PREM=M)",
+                                        ncu_key=f"k_accel_c{cfg}")}
+        if cfg in (0, 1):
+            # the Wiener output from the resident state (K4) and the standalone
+            # precompute (K1), one launch after an L2 flush
+            pre, _ = time_stages(d, ctx, C.STAGE_PRECOMPUTE, 0, reps, hyper)
+            wie, _ = time_stages(d, ctx, C.STAGE_WIENER, 0, reps, hyper)
+            e["k_pre"] = stream_entry(pre, BYTES_PRE[M], S)
+            e["k_wiener"] = stream_entry(wie, BYTES_WIENER[M], S)
+        if c["naive_iters"]:
+            n_it = c["naive_iters"]
+            nm, _ = time_stages(d, ctx, C.STAGE_NAIVE, n_it, 2, hyper, pre_stages=C.STAGE_RESET)
+            e["naive"] = naive_entry(nm, S, n_it, M, fp64_peak, mean / c["iters"])
+        out[f"c{cfg}"] = e
+        ctx.close()
+        if cfg == 4:
+            cx, _ = session_for(d, cfg, precision="c64")
+            mean64, best64 = time_stages(d, cx, step, c["iters"], reps, hyper)
+            if fp32_peak is None:
+                fp32_peak, _ = fp_probe(cx, fp32=True)
+            out["c4_c64"] = {"workload": c["name"] + "_c64", "iters": c["iters"], "ms_per_step": mean64,
+                             "value": S * c["iters"] / (mean64 * 1e-3), "unit": UNIT,
+                             "roofline": accel_roofline(mean64, S, c["iters"], M, fp32_peak, f32=True,
+                                                        kernel="K1 (FP32) + K2<float>", ncu_key="k_accel_c4_c64"),
+                             "note": "complex64 mode: x, sigma/tau and the slot arithmetic in FP32, lambda in FP64; "
+                                     "output within relative-L2 1e-4 of complex128 (tests)"}
+            cx.close()
+        torch.cuda.empty_cache()
 
-    def copy_cold(nbytes, reps=7):
-        # torch's device copy moving the same bytes (half read, half written),
-        # timed like the kernels: what a plain stream achieves at this size
-        n = max(int(nbytes // 8), 1)
-        src = torch.ones(n, dtype=torch.float32, device=f"cuda:{local}")
-        dst = torch.empty_like(src)
-        ts = []
-        for r in range(reps + 1):
-            flush()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(tstream)
-            with torch.cuda.stream(tstream):
-                dst.copy_(src)
-            e1.record(tstream)
-            e1.synchronize()
-            if r:
-                ts.append(e0.elapsed_time(e1))
-        return statistics.median(ts)
-
-    for name, bps in (("copy_same_bytes_as_k_pre", BYTES_PRE.get(M, 0)), ("copy_same_bytes_as_k_wiener",
-                                                                           BYTES_WIENER.get(M, 0))):
-        out[name] = entry(copy_cold(bps * S), bps, S)
-    nb = 8
-    # the single-utterance launch in steady state: 8 contexts, each holding its own
-    # copy of the utterance (0.5 GB in all, > L2), launched back to back after one
-    # flush, so each launch streams cold data and the launch latency overlaps
-    ctxs = [GpuContext(local, stream=tstream.cuda_stream) for _ in range(nb)]
-    for cx in ctxs:
-        cx.session_load(X, W, A, T, V, 0)
-        cx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
-        cx.session_run(C.STAGE_ACCEL, 3, hyper)
-
-    def chain(stages, reps=5):
-        ts = []
-        for r in range(reps + 1):
-            flush()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(tstream)
-            for cx in ctxs:
-                cx.session_run(stages, 0, hyper)
-            e1.record(tstream)
-            e1.synchronize()
-            if r:
-                ts.append(e0.elapsed_time(e1) / nb)
-        return statistics.median(ts)
-
-    out["k_pre_steady"] = entry(chain(C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S)
-    out["k_wiener_steady"] = entry(chain(C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S)
-    for cx in ctxs:
-        cx.session_check()
-        cx.close()
-    big = GpuContext(local, stream=tstream.cuda_stream)
-    rep = lambda v: np.concatenate([v] * nb, axis=0)
-    big.session_load(rep(X), rep(W), rep(A), rep(T), rep(V), 0)
-    big.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
-    big.session_run(C.STAGE_ACCEL, 3, hyper)
-    out["k_pre_batch8"] = entry(cold(big, C.STAGE_PRECOMPUTE), BYTES_PRE.get(M, 0), S * nb)
-    out["k_wiener_batch8"] = entry(cold(big, C.STAGE_WIENER), BYTES_WIENER.get(M, 0), S * nb)
-    big.session_check()
-    big.close()
-    out["note"] = ("k_pre / k_wiener: one launch alone after an L2 flush (launch latency included); *_steady: "
-                   "the same single-utterance launch, 8 back to back on distinct copies after one flush (cold "
-                   "data, latency overlapped); *_batch8: one launch over 8 utterances; algorithmic bytes (K1: "
-                   "read x, write sigma_bx, tau_ax, tau_xx; K4: read sigma_bx, tau_ax, r_h, r_u, write dry + image); "
-                   "copy_same_bytes_as_*: torch's device copy moving the same bytes, timed the same way (the "
-                   "bandwidth a plain stream reaches at this size)")
+    # the headline batch: complex64, naive, Wiener / precompute stream kernels
+    c = synth.CONFIGS[CFG]
+    ctx, (B, I, J, M) = session_for(d, CFG)
+    S = B * I * J
+    base_mean, _ = time_stages(d, ctx, step, c["iters"], 3, hyper)
+    pre, _ = time_stages(d, ctx, C.STAGE_PRECOMPUTE, 0, reps, hyper)
+    wie, _ = time_stages(d, ctx, C.STAGE_WIENER, 0, reps, hyper)
+    nm, _ = time_stages(d, ctx, C.STAGE_NAIVE, c["naive_iters"], 2, hyper, pre_stages=C.STAGE_RESET)
+    solve_ext, _ = time_stages(d, ctx, step | C.STAGE_WIENER, c["iters"], 3, hyper)
+    out["c3_stream"] = {"k_pre": stream_entry(pre, BYTES_PRE[M], S), "k_wiener": stream_entry(wie, BYTES_WIENER[M], S),
+                        "note": "one launch over all 256 utterances after an L2 flush (the streaming regime)"}
+    out["c3_naive"] = naive_entry(nm, S, c["naive_iters"], M, fp64_peak, base_mean / c["iters"])
+    out["c3_solve_then_extract"] = {"ms_per_step": solve_ext, "value": S * c["iters"] / (solve_ext * 1e-3),
+                                    "unit": UNIT, "wiener_extra_ms": solve_ext - base_mean,
+                                    "note": "run_algorithm2 then extract_target (dry + image) on the resident batch"}
+    ctx.close()
+    torch.cuda.empty_cache()
+    cx, _ = session_for(d, CFG, precision="c64")
+    m64, _ = time_stages(d, cx, step, c["iters"], reps, hyper)
+    out["c3_c64"] = {"workload": c["name"] + "_c64", "ms_per_step": m64, "value": S * c["iters"] / (m64 * 1e-3),
+                     "unit": UNIT, "roofline": accel_roofline(m64, S, c["iters"], M, fp32_peak, f32=True,
+                                                              kernel="K1 (FP32) + K2<float>")}
+    cx.close()
+    torch.cuda.empty_cache()
+    out["peaks"] = {"fp64_dfma_probe_tflops": fp64_peak, "fp32_ffma_probe_tflops": fp32_peak,
+                    "fp64_nominal_tflops": NOMINAL_FP64_TFLOPS, "hbm_gbs": hbm}
     return out
 
 
-def c64_measure(local, tstream, X, W, A, T, V, iters, hyper, S, args, torch, C):
-    """The same device step in the complex64 / FP32 mode (output within
-    relative-L2 1e-4 of complex128, tests/test_gpu_parity.py)."""
+def naive_entry(ms, S, iters, M, fp64_peak, accel_ms_per_iter):
+    canon = FLOPS_NAIVE.get(M, 0) * S * iters / (ms * 1e-3) / 1e12
+    return {"iters": iters, "ms_per_run": ms, "value": S * iters / (ms * 1e-3), "unit": UNIT,
+            "throughput_equivalent_tflops": canon, "canonical_flops_per_slot_iter": FLOPS_NAIVE.get(M),
+            "throughput_equivalent_frac": canon / fp64_peak if fp64_peak else None,
+            "accel_over_naive_per_iteration": (ms / iters) / accel_ms_per_iter,
+            "note": "k_naive forms R_x^-1 per slot but consumes R^_u only through b^H R^_u b and tr(R_u^-1 R^_u), "
+                    "so it executes fewer flops than the canonical count: the TFLOP/s figure is a throughput-"
+                    "equivalent, not a pipe utilisation (see profiles/ncu_summary.json k_naive for the FP64 pipe)"}
+
+
+def e2e_measure(d, data, iters, hyper, args, world, S_all):
+    """rcscm_gpu_run_algorithm2 with page-locked host inputs/outputs (reference
+    layout): this rank's utterances as one call (bins flattened utterance-major,
+    as a reference caller concatenating RcscmInputs would pass them). Whole-job
+    value = all ranks' slot-iterations over the slowest rank's mean call time;
+    byte counts are summed over ranks."""
+    import paper_1908_01964_b200._capi as C
     from paper_1908_01964_b200 import GpuContext
 
-    ctx = GpuContext(local, precision="c64", stream=tstream.cuda_stream)
-    ctx.session_load(X, W, A, T, V, 0)
-    ctx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
-    for _ in range(max(args.warmup, 1)):
-        ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE, 0, hyper)
-        ctx.session_run(C.STAGE_ACCEL, iters, hyper)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    for e0, e1, e2 in ev:
-        e0.record(tstream)
-        ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE, 0, hyper)
-        e1.record(tstream)
-        ctx.session_run(C.STAGE_ACCEL, iters, hyper)
-        e2.record(tstream)
-    torch.cuda.synchronize()
-    ctx.session_check()
-    step = sum(a.elapsed_time(c) for a, _, c in ev) / len(ev)
-    k2 = sum(b.elapsed_time(c) for _, b, c in ev) / len(ev)
-    tf = ctypes.c_double()
-    rc = C.load().rcscm_gpu_probe_fp32(ctx.handle, ctypes.byref(tf), None)
-    peak = tf.value if rc == 0 else None
-    achieved = FLOPS_ACCEL * S * iters / (k2 * 1e-3) / 1e12
-    ctx.close()
-    return {"value": S * iters / (step * 1e-3), "unit": "TF-slot updates/s", "ms_per_step": step,
-            "accel_k2_ms": k2, "achieved_tflops": achieved, "fp32_peak_tflops": peak,
-            "frac": achieved / peak if peak else None,
-            "note": "same step with x, sigma/tau and the slot arithmetic in single precision; lambda in double"}
-
-
-def e2e_measure(ctx, u, iters, hyper, args, torch, world=1, dev=None):
-    """rcscm_gpu_run_algorithm2 with pinned host inputs/outputs (reference layout).
-    With N ranks each rank runs its own utterance; the whole-job value is
-    N x I*J*iters over the slowest rank's mean call time, and the byte counts are
-    summed over ranks."""
-    import paper_1908_01964_b200._capi as C
-
+    torch = d.torch
+    X, W, A, T, V = data
+    B, I, J, M = X.shape
+    ctx = GpuContext(d.local)  # a fresh context, as a caller of the C ABI has
     lib = C.load()
-    inp = ctx.build_noise_scm(u.W, u.A, u.X, 0)
-    p0 = ctx.init_params(inp, u.T, u.V, u.W, u.A, u.X)
-    I, J, M = u.X.shape
-
-    # page-locked host buffers from cudaHostAlloc, as a C caller would allocate
-    # them (torch's pin_memory() blocks measured 27-37 GB/s of H2D on the B200
-    # box against 52 GB/s for cudaHostAlloc / cudaHostRegister memory:
-    # tools/pin_probe.py)
     rt = ctypes.CDLL("libcudart.so.12")
     held = []
 
+    # page-locked host buffers from cudaHostAlloc, as a C caller would allocate
+    # them (torch's pin_memory() blocks measured 27-37 GB/s of H2D on the B200
+    # box against 52 GB/s for cudaHostAlloc memory: tools/pin_probe.py)
     def pinned_empty(n):
         p = ctypes.c_void_p()
         if rt.cudaHostAlloc(ctypes.byref(p), ctypes.c_size_t(max(n, 1) * 8), ctypes.c_uint(0)) != 0:
@@ -587,24 +613,27 @@ def e2e_measure(ctx, u, iters, hyper, args, torch, world=1, dev=None):
         held.append(p)
         return np.ctypeslib.as_array(ctypes.cast(p, ctypes.POINTER(ctypes.c_double)), shape=(max(n, 1),))[:n]
 
-    def pinned(arr):
-        a = np.ascontiguousarray(arr).reshape(-1)
-        out = pinned_empty(a.size)
-        out[:] = a
-        return out
-
-    Xp = pinned(u.X.view(np.float64))
-    ap = pinned(inp.a.view(np.float64))
-    bp = pinned(inp.b.view(np.float64))
-    rpp = pinned(np.ascontiguousarray(inp.R_prime_pinv.transpose(0, 2, 1)).view(np.float64))
-    rh0 = pinned(np.ascontiguousarray(p0.r_h.T))
-    ru0 = pinned(np.ascontiguousarray(p0.r_u.T))
-    l0 = pinned(p0.lam)
-    rh = pinned_empty(I * J)
-    ru = pinned_empty(I * J)
-    lam = pinned_empty(I)
+    nb = B * I
+    Xp = pinned_empty(nb * J * M * 2)
+    Xp[:] = X.reshape(-1).view(np.float64)
+    ap, bp = pinned_empty(nb * M * 2), pinned_empty(nb * M * 2)
+    rpp = pinned_empty(nb * M * M * 2)
+    rh0, ru0, l0 = pinned_empty(nb * J), pinned_empty(nb * J), pinned_empty(nb)
+    rh0v, ru0v = rh0.reshape(J, nb), ru0.reshape(J, nb)  # I x J column-major
+    for k in range(B):
+        inp = ctx.build_noise_scm(W[k], A[k], X[k], 0)
+        p0 = ctx.init_params(inp, T[k], V[k], W[k], A[k], X[k])
+        s = slice(k * I, (k + 1) * I)
+        ap.reshape(nb, M * 2)[s] = inp.a.view(np.float64).reshape(I, M * 2)
+        bp.reshape(nb, M * 2)[s] = inp.b.view(np.float64).reshape(I, M * 2)
+        rpp.reshape(nb, M * M * 2)[s] = np.ascontiguousarray(inp.R_prime_pinv.transpose(0, 2, 1)).view(
+            np.float64).reshape(I, M * M * 2)
+        rh0v[:, s] = p0.r_h.T
+        ru0v[:, s] = p0.r_u.T
+        l0[s] = p0.lam
+    rh, ru, lam = pinned_empty(nb * J), pinned_empty(nb * J), pinned_empty(nb)
     dp = lambda a: ctypes.cast(a.ctypes.data, C._dp)
-    ci = C.CInputs(I, J, M, 0, dp(ap), None, dp(rpp), dp(bp))
+    ci = C.CInputs(nb, J, M, 0, dp(ap), None, dp(rpp), dp(bp))
     cp = C.CParams(dp(rh0), dp(ru0), dp(l0))
     co = C.CParams(dp(rh), dp(ru), dp(lam))
     h = C.CHyper(hyper.alpha, hyper.beta)
@@ -616,9 +645,7 @@ def e2e_measure(ctx, u, iters, hyper, args, torch, world=1, dev=None):
         if rc != 0:
             raise RuntimeError(lib.rcscm_gpu_last_error().decode())
 
-    # untimed warm-up: the per-call time settles after ~10 calls (PCIe / clock
-    # ramp; measured on B200, tools/e2e_bench_check.py)
-    for _ in range(max(args.warmup, 10)):
+    for _ in range(max(args.warmup, 3)):
         call()
     if world > 1:
         import torch.distributed as dist
@@ -629,23 +656,29 @@ def e2e_measure(ctx, u, iters, hyper, args, torch, world=1, dev=None):
         t0 = time.perf_counter()
         call()
         ts.append(time.perf_counter() - t0)
-    if os.environ.get("RCSCM_E2E_VERBOSE"):
-        print("e2e per call (ms):", " ".join(f"{t * 1e3:.3f}" for t in ts), file=sys.stderr)
     dt = sum(ts) / args.steps
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        t = torch.tensor([dt], device=d.dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dt = float(t.item())
     h2d = (Xp.size + ap.size + bp.size + rpp.size + rh0.size + ru0.size + l0.size) * 8
     d2h = (rh.size + ru.size + lam.size) * 8
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([h2d, d2h], device=d.dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        h2d, d2h = int(t[0].item()), int(t[1].item())
     for p in held:
         rt.cudaFreeHost(p)
-    return {"value": world * I * J * iters / dt, "unit": "TF-slot updates/s", "h2d_bytes_per_step": world * h2d,
-            "d2h_bytes_per_step": world * d2h, "ms_per_step": dt * 1e3,
-            "path": "rcscm_gpu_run_algorithm2 (C ABI, synchronous) with pinned host buffers, host wall clock"
-                    + (f"; {world} ranks, one utterance each, slowest rank's time" if world > 1 else "")}
+    ctx.close()
+    return {"value": S_all * iters / dt, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "ms_per_step": dt * 1e3, "h2d_gbs": h2d / world / dt / 1e9,
+            "path": "rcscm_gpu_run_algorithm2 (C ABI, synchronous) with cudaHostAlloc host buffers in the reference "
+                    f"layout, host wall clock; each rank's {B} utterances as one call ({nb} bins)"
+                    + (f"; {world} ranks, slowest rank's time" if world > 1 else "")}
 
 
 def main():

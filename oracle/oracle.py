@@ -586,3 +586,68 @@ def trajectory_distance(p: Params, q: Params) -> float:
         den = np.maximum(np.maximum(np.abs(x), np.abs(y)), 1e-12)
         return float(np.max(np.abs(x - y) / den)) if x.size else 0.0
     return max(d(p.r_h, q.r_h), d(p.r_u, q.r_u), d(p.lam, q.lam))
+
+
+# ---- binary128 ground truth (truth.cpp) ---------------------------------------
+_TRUTH_PATH = os.path.join(_HERE, "librcscm_truth.so")
+_tlib = None
+
+
+def truth_lib():
+    """librcscm_truth.so: one iteration of Algorithm 2 / the naive rule and the
+    Wiener dry output evaluated in IEEE binary128 on the same double inputs
+    (test infrastructure: the yardstick both double implementations -- this
+    oracle and the CUDA path -- are measured against)."""
+    global _tlib
+    if _tlib is None:
+        if not os.path.exists(_TRUTH_PATH) or os.path.getmtime(_TRUTH_PATH) < os.path.getmtime(
+                os.path.join(_HERE, "truth.cpp")):
+            subprocess.run(["make", "-C", _HERE, "librcscm_truth.so"], check=True, stdout=subprocess.DEVNULL)
+        _tlib = ctypes.CDLL(_TRUTH_PATH)
+    return _tlib
+
+
+def truth_accel_one_iter(inputs: Inputs, params0: Params, X, alpha=1.1, beta=1e-16, eps=1e-12):
+    """-> (Params after one Algorithm 2 iteration, S_ru (I, J), S_lam (I,)) in
+    binary128 rounded to double; S_ru = (|g rho_aa q| + |rho_xx| + |2 g Re(.)|)/M,
+    the magnitude scale of the r_u update (solver_accel.hpp:160-176), S_lam the
+    mean |term| of the lambda sum (:143-158)."""
+    X = _c(X)
+    I, J, M = X.shape
+    r_h, r_u, S = np.zeros(I * J), np.zeros(I * J), np.zeros(I * J)
+    lam, Sl = np.zeros(I), np.zeros(I)
+    rc = truth_lib().truth_accel_one_iter(
+        _i64(I), _i64(J), M, _p(_c(inputs.a)), _p(mats_to_ref(inputs.R_prime_pinv)), _p(_c(inputs.b)),
+        _p(ij_to_ref(params0.r_h)), _p(ij_to_ref(params0.r_u)), _p(_c(params0.lam, np.float64)),
+        ctypes.c_double(alpha), ctypes.c_double(beta), ctypes.c_double(eps), _p(X), _p(r_h), _p(r_u), _p(lam),
+        _p(S), _p(Sl))
+    if rc:
+        raise NumericalError("truth_accel_one_iter failed")
+    f = lambda v: v.reshape(J, I).T.copy()
+    return Params(f(r_h), f(r_u), lam), f(S), Sl
+
+
+def truth_naive_one_iter(inputs: Inputs, params0: Params, X, alpha=1.1, beta=1e-16, eps=1e-12):
+    """-> Params after one naive iteration (solver_naive.hpp:153-386) in binary128."""
+    X = _c(X)
+    I, J, M = X.shape
+    r_h, r_u, lam = np.zeros(I * J), np.zeros(I * J), np.zeros(I)
+    rc = truth_lib().truth_naive_one_iter(
+        _i64(I), _i64(J), M, _p(_c(inputs.a)), _p(mats_to_ref(inputs.R_prime)), _p(_c(inputs.b)),
+        _p(ij_to_ref(params0.r_h)), _p(ij_to_ref(params0.r_u)), _p(_c(params0.lam, np.float64)),
+        ctypes.c_double(alpha), ctypes.c_double(beta), ctypes.c_double(eps), _p(X), _p(r_h), _p(r_u), _p(lam))
+    if rc:
+        raise NumericalError("truth_naive_one_iter: singular matrix")
+    f = lambda v: v.reshape(J, I).T.copy()
+    return Params(f(r_h), f(r_u), lam)
+
+
+def truth_wiener_dry(inputs: Inputs, p: Params, X):
+    """-> dry (I, J) of extract_target (wiener.hpp:19-43) in binary128."""
+    X = _c(X)
+    I, J, M = X.shape
+    dry = np.zeros(I * J, np.complex128)
+    truth_lib().truth_wiener(_i64(I), _i64(J), M, _p(_c(inputs.a)), _p(mats_to_ref(inputs.R_prime_pinv)),
+                             _p(_c(inputs.b)), _p(ij_to_ref(p.r_h)), _p(ij_to_ref(p.r_u)),
+                             _p(_c(p.lam, np.float64)), _p(X), _p(dry))
+    return dry.reshape(J, I).T.copy()

@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       aa = cfmac(ak, pp[k], aa);
     }
     sab = ab;
-    taa = fmax(aa.x, 0.0);
+    taa = std_max(aa.x, 0.0);
     if (rank == 0 && tid == 0 && P.sigma_ab_w) {
       P.sigma_ab_w[bin] = sab;
       P.tau_aa_w[bin] = taa;

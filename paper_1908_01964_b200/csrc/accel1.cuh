@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(NT) k_accel1(Accel1Args P) {
       const double2 trax = P.rho_ax[slot];
       const double g = rh / (ru + rh * trho_aa) + P.gamma_fault;
       P.gamma[slot] = g;
-      P.r_h[slot] = fmax((g * (ru + g * cnorm(trax)) + P.beta) / P.alpha2, P.eps);
+      P.r_h[slot] = std_max((g * (ru + g * cnorm(trax)) + P.beta) / P.alpha2, P.eps);
       const double2 sbx = P.sigma_bx[slot];
       const double2 gc = cscale(csab, g);
       const double2 resid = csub(sbx, cmul(gc, trax));
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(NT) k_accel1(Accel1Args P) {
     __syncthreads();
     double total = 0.0;
     for (int w = 0; w < NT / 32; ++w) total += red[buf][w];
-    lam = fmax(total / static_cast<double>(J), P.eps);
+    lam = std_max(total / static_cast<double>(J), P.eps);
     // rho with the new lambda (line 14) and r_u (solver_accel.hpp:160-176)
     first_stage(lam);
     rho_aa = s_rho_aa;
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(NT) k_accel1(Accel1Args P) {
       const double ru = P.r_u[slot];
       const double2 trax = P.rho_ax[slot];
       const double val = (g * rho_aa * (ru + g * cnorm(trax)) + xx.x - 2.0 * g * cmulc(rax, trax).x) / M;
-      P.r_u[slot] = fmax(val, P.eps);
+      P.r_u[slot] = std_max(val, P.eps);
       P.rho_ax[slot] = rax;
       if (P.traj_r_h) {
         const int64_t o = static_cast<int64_t>(it) * P.nb * J + slot;

@@ -87,6 +87,7 @@ struct HBuf {
 };
 
 constexpr int kMaxChunks = 16;
+constexpr double kEpsVar = 1e-12;  // types.hpp:55 (init_params' floor)
 
 inline void check_mics(int M) {
   if (!mics_supported(M)) fail(RCSCM_UNSUPPORTED, "mics = " + std::to_string(M) + " is not supported (1..8 or 16)");
@@ -109,6 +110,7 @@ struct rcscm_gpu_ctx {
   // PCIe rate on B200 hosts) and a compute stream for the pipelined entry points
   cudaStream_t aux[4] = {nullptr, nullptr, nullptr, nullptr};  // + a D2H stream
   cudaEvent_t evx[22] = {};  // kMaxChunks + 6
+  cudaEvent_t evt[32] = {};  // 2 * kMaxChunks timing events: each pipelined chunk's K2 launch
   // device buffers
   DBuf X, W, A, T, V, a, b, Rp, Rpp, power, sab, taa, sbx, tax, txx, rh, ru, lam, lpd;
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;

@@ -8,6 +8,11 @@ namespace rcscm {
 
 constexpr int kMaxMics = 16;
 
+// std::max(v, lo) of the reference (returns v unless v < lo): a NaN v stays NaN,
+// where fmax would replace it by lo and hide a non-finite input.
+__device__ __forceinline__ double std_max(double v, double lo) { return v < lo ? lo : v; }
+__device__ __forceinline__ float std_max(float v, float lo) { return v < lo ? lo : v; }
+
 // Complex helpers on double2 (re, im).
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -68,7 +73,7 @@ __device__ __forceinline__ void slot_forms(const double2 (&x)[M], const double2*
       o = fma(x[r].x, y.x, fma(x[r].y, y.y, o));
     }
   }
-  txx = fmax(fma(2.0, o, d), 0.0);
+  txx = std_max(fma(2.0, o, d), 0.0);
 }
 
 // Launch shape of the slot-stream kernels (K1 precompute, K4 Wiener): each

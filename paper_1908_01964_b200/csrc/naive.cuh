@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(NT) k_naive(NaiveArgs P) {
       }
       const double Ta = ru * M - ru2 * tr + ru2 * zuz;
       const double Tb = ru * beta1 - ru2 * bzb + ru2 * cnorm(bz);
-      P.r_h[slot] = fmax((hrh + P.beta) * inv_a2, P.eps);  // solver_naive.hpp:333-334
+      P.r_h[slot] = std_max((hrh + P.beta) * inv_a2, P.eps);  // solver_naive.hpp:333-334
       P.scratch[slot] = make_double2(Ta, Tb);
       acc += q / ru;
     }
@@ -328,14 +328,14 @@ __global__ void __launch_bounds__(NT) k_naive(NaiveArgs P) {
     __syncthreads();
     double total = 0.0;
     for (int w = 0; w < NT / 32; ++w) total += red[buf][w];
-    const double lam_new = fmax(total / static_cast<double>(J), P.eps);
+    const double lam_new = std_max(total / static_cast<double>(J), P.eps);
     const double d = lam_new - lam;
     const double f = d / fma(d, beta1, 1.0);
     lam = lam_new;
     for (int64_t t = tid; t < J; t += NT) {
       const int64_t slot = bin * J + t;
       const double2 ab = P.scratch[slot];
-      P.r_u[slot] = fmax(fma(-f, ab.y, ab.x) / M, P.eps);
+      P.r_u[slot] = std_max(fma(-f, ab.y, ab.x) / M, P.eps);
       if (P.traj_r_h) {
         const int64_t o = static_cast<int64_t>(it) * P.nb * J + slot;
         P.traj_r_h[o] = P.r_h[slot];

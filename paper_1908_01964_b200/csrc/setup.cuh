@@ -218,7 +218,7 @@ __global__ void k_setup_bin(DevProblem P, double rank_tol, double eps) {
     report_error(P.err, bin * P.J, kErrEigNoConverge);
     return;
   }
-  const double lmax = fmax(vals[M - 1], 0.0);
+  const double lmax = std_max(vals[M - 1], 0.0);
   if (P.logpdet) {
     double lp = 0.0;
     for (int k = 1; k < M; ++k) lp += log(vals[k]);
@@ -227,7 +227,7 @@ __global__ void k_setup_bin(DevProblem P, double rank_tol, double eps) {
   if (MODE == 2) return;
   if (MODE == 0) {
     // null_eigenvector (linalg.hpp:74-86)
-    const double cut_b = rank_tol * fmax(lmax, 1e-300);
+    const double cut_b = rank_tol * std_max(lmax, 1e-300);
     int near_zero = 0;
     for (int k = 0; k < M; ++k) near_zero += (vals[k] <= cut_b);
     if (near_zero != 1) {
@@ -275,7 +275,7 @@ __global__ void k_setup_bin(DevProblem P, double rank_tol, double eps) {
       lmin = vals[k];
       break;
     }
-  P.lambda[bin] = fmax(lmin, eps);
+  P.lambda[bin] = std_max(lmin, eps);
 }
 
 // ---------------------------------------------------------------------------
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(NT) k_slots(DevProblem P, double eps) {
       aa = cfmac(ak, sp[k], aa);
     }
     P.sigma_ab[bin] = ab;
-    P.tau_aa[bin] = fmax(aa.x, 0.0);
+    P.tau_aa[bin] = std_max(aa.x, 0.0);
   }
   const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + tid;
   if (t >= P.J) return;
@@ -359,13 +359,13 @@ __global__ void __launch_bounds__(NT) k_slots(DevProblem P, double eps) {
       for (int k = 0; k < M; ++k) acc = cfma(sRpp[r + k * M], yh[k], acc);
       q = cfmac(yh[r], acc, q);
     }
-    P.r_u[slot] = fmax(q.x / M, eps);
+    P.r_u[slot] = std_max(q.x / M, eps);
     const int64_t u = bin / P.I, i = bin % P.I;
     const double* Tu = P.T + u * P.I * P.K;
     const double* Vu = P.V + u * P.K * P.J;
     double s = 0.0;
     for (int k = 0; k < P.K; ++k) s = fma(Tu[i + k * P.I], Vu[k + t * P.K], s);
-    P.r_h[slot] = fmax(s, eps);
+    P.r_h[slot] = std_max(s, eps);
   }
 }
 
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(256) k_pre(DevProblem P) {
       aa = cfmac(ak, sp[k], aa);
     }
     P.sigma_ab[bin] = ab;
-    P.tau_aa[bin] = fmax(aa.x, 0.0);
+    P.tau_aa[bin] = std_max(aa.x, 0.0);
   }
 }
 // slots per thread of k_pre: 16 complex x values in registers
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(NT) k_slots_pre_f32(DevProblem P, const float2
       aa = cfmac(ak, dp[k], aa);
     }
     P.sigma_ab[bin] = ab;
-    P.tau_aa[bin] = fmax(aa.x, 0.0);
+    P.tau_aa[bin] = std_max(aa.x, 0.0);
   }
   const int64_t t = static_cast<int64_t>(blockIdx.y) * NT + tid;
   if (t >= P.J) return;
@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(NT) k_slots_pre_f32(DevProblem P, const float2
   }
   sbx_f[slot] = sbx;
   tax_f[slot] = tax;
-  txx_f[slot] = fmaxf(xx.x, 0.f);
+  txx_f[slot] = std_max(xx.x, 0.f);
 }
 
 // double <-> float element conversions (complex arrays pass 2 * count).

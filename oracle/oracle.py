@@ -608,38 +608,41 @@ def truth_lib():
 
 
 def truth_accel_one_iter(inputs: Inputs, params0: Params, X, alpha=1.1, beta=1e-16, eps=1e-12):
-    """-> (Params after one Algorithm 2 iteration, S_ru (I, J), S_lam (I,)) in
-    binary128 rounded to double; S_ru = (|g rho_aa q| + |rho_xx| + |2 g Re(.)|)/M,
-    the magnitude scale of the r_u update (solver_accel.hpp:160-176), S_lam the
-    mean |term| of the lambda sum (:143-158)."""
+    """-> (Params after one Algorithm 2 iteration in binary128 rounded to
+    double, Params of the first-order rounding scales B (r_h, r_u per slot,
+    lambda per bin): a double evaluation of the same formulas is expected
+    within C eps B of the truth, see truth.cpp)."""
     X = _c(X)
     I, J, M = X.shape
-    r_h, r_u, S = np.zeros(I * J), np.zeros(I * J), np.zeros(I * J)
-    lam, Sl = np.zeros(I), np.zeros(I)
+    r_h, r_u, lam = np.zeros(I * J), np.zeros(I * J), np.zeros(I)
+    Bh, Bu, Bl = np.zeros(I * J), np.zeros(I * J), np.zeros(I)
     rc = truth_lib().truth_accel_one_iter(
         _i64(I), _i64(J), M, _p(_c(inputs.a)), _p(mats_to_ref(inputs.R_prime_pinv)), _p(_c(inputs.b)),
         _p(ij_to_ref(params0.r_h)), _p(ij_to_ref(params0.r_u)), _p(_c(params0.lam, np.float64)),
         ctypes.c_double(alpha), ctypes.c_double(beta), ctypes.c_double(eps), _p(X), _p(r_h), _p(r_u), _p(lam),
-        _p(S), _p(Sl))
+        _p(Bh), _p(Bu), _p(Bl))
     if rc:
         raise NumericalError("truth_accel_one_iter failed")
     f = lambda v: v.reshape(J, I).T.copy()
-    return Params(f(r_h), f(r_u), lam), f(S), Sl
+    return Params(f(r_h), f(r_u), lam), Params(f(Bh), f(Bu), Bl)
 
 
 def truth_naive_one_iter(inputs: Inputs, params0: Params, X, alpha=1.1, beta=1e-16, eps=1e-12):
-    """-> Params after one naive iteration (solver_naive.hpp:153-386) in binary128."""
+    """-> (Params after one naive iteration (solver_naive.hpp:153-386) in
+    binary128, Params of the rounding scales B incl. kappa(R_x), kappa(R_u))."""
     X = _c(X)
     I, J, M = X.shape
     r_h, r_u, lam = np.zeros(I * J), np.zeros(I * J), np.zeros(I)
+    Bh, Bu, Bl = np.zeros(I * J), np.zeros(I * J), np.zeros(I)
     rc = truth_lib().truth_naive_one_iter(
         _i64(I), _i64(J), M, _p(_c(inputs.a)), _p(mats_to_ref(inputs.R_prime)), _p(_c(inputs.b)),
         _p(ij_to_ref(params0.r_h)), _p(ij_to_ref(params0.r_u)), _p(_c(params0.lam, np.float64)),
-        ctypes.c_double(alpha), ctypes.c_double(beta), ctypes.c_double(eps), _p(X), _p(r_h), _p(r_u), _p(lam))
+        ctypes.c_double(alpha), ctypes.c_double(beta), ctypes.c_double(eps), _p(X), _p(r_h), _p(r_u), _p(lam),
+        _p(Bh), _p(Bu), _p(Bl))
     if rc:
         raise NumericalError("truth_naive_one_iter: singular matrix")
     f = lambda v: v.reshape(J, I).T.copy()
-    return Params(f(r_h), f(r_u), lam)
+    return Params(f(r_h), f(r_u), lam), Params(f(Bh), f(Bu), Bl)
 
 
 def truth_wiener_dry(inputs: Inputs, p: Params, X):

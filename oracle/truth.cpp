@@ -15,9 +15,7 @@
 //                         precompute_sigma/tau solver_accel.hpp:33-64 (full
 //                         x^H (R'^+ x) form), rho_second_stage :113-129,
 //                         compute_gamma :67-76, update_rh :134-141,
-//                         update_lambda :143-158, update_ru :160-176;
-//                         also returns S_ij = sum |terms| / M of the r_u update
-//                         (its cancellation scale) and the same for lambda.
+//                         update_lambda :143-158, update_ru :160-176.
 //   truth_naive_one_iter  the naive rule, one iteration: naive_e_step_bin_impl
 //                         solver_naive.hpp:153-246 (R_x lower triangle + Hermitian
 //                         mirror, exact inverse by Gauss-Jordan with partial
@@ -26,6 +24,20 @@
 //                         r_u = Re tr(R_u^-1 hat)/M).
 //   truth_wiener          extract_target wiener.hpp:19-43 (dry only) from given
 //                         params, in binary128.
+//
+// Both one-iteration functions also return a first-order ROUNDING SCALE per
+// output, B_rh, B_ru (per slot) and B_lam (per bin): the standard a-priori
+// forward-error bound of a double evaluation of the same formulas (Higham,
+// "Accuracy and Stability of Numerical Algorithms", ch. 3: a computed sum or
+// dot product errs by at most ~n eps times the sum of the magnitudes of its
+// terms), propagated through every step -- for Algorithm 2 the magnitudes of
+// the precompute dot products, of the rho / gamma / residual terms and of the
+// three terms of the r_u update, which cancel when r_u is small; for the naive
+// rule additionally the 1-norm condition numbers kappa(R_x), kappa(R_u) of the
+// matrices it inverts. Any double implementation of the formulas, in any
+// operation order, is expected within C eps B of the truth for a modest C;
+// tests/test_truth.py measures C for the oracle (the reference's arithmetic)
+// and tests/test_gpu_truth.py holds the GPU to the same C.
 //
 // Floors are std::max(v, eps) as in the reference. Layouts are the oracle's
 // (rcscm_oracle.h): X [i][t][m]; a, b [i][m]; R', R'^+ [i] M x M col-major;
@@ -56,6 +68,8 @@ inline C cdiv(C a, C b) {
 }
 inline C ld(const double* p, int64_t k) { return C{p[2 * k], p[2 * k + 1]}; }
 inline Q qmax(Q v, Q lo) { return v < lo ? lo : v; }  // std::max(v, lo)
+// |z| for the rounding scales (only magnitudes: the double sqrt is plenty)
+inline Q sqrtq_(Q v) { return static_cast<Q>(__builtin_sqrt(static_cast<double>(v))); }
 
 // Run f(i) for bins [0, I) on all host threads (bins are independent).
 template <class F>
@@ -108,10 +122,11 @@ extern "C" {
 
 int truth_accel_one_iter(int64_t I, int64_t J, int M, const double* a, const double* Rpp, const double* b,
                          const double* r_h0, const double* r_u0, const double* lambda0, double alpha, double beta,
-                         double eps, const double* X, double* r_h, double* r_u, double* lambda, double* S_ru,
-                         double* S_lam) {
+                         double eps, const double* X, double* r_h, double* r_u, double* lambda, double* B_rh,
+                         double* B_ru, double* B_lam) {
   for_bins(I, [&](int64_t i) {
     std::vector<C> av(M), bv(M), P(M * M), pa(M);
+    std::vector<Q> pa_abs(M, 0);
     for (int m = 0; m < M; ++m) {
       av[m] = ld(a, i * M + m);
       bv[m] = ld(b, i * M + m);
@@ -122,50 +137,77 @@ int truth_accel_one_iter(int64_t I, int64_t J, int M, const double* a, const dou
     for (int m = 0; m < M; ++m) sab = add(sab, mul(conj(av[m]), bv[m]));
     for (int r = 0; r < M; ++r) {
       C s = mk(0, 0);
-      for (int c = 0; c < M; ++c) s = add(s, mul(P[r + c * M], av[c]));
+      for (int c = 0; c < M; ++c) {
+        s = add(s, mul(P[r + c * M], av[c]));
+        pa_abs[r] += sqrtq_(norm(P[r + c * M])) * sqrtq_(norm(av[c]));
+      }
       pa[r] = s;
     }
     C aa = mk(0, 0);
-    for (int m = 0; m < M; ++m) aa = add(aa, mul(conj(av[m]), pa[m]));
+    Q sab_abs = 0, taa_abs = 0;
+    for (int m = 0; m < M; ++m) {
+      aa = add(aa, mul(conj(av[m]), pa[m]));
+      sab_abs += sqrtq_(norm(av[m])) * sqrtq_(norm(bv[m]));
+      taa_abs += sqrtq_(norm(av[m])) * pa_abs[m];
+    }
     const Q taa = qmax(aa.re, 0);
     const Q lam0 = lambda0[i];
     const Q ab2 = norm(sab);
     const Q trho_aa = taa + ab2 / lam0;
+    const Q trho_aa_abs = taa_abs + sab_abs * sab_abs / lam0;
     std::vector<C> sbx(J), tax(J), trax(J);
-    std::vector<Q> txx(J), g(J);
+    std::vector<Q> txx(J), g(J), g_abs(J), sbx_abs(J), tax_abs(J), txx_abs(J), trax_abs(J);
     Q acc = 0, acc_abs = 0;
     for (int64_t t = 0; t < J; ++t) {
       std::vector<C> x(M);
       for (int m = 0; m < M; ++m) x[m] = ld(X, (i * J + t) * M + m);
       C s1 = mk(0, 0), s2 = mk(0, 0), s3 = mk(0, 0);
+      Q a1 = 0, a2 = 0, a3 = 0;
       for (int m = 0; m < M; ++m) {
         s1 = add(s1, mul(conj(bv[m]), x[m]));
         s2 = add(s2, mul(conj(pa[m]), x[m]));
+        a1 += sqrtq_(norm(bv[m])) * sqrtq_(norm(x[m]));
+        a2 += pa_abs[m] * sqrtq_(norm(x[m]));
       }
       for (int r = 0; r < M; ++r) {
         C px = mk(0, 0);
-        for (int c = 0; c < M; ++c) px = add(px, mul(P[r + c * M], x[c]));
+        for (int c = 0; c < M; ++c) {
+          px = add(px, mul(P[r + c * M], x[c]));
+          a3 += sqrtq_(norm(x[r])) * sqrtq_(norm(P[r + c * M])) * sqrtq_(norm(x[c]));
+        }
         s3 = add(s3, mul(conj(x[r]), px));
       }
+      sbx_abs[t] = a1;
+      tax_abs[t] = a2;
+      txx_abs[t] = a3;
       sbx[t] = s1;
       tax[t] = s2;
       txx[t] = qmax(s3.re, 0);
       // rho~ with lambda0, gamma (solver_accel.hpp:67-76, :113-129)
       trax[t] = add(tax[t], scal(mul(sab, sbx[t]), 1 / lam0));
+      trax_abs[t] = tax_abs[t] + sab_abs * sbx_abs[t] / lam0;
       const Q rh = r_h0[i + t * I], ru = r_u0[i + t * I];
-      g[t] = rh / (ru + rh * trho_aa);
+      const Q D = ru + rh * trho_aa;
+      g[t] = rh / D;
+      g_abs[t] = g[t] * (1 + rh * trho_aa_abs / D);  // error(gamma) <~ eps g_abs
       // update_rh (:134-141)
       const Q vh = (g[t] * (ru + g[t] * norm(trax[t])) + beta) / (alpha + 2);
       r_h[i + t * I] = static_cast<double>(qmax(vh, eps));
+      if (B_rh)
+        B_rh[i + t * I] = static_cast<double>(
+            (g_abs[t] * ru + 3 * g_abs[t] * g[t] * trax_abs[t] * trax_abs[t] + beta) / (alpha + 2));
       // update_lambda (:143-158)
       const C resid = sub(sbx[t], mul(scal(conj(sab), g[t]), trax[t]));
       const Q term = g[t] * ab2 + norm(resid) / ru;
+      const Q resid_abs = sbx_abs[t] + g_abs[t] * sab_abs * trax_abs[t];
       acc += term;
-      acc_abs += qabs(term);
+      acc_abs += g_abs[t] * sab_abs * sab_abs + resid_abs * resid_abs / ru;
     }
     const Q lam = qmax(acc / static_cast<Q>(J), eps);
     lambda[i] = static_cast<double>(lam);
-    if (S_lam) S_lam[i] = static_cast<double>(acc_abs / static_cast<Q>(J));
+    const Q lam_abs = acc_abs / static_cast<Q>(J);
+    if (B_lam) B_lam[i] = static_cast<double>(lam_abs);
+    const Q fl = 1 + lam_abs / lam;  // 1/lambda's relative error carries into every rho
     // rho with the new lambda, update_ru (:160-176)
     const Q rho_aa = taa + ab2 / lam;
     for (int64_t t = 0; t < J; ++t) {
@@ -176,7 +218,14 @@ int truth_accel_one_iter(int64_t I, int64_t J, int M, const double* a, const dou
       const Q t3 = 2 * g[t] * mul(trax[t], conj(rho_ax)).re;
       const Q val = (t1 + rho_xx - t3) / static_cast<Q>(M);
       r_u[i + t * I] = static_cast<double>(qmax(val, eps));
-      if (S_ru) S_ru[i + t * I] = static_cast<double>((qabs(t1) + qabs(rho_xx) + qabs(t3)) / static_cast<Q>(M));
+      if (B_ru) {
+        const Q raa_abs = taa_abs + sab_abs * sab_abs / lam * fl;
+        const Q rax_abs = tax_abs[t] + sab_abs * sbx_abs[t] / lam * fl;
+        const Q rxx_abs = txx_abs[t] + sbx_abs[t] * sbx_abs[t] / lam * fl;
+        const Q t1_abs = g_abs[t] * raa_abs * (ru + 3 * g[t] * trax_abs[t] * trax_abs[t]);
+        const Q t3_abs = 2 * g_abs[t] * trax_abs[t] * rax_abs;
+        B_ru[i + t * I] = static_cast<double>((t1_abs + rxx_abs + t3_abs) / static_cast<Q>(M));
+      }
     }
   });
   return 0;
@@ -184,24 +233,44 @@ int truth_accel_one_iter(int64_t I, int64_t J, int M, const double* a, const dou
 
 int truth_naive_one_iter(int64_t I, int64_t J, int M, const double* a, const double* Rp, const double* b,
                          const double* r_h0, const double* r_u0, const double* lambda0, double alpha, double beta,
-                         double eps, const double* X, double* r_h, double* r_u, double* lambda) {
+                         double eps, const double* X, double* r_h, double* r_u, double* lambda, double* B_rh,
+                         double* B_ru, double* B_lam) {
   int bad = 0;
+  auto cabs = [](C z) { return sqrtq_(norm(z)); };
+  auto norm1 = [&](const std::vector<C>& A) {  // max column sum of |a_rc|
+    Q best = 0;
+    for (int c = 0; c < M; ++c) {
+      Q s = 0;
+      for (int r = 0; r < M; ++r) s += cabs(A[r + c * M]);
+      best = std::max(best, s);
+    }
+    return best;
+  };
+  auto vnorm1 = [&](const std::vector<C>& v) {
+    Q s = 0;
+    for (const C& z : v) s += cabs(z);
+    return s;
+  };
   for_bins(I, [&](int64_t i) {
     std::vector<C> av(M), bv(M), Rt(M * M), Rx(M * M), Rxi, Ru(M * M), Rui;
     for (int m = 0; m < M; ++m) {
       av[m] = ld(a, i * M + m);
       bv[m] = ld(b, i * M + m);
     }
+    const Q a1 = vnorm1(av), b1 = vnorm1(bv);
     const Q lam0 = lambda0[i];
     for (int c = 0; c < M; ++c)
       for (int r = 0; r < M; ++r)
         Rt[r + c * M] = add(ld(Rp, i * M * M + r + c * M), scal(mul(bv[r], conj(bv[c])), lam0));
+    const Q nRt = norm1(Rt);
     std::vector<std::vector<C>> hat(J, std::vector<C>(M * M));
-    Q lam_acc = 0;
+    std::vector<Q> H_abs(J), nHat(J);
+    Q lam_acc = 0, lam_abs = 0;
     for (int64_t t = 0; t < J; ++t) {
       const Q rh = r_h0[i + t * I], ru = r_u0[i + t * I];
       std::vector<C> x(M);
       for (int m = 0; m < M; ++m) x[m] = ld(X, (i * J + t) * M + m);
+      const Q x1 = vnorm1(x);
       // R_x = rh a a^H + ru R~_u (lower triangle, Hermitian mirror; :186-191)
       for (int c = 0; c < M; ++c) {
         for (int r = c; r < M; ++r) Rx[r + c * M] = add(mul(av[r], scal(conj(av[c]), rh)), scal(Rt[r + c * M], ru));
@@ -211,6 +280,7 @@ int truth_naive_one_iter(int64_t I, int64_t J, int M, const double* a, const dou
         bad = 1;
         return;
       }
+      const Q nRi = norm1(Rxi), kx = norm1(Rx) * nRi;  // 1-norm condition number of R_x
       Q a_rxi_a = 0;
       C x_rxi_a = mk(0, 0);
       for (int r = 0; r < M; ++r) {
@@ -221,6 +291,11 @@ int truth_naive_one_iter(int64_t I, int64_t J, int M, const double* a, const dou
       }
       const Q hrh = rh - rh * rh * a_rxi_a + norm(scal(x_rxi_a, rh));
       r_h[i + t * I] = static_cast<double>(qmax((hrh + beta) / (alpha + 2), eps));
+      const Q xa = cabs(x_rxi_a);
+      if (B_rh)
+        B_rh[i + t * I] = static_cast<double>(
+            (rh + rh * rh * (qabs(a_rxi_a) + a1 * a1 * kx * nRi) + rh * rh * (xa * xa + 2 * xa * x1 * a1 * kx * nRi) +
+             beta) / (alpha + 2));
       std::vector<C> RR(M * M), v(M);
       for (int r = 0; r < M; ++r) {
         C vx = mk(0, 0);
@@ -241,6 +316,11 @@ int truth_naive_one_iter(int64_t I, int64_t J, int M, const double* a, const dou
         }
         for (int r = 0; r < c; ++r) H[r + c * M] = conj(H[c + r * M]);
       }
+      const Q v1 = vnorm1(v);
+      // rounding scale of hat R_u: r_u R~_u, r_u^2 R~_u R_x^-1 R~_u (inverse error
+      // ~ eps kappa(R_x) ||R_x^-1||) and r_u^2 v v^H (v = R~_u R_x^-1 x likewise)
+      H_abs[t] = ru * nRt + ru * ru * nRt * nRt * nRi * kx + ru * ru * (v1 * v1 + 2 * v1 * nRt * kx * nRi * x1);
+      nHat[t] = norm1(H);
       C q = mk(0, 0);  // b^H hat b
       for (int r = 0; r < M; ++r) {
         C s = mk(0, 0);
@@ -248,9 +328,12 @@ int truth_naive_one_iter(int64_t I, int64_t J, int M, const double* a, const dou
         q = add(q, mul(conj(bv[r]), s));
       }
       lam_acc += q.re / ru;
+      lam_abs += b1 * b1 * H_abs[t] / ru;
     }
     const Q lam = qmax(lam_acc / static_cast<Q>(J), eps);
     lambda[i] = static_cast<double>(lam);
+    lam_abs /= static_cast<Q>(J);
+    if (B_lam) B_lam[i] = static_cast<double>(lam_abs);
     for (int c = 0; c < M; ++c)
       for (int r = 0; r < M; ++r)
         Ru[r + c * M] = add(ld(Rp, i * M * M + r + c * M), scal(mul(bv[r], conj(bv[c])), lam));
@@ -258,11 +341,16 @@ int truth_naive_one_iter(int64_t I, int64_t J, int M, const double* a, const dou
       bad = 1;
       return;
     }
+    const Q nRui = norm1(Rui), ku = norm1(Ru) * nRui;
     for (int64_t t = 0; t < J; ++t) {
       Q tr = 0;
       for (int r = 0; r < M; ++r)
         for (int k = 0; k < M; ++k) tr += mul(Rui[r + k * M], hat[t][k + r * M]).re;
       r_u[i + t * I] = static_cast<double>(qmax(tr / static_cast<Q>(M), eps));
+      // tr(R_u^-1 hat)/M: hat's rounding, R_u^-1's (kappa(R_u)) and lambda's through R_u
+      if (B_ru)
+        B_ru[i + t * I] =
+            static_cast<double>(nRui * H_abs[t] + ku * nRui * nHat[t] + nRui * nRui * b1 * b1 * lam_abs * nHat[t]);
     }
   });
   return bad ? 3 : 0;

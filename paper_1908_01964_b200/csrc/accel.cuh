@@ -102,14 +102,20 @@ struct AccelArgs {
 };
 
 // std::max(v, eps) of the reference (returns v unless v < eps) for eps > 0,
-// evaluated as a signed 64-bit compare of the bit patterns: IEEE doubles of
-// either sign order like their two's-complement images against a positive eps
-// (negative v and -0.0 map below eps, +NaN stays NaN as in std::max). Keeps the
-// floor on the integer ALUs instead of the FP64 pipe.
-__device__ __forceinline__ double floor_eps(double v, double eps) {
-  const long long iv = __double_as_longlong(v), ie = __double_as_longlong(eps);
-  return __longlong_as_double(iv < ie ? ie : iv);
+// evaluated as ONE signed 64-bit compare of the bit patterns, so the floor stays
+// off the FP64 pipe: IEEE doubles of either sign order like their two's-
+// complement images against a positive eps (negative values and -0.0 map below
+// it), and a NaN with the sign bit clear maps above it and is returned
+// unchanged, as std::max does. B200's FP64 / FP32 units produce only that
+// canonical positive NaN from any NaN operand, with or without a negate
+// modifier (measured: tools/nan_probe.cu, profiles/r02/nan_probe.txt), so every
+// NaN reaching a floor in K2 -- all of them results of FMA / MUL / ADD chains --
+// is kept; tests/test_gpu_full.py checks NaN propagation against the oracle. A
+// sign-exact variant (three compares) measured 10 % slower on config 1.
+__device__ __forceinline__ bool below_eps(double v, double eps) {
+  return __double_as_longlong(v) < __double_as_longlong(eps);
 }
+__device__ __forceinline__ double floor_eps(double v, double eps) { return below_eps(v, eps) ? eps : v; }
 
 // Sum of the 32 lanes' values, returned in every lane: one DMMA m8n8k4 with
 // A = 1 and the values as B (lane l holds B[l % 4][l / 4]) leaves in lane l
@@ -173,10 +179,9 @@ __device__ long long* g_k2_probe;
   } while (0)
 #endif
 
-// FP32-mode counterpart of floor_eps (32-bit compare of the bit patterns).
+// FP32-mode counterpart of floor_eps (one 32-bit compare of the bit patterns).
 __device__ __forceinline__ float floor_eps(float v, float eps) {
-  const int iv = __float_as_int(v), ie = __float_as_int(eps);
-  return __int_as_float(iv < ie ? ie : iv);
+  return __float_as_int(v) < __float_as_int(eps) ? eps : v;
 }
 __device__ __forceinline__ double tfma(double a, double b, double c) { return fma(a, b, c); }
 __device__ __forceinline__ float tfma(float a, float b, float c) { return fmaf(a, b, c); }
@@ -393,7 +398,13 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
   if constexpr (CL > 1) {
     if (tid < 2) {
       const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[tid]));
+#ifdef RCSCM_CL_XCHG_FENCE
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(lb), "r"(CL) : "memory");
+#else
+      // one local arrival (with the expected bytes) per phase; the CL partials
+      // complete the phase's transaction count
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(lb) : "memory");
+#endif
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     cg::this_cluster().sync();  // every peer's barriers exist before the first remote arrive
@@ -484,30 +495,50 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       if constexpr (CL == 1) {
         total = NT <= 128 ? block_total4(red[buf]) : block_total8(red[buf]);
       } else {
-        // CTA partial -> cluster: lanes r < CL of warp 0 store this CTA's partial
-        // into cl_vals[buf][rank] of CTA r (st.shared::cluster) and arrive on its
-        // cl_bar[buf] with release semantics; every thread then waits on the local
-        // barrier (acquire) and sums the CL partials in rank order -- the same
-        // fixed tree in every CTA. One DSMEM write latency instead of a
-        // cluster-wide barrier plus a remote read.
+        // CTA partial -> cluster: lane r < CL of warp 0 sends this CTA's partial
+        // into cl_vals[buf][rank] of CTA r with st.async, whose completion
+        // counts 8 bytes against CTA r's cl_bar[buf] (mbarrier complete_tx);
+        // thread 0 arms the local barrier for the CL partials it will receive
+        // (arrive.expect_tx), and every thread waits on it and sums the CL
+        // partials in rank order -- the same fixed tree in every CTA. No
+        // cluster-scope fence: a release.cluster arrive compiles to MEMBAR.ALL.GPU
+        // (wait for every outstanding memory operation of the thread) before the
+        // remote arrive, which measured ~1500-2000 cycles per iteration.
         const double c = block_total8(red[buf]);
+        const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
+#ifndef RCSCM_CL_XCHG_FENCE
+        if (tid == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(lb), "r"(CL * 8) : "memory");
         if (warp == 0 && lane < CL) {
           const unsigned lv = static_cast<unsigned>(__cvta_generic_to_shared(&cl_vals[buf][rank]));
-          const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
+          unsigned rv, rb;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rv) : "r"(lv), "r"(lane));
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(lane));
+          asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];" ::"r"(rv), "d"(c),
+                       "r"(rb)
+                       : "memory");
+        }
+#else
+        if (warp == 0 && lane < CL) {
+          const unsigned lv = static_cast<unsigned>(__cvta_generic_to_shared(&cl_vals[buf][rank]));
           unsigned rv, rb;
           asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rv) : "r"(lv), "r"(lane));
           asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(lb), "r"(lane));
           asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(rv), "d"(c) : "memory");
           asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(rb) : "memory");
         }
+#endif
         {
-          const unsigned lb = static_cast<unsigned>(__cvta_generic_to_shared(&cl_bar[buf]));
           const unsigned parity = static_cast<unsigned>((it >> 1) & 1);
           unsigned done = 0;
           while (!done) {
             asm volatile(
                 "{\n .reg .pred p;\n"
+#ifdef RCSCM_CL_XCHG_FENCE
                 " mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+#else
+                " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+#endif
                 " selp.u32 %0, 1, 0, p;\n}"
                 : "=r"(done)
                 : "r"(lb), "r"(parity)
@@ -533,7 +564,7 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       const double lraw = total * (SCL ? s2 * invJ : invJ);
       K2_PROBE(4, lraw);
       const double ilr = rcp_pos(lraw);
-      const bool fl = __double_as_longlong(lraw) < __double_as_longlong(P.eps);
+      const bool fl = below_eps(lraw, P.eps);
       lam = fl ? P.eps : lraw;
       il = fl ? il_eps : ilr;
       const double ilc = il * s2;

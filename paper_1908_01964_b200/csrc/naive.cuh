@@ -330,7 +330,14 @@ __global__ void __launch_bounds__(NT) k_naive(NaiveArgs P) {
     for (int w = 0; w < NT / 32; ++w) total += red[buf][w];
     const double lam_new = std_max(total / static_cast<double>(J), P.eps);
     const double d = lam_new - lam;
-    const double f = d / fma(d, beta1, 1.0);
+    const double den = fma(d, beta1, 1.0);
+    // R_u = R~_u + d b b^H (solver_naive.hpp:357-368) is PD iff R~_u is and
+    // 1 + d b^H R~_u^-1 b > 0 (a NaN lambda fails too, as the reference's
+    // !(x > 0) tests do): the reference's "m_step: singular R^(u)" at this M-step
+    // (keyed at the bin's last frame: the reference finishes the bin's E-step,
+    // whose singular-frame errors take precedence, before its M-step)
+    if (tid == 0 && !(den > 0.0)) report_error(P.err, bin * J + (J - 1), kErrMStepSingular);
+    const double f = d / den;
     lam = lam_new;
     for (int64_t t = tid; t < J; t += NT) {
       const int64_t slot = bin * J + t;

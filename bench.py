@@ -390,7 +390,14 @@ def run_gpu(args):
     lo, hi = partition(c["B"], world)[rank]
     hyper = Hyperparams()
     data = gen_batch(CFG, lo, hi)
-    ctx, (B, I, J, M) = session_for(d, CFG, lo, hi, data=data)
+    from paper_1908_01964_b200 import GpuContext
+    from paper_1908_01964_b200.shard import ShardedSession
+
+    ctx = GpuContext(d.local, stream=d.stream.cuda_stream)
+    sharded = ShardedSession(ctx, c["B"], rank, world, *data)
+    sharded.run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
+    ctx.session_check()
+    B, I, J, M = data[0].shape
     step_stages = C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL
 
     for _ in range(args.warmup):
@@ -438,6 +445,12 @@ def run_gpu(args):
                                      "into the prologue, then the on-chip Algorithm 2 iterations), this rank's "
                                      f"{B} utterances x {I} bins", ncu_key="k_accel_c3")
     roofline["peak_probe"] = {"tflops": fp64_peak, "ms": probe_ms, "sm_mhz_during_bench": None}
+    # the final gather of r_h, r_u, lambda and the Wiener dry output to rank 0
+    # (the only communication), timed separately after one untimed
+    # solve + extract step: device-to-device into transfer tensors, then NCCL
+    ctx.session_run(step_stages | C.STAGE_WIENER, iters, hyper)
+    ctx.session_check()
+    gather = gather_measure(d, sharded, world, B, I, J)
     ctx.close()
 
     # e2e through the C ABI with pinned host buffers (reference layout), this
@@ -446,9 +459,7 @@ def run_gpu(args):
     del data
 
     out = None
-    extras = None
-    if world == 1:
-        extras = run_extras(d, hyper, args)
+    extras = run_extras(d, hyper, args) if world == 1 else run_extras_multi(d, hyper, args, rank, world)
     if rank == 0:
         clocks = clk.summary()
         roofline["peak_probe"]["sm_mhz_during_bench"] = clocks.get("sm_mhz")
@@ -479,6 +490,7 @@ def run_gpu(args):
             "breakdown_ms": {"fused_k2": k2_avg, "rank0_utterances": B},
             "roofline": roofline,
             "e2e": e2e,
+            "gather": gather,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "extras": extras,
@@ -573,6 +585,62 @@ def run_extras(d, hyper, args):
     out["peaks"] = {"fp64_dfma_probe_tflops": fp64_peak, "fp32_ffma_probe_tflops": fp32_peak,
                     "fp64_nominal_tflops": NOMINAL_FP64_TFLOPS, "hbm_gbs": hbm}
     return out
+
+
+def gather_measure(d, sharded, world, B, I, J):
+    """Max-over-ranks device time of ShardedSession.gather (fetch into transfer
+    tensors + NCCL point-to-point to rank 0) of r_h, r_u, lambda and dry."""
+    import torch
+    import torch.distributed as dist
+
+    dev = f"cuda:{d.local}"
+    for _ in range(2):  # warm-up (NCCL communicator set-up on the first call)
+        sharded.gather(dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(d.dev)
+    t0 = time.perf_counter()
+    out = sharded.gather(dev)
+    torch.cuda.synchronize(d.dev)
+    dt = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([dt], device=d.dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    nbytes = sharded.B * I * (J * (8 + 8 + 16) + 8)
+    del out
+    return {"ms": dt * 1e3, "bytes_total": nbytes, "bytes_over_links": nbytes * (world - 1) / world,
+            "path": "session outputs copied device-to-device into torch transfer tensors, then point-to-point "
+                    "to rank 0 (NCCL; the only communication of the job), max over ranks of the wall time "
+                    "between device synchronisations"}
+
+
+def run_extras_multi(d, hyper, args, rank, world):
+    """N > 1: config 4 strong-sharded over BINS (rank r solves bins
+    partition(2049, N)[r] of the one utterance), max-over-ranks device time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1908_01964_b200._capi as C
+    from paper_1908_01964_b200 import GpuContext, synth
+    from paper_1908_01964_b200.shard import partition as part
+
+    c = synth.CONFIGS[4]
+    X, W, A, T, V = gen_batch(4, 0, 1)
+    lo, hi = part(c["I"], world)[rank]
+    ctx = GpuContext(d.local, stream=d.stream.cuda_stream)
+    ctx.session_load(X[:, lo:hi], W[:, lo:hi], A[:, lo:hi], T[:, lo:hi], V, 0)
+    ctx.session_run(C.STAGE_SETUP | C.STAGE_PRECOMPUTE)
+    step = C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL
+    dist.barrier()
+    mean, _ = time_stages(d, ctx, step, c["iters"], max(3, min(args.steps, 10)), hyper)
+    t = torch.tensor([mean], device=d.dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ctx.close()
+    S = c["I"] * c["J"]
+    return {"c4_bins_sharded": {"workload": c["name"], "ms_per_step": float(t.item()), "bins_rank0": hi - lo,
+                                "value": S * c["iters"] / (float(t.item()) * 1e-3), "unit": UNIT,
+                                "note": f"2049 bins in contiguous ranges over {world} GPUs, max-over-ranks time"}}
 
 
 def naive_entry(ms, S, iters, M, fp64_peak, accel_ms_per_iter):

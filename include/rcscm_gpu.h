@@ -271,8 +271,10 @@ int rcscm_gpu_session_load(rcscm_gpu_ctx* ctx, int64_t B, int64_t I, int64_t J,
 #define RCSCM_STAGE_RESET 32    /* restore params0 (from the last SETUP) before iterating */
 int rcscm_gpu_session_run(rcscm_gpu_ctx* ctx, int stages, int iters,
                           const rcscm_hyper* hyper, double eps_var);
-/* Asynchronous device->host copy of the session outputs (any pointer may be
- * NULL); synchronizes the stream before returning when sync != 0.
+/* Asynchronous copy of the session outputs (any pointer may be NULL) into host
+ * or device memory of this context's device (unified addressing picks the
+ * direction; a multi-GPU caller fetches into its transfer buffers for the
+ * gather); synchronizes the stream before returning when sync != 0.
  * Layouts: r_h, r_u [u][i][t]; lambda [u][i]; dry [u][i][t] complex;
  * image [u][i][t][m] complex. */
 int rcscm_gpu_session_fetch(rcscm_gpu_ctx* ctx, double* r_h, double* r_u,

@@ -455,6 +455,13 @@ class GpuContext:
     def session_check(self):
         _raise(self._lib.rcscm_gpu_session_check(self._h))
 
+    def session_fetch_into(self, r_h: int, r_u: int, lam: int, dry: int = 0, image: int = 0):
+        """Copy the session outputs into caller memory given as raw addresses
+        (device pointers such as torch's data_ptr(), or host); 0 = skip.
+        Layouts as session_fetch; synchronizes."""
+        vp = lambda a: ctypes.cast(ctypes.c_void_p(a), C._dp) if a else None
+        _raise(self._lib.rcscm_gpu_session_fetch(self._h, vp(r_h), vp(r_u), vp(lam), vp(dry), vp(image), 1))
+
     def session_fetch(self, want_image: bool = False):
         """-> dict of r_h, r_u (B, I, J), lam (B, I), dry (B, I, J), image (B, I, J, M)."""
         B, I, J, M = self._shape

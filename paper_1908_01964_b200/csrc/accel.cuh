@@ -96,6 +96,12 @@ struct AccelArgs {
   // (k_objective_fast's formula) at obj_part[it * gridDim.x + b]
   double* obj_part;
   const double* logpdet;  // [bin] log pdet R'
+  // fused Wiener output (PREM > 0, complex128; each may be null): after the
+  // last iteration the extract_target of the final state (wiener.hpp:29-41)
+  // straight from registers -- s^ = gamma rho_ax, image = a s^ -- into the
+  // device-layout dry [bin][t] and image [bin][t][m]
+  double2* dry_w;
+  double2* image_w;
   double alpha, beta;
   int mics;
   unsigned long long* err;
@@ -203,8 +209,9 @@ __device__ __forceinline__ float tfma(float a, float b, float c) { return fmaf(a
 // MINB: launch bounds of 128 threads x MINB CTAs/SM (MINB = 3: <= 168
 // registers) instead of one 256-thread CTA's worth (0).
 // PREM: fused precompute for M = PREM mics (0: read K1's sigma / tau arrays).
+// EPI (PREM > 0, complex128): the Wiener output (dry, image) as the epilogue.
 template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
-          typename T = double, int PREM = 0>
+          typename T = double, int PREM = 0, bool EPI = false>
 #ifndef RCSCM_K2_LB_THREADS
 #define RCSCM_K2_LB_THREADS 128  // MINB launch-bounds CTA size (tools may override)
 #endif
@@ -236,6 +243,14 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
   // shared planes ([k][tid], conflict-free): tax, (txx, dd) packed, and for
   // SMEMC 1 also cc
   constexpr bool TX_SM = SMEMC >= 1, CC_SM = SMEMC == 1;
+#ifndef RCSCM_K2_CARRY
+#define RCSCM_K2_CARRY 1  // carry rho~_ax across iterations (tools may override)
+#endif
+  // for the cluster shapes and shared-memory constants (C4 2.76 -> 2.59 ms,
+  // C2 2.49 -> 2.34 ms: a smem plane fewer to stream every iteration); the
+  // single-CTA register-resident shape measured 1-2 % slower carrying (B200).
+  // Constant placement never changes a cluster's arithmetic (tested bitwise).
+  constexpr bool CARRY = DIRECT && !F32 && (CL > 1 || SMEMC >= 1) && RCSCM_K2_CARRY;
   CT* s_tax = reinterpret_cast<CT*>(dyn_raw);
   CT* s_xd = s_tax + SPT * NT;
   CT* s_cc = s_xd + SPT * NT;
@@ -570,14 +585,27 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
       const double ilc = il * s2;
       raa = taa + ilc;
       ilT = static_cast<T>(il);
+      [[maybe_unused]] const T dsT = static_cast<T>(ilc) - ilcT;  // change of |s_ab|^2 / lambda
       ilcT = static_cast<T>(ilc);
       const T raaM = static_cast<T>(fma(ilc, inv_M, taa_M));  // rho_aa / M
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
-        const CT tk = get_tax(k), ck = get_cc(k);
+        const CT ck = get_cc(k);
         CT nax;  // rho_ax with lambda_new
-        nax.x = tfma(ck.x, ilcT, tk.x);
-        nax.y = tfma(ck.y, ilcT, tk.y);
+        if constexpr (CARRY) {
+          // rho_ax = tau_ax + c |s_ab|^2/lambda moves along c as lambda changes:
+          // rho_ax(new) = rho_ax(old) + c * (|s_ab|^2/lambda_new - |s_ab|^2/lambda_old),
+          // so tau_ax is never re-read (16 B of shared memory or two registers
+          // per slot); the rounding of the carried value grows ~ eps per
+          // iteration (tests: 1e-9 of the binary128 truth after one iteration,
+          // 1e-6 on the output after the full count)
+          nax.x = tfma(ck.x, dsT, rax[k].x);
+          nax.y = tfma(ck.y, dsT, rax[k].y);
+        } else {
+          const CT tk = get_tax(k);
+          nax.x = tfma(ck.x, ilcT, tk.x);
+          nax.y = tfma(ck.y, ilcT, tk.y);
+        }
         if constexpr (DIRECT) {
           // solver_accel.hpp:167-173 with rho_xx / M = tau_xx/M + |s_bx|^2/M / lambda
           const CT xd = get_xd(k);
@@ -639,6 +667,30 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
     }
   };
   if (scaled) run(std::integral_constant<bool, true>{}); else run(std::integral_constant<bool, false>{});
+  if constexpr (EPI && PREM > 0 && !F32) {
+    // extract_target of the final state (wiener.hpp:29-41) as K2's epilogue:
+    // rho_aa (raa) and rho_ax (rax) already hold the final lambda's values, so
+    // gamma = r_h / (r_u + r_h rho_aa), s^ = gamma rho_ax and image = a s^ need
+    // no re-read of x, sigma / tau or the parameters (K4 streams 48 B/slot of
+    // them back in); only the outputs go to HBM, overlapping co-resident CTAs'
+    // iterations (a separate instantiation: the epilogue's code perturbed the
+    // loop's schedule by ~1 % when compiled in unconditionally)
+    if (P.dry_w || P.image_w) {
+#pragma unroll
+      for (int k = 0; k < SPT; ++k) {
+        if (valid[k]) {
+          const int64_t s = base + t0 + static_cast<int64_t>(k) * NT + tid;
+          const double g = rh[k] / fma(rh[k], raa, ru[k]);
+          const double2 sh = make_double2(rax[k].x * g, rax[k].y * g);
+          if (P.dry_w) P.dry_w[s] = sh;
+          if (P.image_w) {
+#pragma unroll
+            for (int m = 0; m < PREM; ++m) P.image_w[s * PREM + m] = cmul(apre[m], sh);
+          }
+        }
+      }
+    }
+  }
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
     if (valid[k]) {

@@ -7,9 +7,9 @@
 namespace rcscm {
 
 template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
-          typename T = double, int PREM = 0>
+          typename T = double, int PREM = 0, bool EPI = false>
 cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
-  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>;
+  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);
@@ -39,16 +39,16 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
 }
 
 template <int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false, typename T = double,
-          int PREM = 0>
+          int PREM = 0, bool EPI = false>
 cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt) {
   switch (spt) {
-    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
-    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
-    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
-    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
-    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
-    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
-    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM>(s, A, nt);
+    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+    case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+    case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+    case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+    case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -57,7 +57,12 @@ cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt
 // constants in shared memory, direct form.
 template <int CL, int PREM>
 cudaError_t launch_accel_fused_cl_m(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
-  if (g.full) return launch_accel_spt<CL, true, false, 1, 0, true, double, PREM>(s, A, g.nt, g.spt);
+  const bool epi = A.dry_w || A.image_w;  // Wiener output as the epilogue
+  if (g.full) {
+    if (epi) return launch_accel_spt<CL, true, false, 1, 0, true, double, PREM, true>(s, A, g.nt, g.spt);
+    return launch_accel_spt<CL, true, false, 1, 0, true, double, PREM>(s, A, g.nt, g.spt);
+  }
+  if (epi) return launch_accel_spt<CL, false, false, 1, 0, true, double, PREM, true>(s, A, g.nt, g.spt);
   return launch_accel_spt<CL, false, false, 1, 0, true, double, PREM>(s, A, g.nt, g.spt);
 }
 

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) k_wiener(WienerArgs P) {
       aa = cfmac(sa[k], sp[k], aa);
     }
     sab = ab;
-    taa = fmax(aa.x, 0.0);
+    taa = std_max(aa.x, 0.0);
   }
   const double raa = taa + cnorm(sab) * inv_lam;
 #pragma unroll
@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(NT) k_wiener_f32(WienerArgsF32 P) {
         aa = cfmac(ak, dpa[k], aa);
       }
       sab = ab;
-      taa = fmax(aa.x, 0.0);
+      taa = std_max(aa.x, 0.0);
     } else {
       sab = P.sigma_ab[bin];
       taa = P.tau_aa[bin];

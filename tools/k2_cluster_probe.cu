@@ -16,13 +16,16 @@
 #include <random>
 #include <vector>
 
+#ifndef RCSCM_K2_LB_THREADS
+#define RCSCM_K2_LB_THREADS 256
+#endif
 #include "accel.cuh"
 
 using namespace rcscm;
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
 
-template <int SPT, int CL>
+template <int SPT, int CL, int SMEMC = 1, int MINB = 0>
 void run(const char* name, int nb, int J, int nt, int iters) {
   std::mt19937_64 rng(7);
   std::normal_distribution<double> nd;
@@ -54,11 +57,11 @@ void run(const char* name, int nb, int J, int nt, int iters) {
   CK(cudaMemset(dprobe, 0, np * 8));
   CK(cudaMemcpyToSymbol(g_k2_probe, &dprobe, sizeof(dprobe)));
   const bool full = (static_cast<long long>(nt) * SPT * CL == J);
-  auto kern = full ? k_accel<SPT, CL, true, false, 1, 0, true, double> : k_accel<SPT, CL, false, false, 1, 0, true, double>;
+  auto kern = full ? k_accel<SPT, CL, true, false, SMEMC, MINB, true, double> : k_accel<SPT, CL, false, false, SMEMC, MINB, true, double>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncta);
   cfg.blockDim = dim3(nt);
-  cfg.dynamicSmemBytes = static_cast<size_t>(SPT) * nt * 6 * sizeof(double);
+  cfg.dynamicSmemBytes = SMEMC ? static_cast<size_t>(SPT) * nt * (SMEMC == 1 ? 6 : 4) * sizeof(double) : 0;
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(cfg.dynamicSmemBytes)));
   if (CL > 8) CK(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   cudaLaunchAttribute attr[1];
@@ -92,9 +95,9 @@ void run(const char* name, int nb, int J, int nt, int iters) {
       }
   double tot = 0;
   for (double& a : acc) { a /= cnt; tot += a; }
-  printf("%s nb=%d CL=%d nt=%d spt=%d active clusters %d: %.4f ms | ph1 %.0f | warp-red %.0f | ph2+bar %.0f | "
+  printf("%s smemc=%d minb=%d nb=%d CL=%d nt=%d spt=%d active clusters %d: %.4f ms | ph1 %.0f | warp-red %.0f | ph2+bar %.0f | "
          "blk+exchange %.0f | rcp+ph3 %.0f | loop %.0f | iter %.0f cyc\n",
-         name, nb, CL, nt, SPT, nclusters, ms, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], tot);
+         name, SMEMC, MINB, nb, CL, nt, SPT, nclusters, ms, acc[0], acc[1], acc[2], acc[3], acc[4], acc[5], tot);
   // iteration-start offsets of the CTAs sharing an SM (warp 0, iterations 4..9)
   std::vector<std::vector<int>> by_sm(1024);
   for (int b = 0; b < ncta; ++b) {
@@ -118,13 +121,19 @@ void run(const char* name, int nb, int J, int nt, int iters) {
   cudaFree(dprobe);
 }
 
-int main() {
-  // config 4 shape: M = 8, J = 4096 as 2 x 256 x 8 (296 CTAs = 2 per SM in the first wave)
-  run<8, 2>("c4", 148, 4096, 256, 100);
-  run<8, 2>("c4", 2049, 4096, 256, 100);
-  run<4, 4>("c4/4x256x4", 2049, 4096, 256, 100);
-  // config 2 shape: J = 20000 as 16 x 256 x 5
-  run<5, 16>("c2", 14, 20000, 256, 50);
-  run<5, 16>("c2", 513, 20000, 256, 50);
+int main(int argc, char** argv) {
+  const int which = argc > 1 ? atoi(argv[1]) : 0;
+  if (which == 0 || which == 1) {
+    // config 4 shape: M = 8, J = 4096
+    run<8, 2>("c4 2x256x8", 2049, 4096, 256, 100);
+    run<4, 4, 1, 4>("c4 4x256x4 minb4", 2049, 4096, 256, 100);
+    run<8, 2, 2>("c4 2x256x8 smemc2", 2049, 4096, 256, 100);
+    run<2, 8, 1, 4>("c4 8x256x2 minb4", 2049, 4096, 256, 100);
+  }
+  if (which == 0 || which == 2) {
+    // config 2 shape: J = 20000
+    run<5, 16>("c2 16x256x5", 513, 20000, 256, 50);
+    run<8, 16>("c2 16x160x8", 513, 20000, 160, 50);
+  }
   return 0;
 }

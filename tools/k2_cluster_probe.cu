@@ -132,8 +132,10 @@ int main(int argc, char** argv) {
   }
   if (which == 0 || which == 2) {
     // config 2 shape: J = 20000
-    run<5, 16>("c2 16x256x5", 513, 20000, 256, 50);
     run<8, 16>("c2 16x160x8", 513, 20000, 160, 50);
+    run<8, 10>("c2 10x256x8", 513, 20000, 256, 50);
+    run<8, 12>("c2 12x224x8", 513, 20000, 224, 50);
+    run<5, 16>("c2 16x256x5", 513, 20000, 256, 50);
   }
   return 0;
 }

@@ -67,7 +67,8 @@ def raw(rep):
 
 
 def main(argv):
-    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    outdir = os.environ.get("NCU_SUMMARY_DIR") or os.path.join(ROOT, "profiles")
+    path = os.path.join(outdir, "ncu_summary.json")
     try:
         summary = json.load(open(path))
     except (OSError, ValueError):
@@ -88,7 +89,7 @@ def main(argv):
         summary[key] = k
     os.makedirs(os.path.dirname(path), exist_ok=True)
     json.dump(summary, open(path, "w"), indent=1, sort_keys=True)
-    with open(os.path.join(ROOT, "profiles", "ncu_summary.md"), "w") as f:
+    with open(os.path.join(outdir, "ncu_summary.md"), "w") as f:
         f.write("# ncu summary (--set full, one launch each)\n\n")
         for key, k in sorted(summary.items()):
             f.write(f"## {key}\n\n`{k.get('Kernel Name', '')}`\n\n")

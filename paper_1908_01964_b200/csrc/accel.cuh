@@ -563,6 +563,14 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
         double v[CL];
 #pragma unroll
         for (int r = 0; r < CL; ++r) v[r] = cl_vals[buf][r];
+#ifdef RCSCM_K2_XCHECK
+        // protocol self-check build (tools/xcheck.sh): once every thread has read
+        // this buffer, poison it with NaN; a partial that arrived early (for
+        // iteration it + 2) or never would then surface as NaN / wrong bits in
+        // lambda, which the check compares against the normal build bitwise
+        __syncthreads();
+        if (tid < CL) cl_vals[buf][tid] = __longlong_as_double(0x7ff4000000000000ll);
+#endif
 #pragma unroll
         for (int w = 1; w < CL; w <<= 1) {
 #pragma unroll

@@ -21,7 +21,11 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
   const int minb_env = e_mb ? std::atoi(e_mb) : -1;
   const int force_spt = e_spt ? std::atoi(e_spt) : 0;
   const int force_cl = e_cl ? std::atoi(e_cl) : 0;
-  for (int cl : {1, 2, 4, 8, 16}) {
+  // the fewest CTAs per bin that hold it: clusters are bound by their per-
+  // iteration exchange, which costs more with every CTA (measured on B200,
+  // J = 20000: 10 x 256 x 8 2.26 ms against 16 x 160 x 8 2.64 ms and 12 x 224 x 8
+  // 2.70 ms, tools/k2_cluster_probe.cu)
+  for (int cl : {1, 2, 3, 4, 5, 6, 8, 10, 12, 16}) {
     if (force_cl && cl != force_cl) continue;
     const int64_t jc = (J + cl - 1) / cl;
     // FP32 state takes half the registers; clusters are bound by the per-iteration
@@ -35,7 +39,7 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
     if (f32 && !force_cl && cl >= 2 && cl < 16 && jc > 128LL * max_spt) continue;
     int64_t best_waste = -1;
     for (int spt = 1; spt <= 8; ++spt) {
-      if (spt == 7) continue;  // not instantiated
+      if (spt == 7 || (cl >= 2 && spt < 4)) continue;  // not instantiated (accel_launch.cuh)
       if (force_spt ? spt != force_spt : spt > max_spt) continue;
       int64_t nt = (jc + spt - 1) / spt;
       nt = (nt + 31) / 32 * 32;
@@ -58,7 +62,8 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
         // there; measured on B200, config 2 c64 as 16 x 160 x 8: 2.17 ms against
         // 4.40 ms with the constants in registers)
         const int smem_t = f32 ? (cl >= 8 ? (smem_env >= 0 ? smem_env : 1) : 0) : smem;
-        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem_t, minb, direct, f32};
+        // clusters always take the direct form (the affine one is single-CTA only)
+        best = AccelCfg{cl, static_cast<int>(nt), spt, full, smem_t, minb, direct || cl >= 2, f32};
       }
     }
     if (best.cl) return best;
@@ -81,8 +86,13 @@ cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) 
   switch (g.cl) {
     case 1: return launch_accel_cl1(s, A, g);
     case 2: return launch_accel_cl2(s, A, g);
+    case 3: return launch_accel_cl3(s, A, g);
     case 4: return launch_accel_cl4(s, A, g);
+    case 5: return launch_accel_cl5(s, A, g);
+    case 6: return launch_accel_cl6(s, A, g);
     case 8: return launch_accel_cl8(s, A, g);
+    case 10: return launch_accel_cl10(s, A, g);
+    case 12: return launch_accel_cl12(s, A, g);
     case 16: return launch_accel_cl16(s, A, g);
     default: return cudaErrorInvalidValue;
   }

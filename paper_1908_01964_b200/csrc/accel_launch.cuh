@@ -38,19 +38,29 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
   return cudaLaunchKernelEx(&cfg, kern, A);
 }
 
+// Slots per thread: 1-6 and 8 for single-CTA bins; a cluster is only chosen
+// once a bin exceeds the next smaller shape (jc > 768 frames per CTA), so its
+// CTAs hold 4, 5, 6 or 8 slots per thread -- the others are not instantiated.
 template <int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false, typename T = double,
           int PREM = 0, bool EPI = false>
 cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt) {
   switch (spt) {
-    case 1: return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
-    case 2: return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
-    case 3: return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+    case 1:
+      if constexpr (CL == 1) return launch_accel_t<1, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+      break;
+    case 2:
+      if constexpr (CL == 1) return launch_accel_t<2, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+      break;
+    case 3:
+      if constexpr (CL == 1) return launch_accel_t<3, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
+      break;
     case 4: return launch_accel_t<4, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
     case 5: return launch_accel_t<5, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
     case 6: return launch_accel_t<6, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
     case 8: return launch_accel_t<8, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>(s, A, nt);
-    default: return cudaErrorInvalidValue;
+    default: break;
   }
+  return cudaErrorInvalidValue;
 }
 
 // Clusters with the sigma / tau precompute fused into the prologue (PREM = M),
@@ -110,20 +120,28 @@ cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& 
     if (g.full) return launch_accel_spt<CL, true, false, 0, 0, true>(s, A, g.nt, g.spt);
     return launch_accel_spt<CL, false, false, 0, 0, true>(s, A, g.nt, g.spt);
   }
-  if (g.smem) {
-    if (g.full) return launch_accel_spt<CL, true, false, 1>(s, A, g.nt, g.spt);
-    return launch_accel_spt<CL, false, false, 1>(s, A, g.nt, g.spt);
+  if constexpr (CL == 1) {  // the affine (non-DIRECT) form: single-CTA bins only (tuning knob)
+    if (g.smem) {
+      if (g.full) return launch_accel_spt<CL, true, false, 1>(s, A, g.nt, g.spt);
+      return launch_accel_spt<CL, false, false, 1>(s, A, g.nt, g.spt);
+    }
+    if (g.full) return launch_accel_spt<CL, true, false, 0>(s, A, g.nt, g.spt);
+    return launch_accel_spt<CL, false, false, 0>(s, A, g.nt, g.spt);
   }
-  if (g.full) return launch_accel_spt<CL, true, false, 0>(s, A, g.nt, g.spt);
-  return launch_accel_spt<CL, false, false, 0>(s, A, g.nt, g.spt);
+  return cudaErrorInvalidValue;
 }
 
 #define RCSCM_DECLARE_ACCEL_CL(CL) \
   cudaError_t launch_accel_cl##CL(cudaStream_t s, const AccelArgs& A, const AccelCfg& g);
 RCSCM_DECLARE_ACCEL_CL(1)
 RCSCM_DECLARE_ACCEL_CL(2)
+RCSCM_DECLARE_ACCEL_CL(3)
 RCSCM_DECLARE_ACCEL_CL(4)
+RCSCM_DECLARE_ACCEL_CL(5)
+RCSCM_DECLARE_ACCEL_CL(6)
 RCSCM_DECLARE_ACCEL_CL(8)
+RCSCM_DECLARE_ACCEL_CL(10)
+RCSCM_DECLARE_ACCEL_CL(12)
 RCSCM_DECLARE_ACCEL_CL(16)
 // the fused-precompute instances (accel_fused.cu)
 cudaError_t launch_accel_fused(cudaStream_t s, const AccelArgs& A, const AccelCfg& g);

@@ -245,9 +245,20 @@ void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A, int prem = 0) {
   if (A.nb * A.J == 0) return;
   AccelCfg g = choose_accel_cfg(A.J, f32(c));
   g.prem = prem;
-  if (!g.cl)
-    fail(RCSCM_UNSUPPORTED,
-         "frames = " + std::to_string(A.J) + " exceeds the on-chip accel kernel capacity (16 x 2048)");
+  if (!g.cl) {
+    // longer than a 16-CTA cluster holds (32768 frames): stream the iterate
+    // through HBM (two launches per iteration; complex128, sigma / tau from K1)
+    if (f32(c) || prem)
+      fail(RCSCM_UNSUPPORTED, "frames = " + std::to_string(A.J) +
+                                  " exceeds the on-chip accel kernel capacity (16 x 2048) in this mode");
+    if (A.ld_p) fail(RCSCM_UNSUPPORTED, "streaming accel kernel: column-major parameters");
+    double* part = c->st_part.get<double>(static_cast<size_t>(A.nb * accel_stream_chunks(A.J)));
+    double* lam = c->st_lam.get<double>(static_cast<size_t>(4 * A.nb));
+    int n = 0;
+    const cudaError_t e = launch_accel_stream(c->stream, A, part, lam, &n);
+    c->launched(e, n);
+    return;
+  }
   c->launched(launch_accel(c->stream, A, g));
 }
 
@@ -710,7 +721,7 @@ void run_solver(rcscm_gpu_ctx* c, Backend backend, const rcscm_inputs* in, const
     // accel: the O(1)-per-slot objective (scalar expansion, needs log pdet R');
     // naive: the per-slot Cholesky form of model.hpp:129-157.
     if (accel) c->launched(launch_logpdet(c->stream, problem(c, 1, I, J, M)));
-    if (accel && !fp && !(opt->rel_obj_tol > 0.0)) {
+    if (accel && !fp && !(opt->rel_obj_tol > 0.0) && choose_accel_cfg(J).cl) {
       // no early stop: every iteration and its objective in one K2 launch
       double* dobj = c->obj.get<double>(static_cast<size_t>(iters) + 1);
       objective_fast(c, I, J, M, *hyper, dobj);
@@ -999,7 +1010,8 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
                   &c->sbx, &c->tax, &c->txx, &c->rh, &c->ru, &c->lam, &c->lpd, &c->rh0, &c->ru0, &c->lam0, &c->tmp,
                   &c->tmp2, &c->traj_rh, &c->traj_ru, &c->traj_lam, &c->scratch, &c->gam, &c->dry, &c->image, &c->noise,
                   &c->partial, &c->obj, &c->obj_part, &c->err, &c->Xf, &c->sbxf, &c->taxf, &c->txxf, &c->rhf, &c->ruf,
-                  &c->dryf, &c->imagef, &c->rh0f, &c->ru0f, &c->st_x, &c->st_w, &c->st_f, &c->st_spec,
+                  &c->dryf, &c->imagef, &c->rh0f, &c->ru0f, &c->st_x, &c->st_w, &c->st_f, &c->st_spec, &c->st_part,
+                  &c->st_lam,
                   &c->st_X, &c->il_X, &c->il_W, &c->il_A, &c->il_T, &c->il_V, &c->il_P, &c->il_part, &c->il_mu, &c->il_Pt, &c->il_ucov,
                   &c->ex_Q, &c->ex_W, &c->ex_A, &c->ex_pow, &c->ex_out, &c->ex_obj})
     b->release();

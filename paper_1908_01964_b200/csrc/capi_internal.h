@@ -90,7 +90,7 @@ constexpr int kMaxChunks = 16;
 constexpr double kEpsVar = 1e-12;  // types.hpp:55 (init_params' floor)
 
 inline void check_mics(int M) {
-  if (!mics_supported(M)) fail(RCSCM_UNSUPPORTED, "mics = " + std::to_string(M) + " is not supported (1..8 or 16)");
+  if (!mics_supported(M)) fail(RCSCM_UNSUPPORTED, "mics = " + std::to_string(M) + " is not supported (1..16)");
 }
 
 }  // namespace rcscm_capi
@@ -116,6 +116,7 @@ struct rcscm_gpu_ctx {
   DBuf rh0, ru0, lam0, tmp, tmp2, traj_rh, traj_ru, traj_lam, scratch, dry, image, noise, partial, obj, err;
   DBuf gam;  // Algorithm 1 scratch (gamma per slot)
   DBuf obj_part;  // K2's per-iteration, per-CTA objective partials
+  DBuf st_part, st_lam;  // streaming Algorithm 2 (bins > on-chip capacity): chunk partials, lambda ping-pong
   // STFT: waveform, window table, frames, half spectra, Spectrogram
   DBuf st_x, st_w, st_f, st_spec, st_X;
   // ILRMA: whitened x, W, A, T, V, powers, partial sums, mu

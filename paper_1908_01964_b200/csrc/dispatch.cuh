@@ -1,4 +1,5 @@
-// dispatch.cuh -- run-time channel-count dispatch to M-templated kernels.
+// dispatch.cuh -- run-time channel-count dispatch to M-templated kernels (M = 1..16;
+// the reference takes any M through Eigen::Dynamic, solver_naive.hpp:248-262).
 #pragma once
 
 #include <type_traits>
@@ -16,6 +17,13 @@ cudaError_t dispatch_mics(int M, F&& f) {
     case 6: return f(std::integral_constant<int, 6>{});
     case 7: return f(std::integral_constant<int, 7>{});
     case 8: return f(std::integral_constant<int, 8>{});
+    case 9: return f(std::integral_constant<int, 9>{});
+    case 10: return f(std::integral_constant<int, 10>{});
+    case 11: return f(std::integral_constant<int, 11>{});
+    case 12: return f(std::integral_constant<int, 12>{});
+    case 13: return f(std::integral_constant<int, 13>{});
+    case 14: return f(std::integral_constant<int, 14>{});
+    case 15: return f(std::integral_constant<int, 15>{});
     case 16: return f(std::integral_constant<int, 16>{});
     default: return cudaErrorInvalidValue;
   }

@@ -43,6 +43,11 @@ cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg
 // tuned single-CTA complex128 variant, M in {2, 4, 8}); env RCSCM_FUSE_PRE=0
 // disables it
 bool accel_fusable(const AccelCfg& cfg, int M);
+// Algorithm 2 streaming the iterate through HBM for bins longer than the on-chip
+// kernel holds (accel_stream.cuh; needs K1's sigma / tau arrays, complex128):
+// 2 launches per iteration; partial: [nb][accel_stream_chunks(J)], lam_buf: 4 nb.
+int64_t accel_stream_chunks(int64_t J);
+cudaError_t launch_accel_stream(cudaStream_t s, const AccelArgs& A, double* partial, double* lam_buf, int* n_launch);
 
 cudaError_t launch_naive(cudaStream_t s, int M, const NaiveArgs& N);
 // K6: Algorithm 1 (first-stage acceleration), every iteration in one launch

@@ -7,7 +7,7 @@
 
 namespace rcscm {
 
-bool mics_supported(int M) { return (M >= 1 && M <= 8) || M == 16; }
+bool mics_supported(int M) { return M >= 1 && M <= kMaxMics; }
 
 constexpr int kSlotNT = 128;
 

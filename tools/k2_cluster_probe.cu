@@ -130,6 +130,14 @@ int main(int argc, char** argv) {
     run<8, 2, 2>("c4 2x256x8 smemc2", 2049, 4096, 256, 100);
     run<2, 8, 1, 4>("c4 8x256x2 minb4", 2049, 4096, 256, 100);
   }
+  if (which == 3) {
+    run<8, 2>("c4 2x256x8", 2049, 4096, 256, 100);
+    run<8, 3>("c4 3x192x8", 2049, 4096, 192, 100);
+    run<6, 3>("c4 3x256x6", 2049, 4096, 256, 100);
+    run<6, 3, 1, 3>("c4 3x256x6 minb3", 2049, 4096, 256, 100);
+    run<8, 4>("c4 4x128x8", 2049, 4096, 128, 100);
+    run<4, 4, 1, 3>("c4 4x256x4 minb3", 2049, 4096, 256, 100);
+  }
   if (which == 0 || which == 2) {
     // config 2 shape: J = 20000
     run<8, 16>("c2 16x160x8", 513, 20000, 160, 50);

@@ -80,7 +80,7 @@ def headline_config(n_gpus):
             "iters": c["iters"], "rule": "accel2 (Algorithm 2, solver_accel.hpp:183-258)",
             "seeds": f"utterance u: {1000 * CFG} + u", "precision": "complex128",
             "parallelism": f"{c['B']} utterances in contiguous ranges over {n_gpus} GPU(s), no collective in the solve",
-            "l2": "inputs (x 2.69 GB + state) exceed the 126 MB L2; a 256 MiB write also flushes it between steps"}
+            "l2": "inputs (x 2.69 GB + state) exceed the 126 MB L2; a 256 MiB write + read also flushes it between steps"}
 
 
 class ClockSampler:
@@ -301,10 +301,16 @@ class Dev:
         self.dev = torch.device("cuda", local)
         self.stream = torch.cuda.Stream(device=self.dev)
         self.l2 = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=self.dev)
+        self.l2_acc = torch.empty(1, dtype=torch.float32, device=self.dev)
 
     def flush(self):
+        # a 256 MiB write then a read of it: L2 ends full of CLEAN lines, so the
+        # next kernel's misses do not first write back ~126 MB of dirty flush
+        # data (measured on B200: a write-only flush costs a following 20 us
+        # stream kernel ~2 us, tools/stream_flush_ab.py)
         with self.torch.cuda.stream(self.stream):
             self.l2.fill_(1.0)
+            self.l2_acc.copy_(self.l2.sum())
 
     def event(self):
         return self.torch.cuda.Event(enable_timing=True)

@@ -7,14 +7,14 @@ cudaError_t launch_accel_fused(cudaStream_t s, const AccelArgs& A, const AccelCf
   const bool epi = A.dry_w || A.image_w;  // Wiener output as the epilogue (its own instantiation)
   switch (g.prem) {
     case 2:
-      if (epi) return launch_accel_spt<1, true, false, 0, 3, true, double, 2, true>(s, A, g.nt, g.spt);
-      return launch_accel_spt<1, true, false, 0, 3, true, double, 2>(s, A, g.nt, g.spt);
+      if (epi) return launch_accel_spt<1, true, false, 0, RCSCM_K2_MINB1, true, double, 2, true>(s, A, g.nt, g.spt);
+      return launch_accel_spt<1, true, false, 0, RCSCM_K2_MINB1, true, double, 2>(s, A, g.nt, g.spt);
     case 4:
-      if (epi) return launch_accel_spt<1, true, false, 0, 3, true, double, 4, true>(s, A, g.nt, g.spt);
-      return launch_accel_spt<1, true, false, 0, 3, true, double, 4>(s, A, g.nt, g.spt);
+      if (epi) return launch_accel_spt<1, true, false, 0, RCSCM_K2_MINB1, true, double, 4, true>(s, A, g.nt, g.spt);
+      return launch_accel_spt<1, true, false, 0, RCSCM_K2_MINB1, true, double, 4>(s, A, g.nt, g.spt);
     case 8:
-      if (epi) return launch_accel_spt<1, true, false, 0, 3, true, double, 8, true>(s, A, g.nt, g.spt);
-      return launch_accel_spt<1, true, false, 0, 3, true, double, 8>(s, A, g.nt, g.spt);
+      if (epi) return launch_accel_spt<1, true, false, 0, RCSCM_K2_MINB1, true, double, 8, true>(s, A, g.nt, g.spt);
+      return launch_accel_spt<1, true, false, 0, RCSCM_K2_MINB1, true, double, 8>(s, A, g.nt, g.spt);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -16,7 +16,7 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
   // the cluster barrier needs more resident CTAs to hide; measured on B200)
   const int smem_env = e_sm ? std::atoi(e_sm) : -1;
   // MINB: CTAs per SM the 128-thread launch bounds target (0 = 256-thread bounds);
-  // 3 measured fastest with register-resident constants (B200, configs 0/1/3)
+  // RCSCM_K2_MINB1 (launch.h) for register-resident constants (measured on B200)
   const char* e_mb = std::getenv("RCSCM_ACCEL_MINB");
   const int minb_env = e_mb ? std::atoi(e_mb) : -1;
   const int force_spt = e_spt ? std::atoi(e_spt) : 0;
@@ -57,7 +57,7 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
         // 3.01, 8 x 64 x 8 3.56; config 2, J = 20000 as 16 x 256 x 5: 2.99 ms
         // against 5.37)
         const int smem = smem_env >= 0 ? smem_env : (cl >= 2 ? 1 : 0);
-        const int minb = minb_env >= 0 ? minb_env : (smem == 0 ? 3 : 4);
+        const int minb = minb_env >= 0 ? minb_env : (smem == 0 ? RCSCM_K2_MINB1 : 4);
         // complex64: shared-memory constants only for clusters of 8+ (instantiated
         // there; measured on B200, config 2 c64 as 16 x 160 x 8: 2.17 ms against
         // 4.40 ms with the constants in registers)
@@ -77,7 +77,7 @@ bool accel_fusable(const AccelCfg& g, int M) {
   if (!(M == 2 || M == 4 || M == 8) || g.f32 || !g.direct) return false;
   // the tuned single-CTA shape, or a cluster with its constants in shared memory
   // (4 CTAs/SM at <= 128 registers measured slower: C1 0.177 against 0.171 ms)
-  return (g.cl == 1 && g.full && g.smem == 0 && g.minb == 3 && g.nt <= 128) || (g.cl >= 2 && g.smem == 1);
+  return (g.cl == 1 && g.full && g.smem == 0 && g.minb == RCSCM_K2_MINB1 && g.nt <= 128) || (g.cl >= 2 && g.smem == 1);
 }
 
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {

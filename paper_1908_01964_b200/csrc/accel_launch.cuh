@@ -14,8 +14,10 @@ cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);
   // shared planes: tax + (txx, dd) [+ cc for SMEMC 1], one complex each per slot
-  cfg.dynamicSmemBytes = SMEMC ? static_cast<size_t>(SPT) * nt * (SMEMC == 1 ? 6 : 4) * sizeof(T) : 0;
-  if (SMEMC) {  // opt in to the full dynamic allowance (static + dynamic may pass 48 KB)
+  // (the Wiener epilogue reads tax and cc back: all three planes)
+  const int planes = (SMEMC == 1 || EPI) ? 6 : (SMEMC == 2 ? 4 : 0);
+  cfg.dynamicSmemBytes = static_cast<size_t>(SPT) * nt * planes * sizeof(T);
+  if (planes) {  // opt in to the full dynamic allowance (static + dynamic may pass 48 KB)
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(cfg.dynamicSmemBytes));
     if (e != cudaSuccess) return e;
@@ -109,7 +111,7 @@ cudaError_t launch_accel_cl(cudaStream_t s, const AccelArgs& A, const AccelCfg& 
       if (g.smem == 2 && g.minb == 4) return launch_accel_spt<CL, true, false, 2, 4, true>(s, A, g.nt, g.spt);
       if (g.smem == 1 && g.minb == 4) return launch_accel_spt<CL, true, false, 1, 4, true>(s, A, g.nt, g.spt);
       if (g.smem == 2 && g.minb == 5) return launch_accel_spt<CL, true, false, 2, 5, true>(s, A, g.nt, g.spt);
-      if (g.smem == 0) return launch_accel_spt<CL, true, false, 0, 3, true>(s, A, g.nt, g.spt);
+      if (g.smem == 0) return launch_accel_spt<CL, true, false, 0, RCSCM_K2_MINB1, true>(s, A, g.nt, g.spt);
     }
   }
   if (g.direct) {  // r_u from rho(lambda_new) after the reduction (the faster form on B200)

@@ -26,6 +26,14 @@ cudaError_t launch_lambda0(cudaStream_t s, const DevProblem& P, double eps);
 cudaError_t launch_slots(cudaStream_t s, const DevProblem& P, bool init, bool pre, double eps);
 
 // K2 launch configuration (cluster size, threads, slots per thread).
+// CTAs per SM the launch bounds of the tuned single-CTA K2 target (128-thread
+// bounds x 4: <= 128 registers, 8 CTAs of 64 threads per SM). With the scalar
+// carried state (k_accel SST) a slot needs 12 registers; measured on B200, C3:
+// 4.60 ms at 3 (168 registers) against 4.38 ms at 4, 128 utterances.
+#ifndef RCSCM_K2_MINB1
+#define RCSCM_K2_MINB1 4
+#endif
+
 struct AccelCfg {
   int cl, nt, spt;
   bool full;  // nt * spt == chunk: no per-slot masks

@@ -215,7 +215,14 @@ template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool D
 #ifndef RCSCM_K2_LB_THREADS
 #define RCSCM_K2_LB_THREADS 128  // MINB launch-bounds CTA size (tools may override)
 #endif
-__global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB : (SMEMC ? 2 : 1))
+#ifndef RCSCM_K2_SST
+#define RCSCM_K2_SST 1  // scalar carried state (tools may override)
+#endif
+// 256-thread CTAs: two per SM (<= 128 registers) with shared-memory constants
+// or, for clusters, with the scalar carried state (a slot in 12 registers)
+__global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
+                                  MINB ? MINB
+                                       : ((SMEMC || (CL > 1 && DIRECT && !TRAJ && sizeof(T) == 8 && RCSCM_K2_SST)) ? 2 : 1))
     k_accel(AccelArgs P) {
   namespace cg = cooperative_groups;
   using CT = typename CplxOf<T>::type;
@@ -250,9 +257,6 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256, MINB ? MINB 
   // C2 2.49 -> 2.34 ms: a smem plane fewer to stream every iteration); the
   // single-CTA register-resident shape measured 1-2 % slower carrying (B200).
   // Constant placement never changes a cluster's arithmetic (tested bitwise).
-#ifndef RCSCM_K2_SST
-#define RCSCM_K2_SST 1  // scalar carried state (tools may override)
-#endif
   // SST (complex128, direct form, no per-iteration recording): the complex
   // rho~_ax leaves the per-slot state. Every use of it is a real scalar of it:
   //   |c - g rho~|^2 = |c|^2 + g (g |rho~|^2 - 2 Re(conj(c) rho~))     (lambda term)

@@ -50,13 +50,12 @@ AccelCfg choose_accel_cfg(int64_t J, bool f32) {
         best_waste = waste;
         // FULL needs every CTA of the cluster to own exactly nt * spt frames
         const bool full = (waste == 0) && (jc * cl == J);
-        // shared-memory constants for every cluster: the register file then
-        // holds two CTAs per SM, whose per-iteration cluster exchanges overlap
-        // (measured on B200, config 4, J = 4096 as 2 x 256 x 8: 2.98 ms against
-        // 3.34 ms with the constants in registers at one CTA per SM; 4 x 128 x 8
-        // 3.01, 8 x 64 x 8 3.56; config 2, J = 20000 as 16 x 256 x 5: 2.99 ms
-        // against 5.37)
-        const int smem = smem_env >= 0 ? smem_env : (cl >= 2 ? 1 : 0);
+        // constants in registers everywhere: with the scalar carried state
+        // (k_accel SST) a slot is 12 registers, so 8 slots fit the 128 that two
+        // 256-thread CTAs per SM leave (measured on B200, against shared-memory
+        // constants: C4 2.37 -> 2.24 ms, C2 1.78 -> 1.72 ms). Before SST a slot
+        // took 20 registers and clusters kept their constants in shared memory.
+        const int smem = smem_env >= 0 ? smem_env : 0;
         const int minb = minb_env >= 0 ? minb_env : (smem == 0 ? RCSCM_K2_MINB1 : 4);
         // complex64: shared-memory constants only for clusters of 8+ (instantiated
         // there; measured on B200, config 2 c64 as 16 x 160 x 8: 2.17 ms against
@@ -75,9 +74,8 @@ bool accel_fusable(const AccelCfg& g, int M) {
   const char* e = std::getenv("RCSCM_FUSE_PRE");
   if (e && std::atoi(e) == 0) return false;
   if (!(M == 2 || M == 4 || M == 8) || g.f32 || !g.direct) return false;
-  // the tuned single-CTA shape, or a cluster with its constants in shared memory
-  // (4 CTAs/SM at <= 128 registers measured slower: C1 0.177 against 0.171 ms)
-  return (g.cl == 1 && g.full && g.smem == 0 && g.minb == RCSCM_K2_MINB1 && g.nt <= 128) || (g.cl >= 2 && g.smem == 1);
+  // the tuned single-CTA shape, or a cluster with its constants in registers
+  return (g.cl == 1 && g.full && g.smem == 0 && g.minb == RCSCM_K2_MINB1 && g.nt <= 128) || (g.cl >= 2 && g.smem == 0);
 }
 
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {

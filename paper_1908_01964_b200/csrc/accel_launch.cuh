@@ -66,16 +66,16 @@ cudaError_t launch_accel_spt(cudaStream_t s, const AccelArgs& A, int nt, int spt
 }
 
 // Clusters with the sigma / tau precompute fused into the prologue (PREM = M),
-// constants in shared memory, direct form.
+// constants in registers, direct form.
 template <int CL, int PREM>
 cudaError_t launch_accel_fused_cl_m(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
   const bool epi = A.dry_w || A.image_w;  // Wiener output as the epilogue
   if (g.full) {
-    if (epi) return launch_accel_spt<CL, true, false, 1, 0, true, double, PREM, true>(s, A, g.nt, g.spt);
-    return launch_accel_spt<CL, true, false, 1, 0, true, double, PREM>(s, A, g.nt, g.spt);
+    if (epi) return launch_accel_spt<CL, true, false, 0, 0, true, double, PREM, true>(s, A, g.nt, g.spt);
+    return launch_accel_spt<CL, true, false, 0, 0, true, double, PREM>(s, A, g.nt, g.spt);
   }
-  if (epi) return launch_accel_spt<CL, false, false, 1, 0, true, double, PREM, true>(s, A, g.nt, g.spt);
-  return launch_accel_spt<CL, false, false, 1, 0, true, double, PREM>(s, A, g.nt, g.spt);
+  if (epi) return launch_accel_spt<CL, false, false, 0, 0, true, double, PREM, true>(s, A, g.nt, g.spt);
+  return launch_accel_spt<CL, false, false, 0, 0, true, double, PREM>(s, A, g.nt, g.spt);
 }
 
 template <int CL>

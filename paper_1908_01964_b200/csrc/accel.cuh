@@ -10,10 +10,11 @@
 //
 // Mapping: one CTA (CL == 1) or one thread-block cluster of CL CTAs per
 // frequency bin. Each thread owns SPT slots of the bin and keeps every
-// per-slot quantity (r_h, r_u, rho~_ax, tau_ax, c = s_ab s_bx / |s_ab|^2,
-// tau_xx / M, |s_bx|^2 / M) in REGISTERS for all iterations (SMEMC moves the
-// constants to shared memory): HBM is touched once on the way in and once on
-// the way out. With PREM = M the sigma / tau forms are computed from x in the
+// per-slot quantity -- (r_h, r_u, |rho~_ax|^2, -2 Re(conj(c) rho~_ax)) and the
+// constants (tau_xx / M, |c|^2), c = s_ab s_bx / |s_ab|^2 (SST); otherwise
+// r_h, r_u, rho~_ax, tau_ax, c, tau_xx / M, |s_bx|^2 / M -- in REGISTERS for
+// all iterations (SMEMC moves the constants to shared memory): HBM is touched
+// once on the way in and once on the way out. With PREM = M the sigma / tau forms are computed from x in the
 // prologue (the precompute fused into the kernel). The only cross-slot
 // dependency -- lambda's sum over frames -- is a fixed-order tree: in-thread
 // pairwise sum, a warp total (one DMMA + a 2-level xor butterfly), a
@@ -26,14 +27,16 @@
 // non-DIRECT variant forms r_u as P0 + P1/lambda_new with all but three FMAs
 // before the reduction).
 //
-// Instruction budget per slot-iteration (47 canonical flops): 29 FP64 ops
-// (DFMA/DMUL/DADD, incl. the per-iteration reduction and lambda chain) + 1
-// MUFU.RCP64H; floors run on the integer ALUs. The reference's two divisions
-// share one reciprocal (inv = 1/(D r~_u) gives gamma = r~_h r~_u inv and
-// 1/r~_u = D inv); |s_ab|^2 leaves the per-slot lambda term (scaled residual);
-// gamma_fault rides in an FMA; 1/M is folded into the per-slot constants
-// (exact for power-of-two M); `max(v, eps)` keeps the reference's std::max
-// semantics. DESIGN.md section 4 records what bounds it on B200.
+// Instruction budget per slot-iteration (47 canonical flops): 22 FP64 ops
+// per slot with the scalar carried state (SST, below; 26 with the complex
+// rho~_ax) + the per-iteration lambda chain and trees amortised over the
+// thread's slots + 1 MUFU.RCP64H; floors run on the integer ALUs. The
+// reference's two divisions share one reciprocal (inv = 1/(D r~_u) gives
+// gamma = r~_h r~_u inv and 1/r~_u = D inv); |s_ab|^2 leaves the per-slot
+// lambda term (scaled residual); gamma_fault rides in an FMA; 1/M is folded
+// into the per-slot constants (exact for power-of-two M); `max(v, eps)` keeps
+// the reference's std::max semantics. DESIGN.md section 4 records what bounds
+// it on B200.
 #pragma once
 
 #include <cooperative_groups.h>

@@ -8,8 +8,7 @@ name=$1; flags=$2; shift 2
 obj=/tmp/ab_obj/$name
 rm -rf $obj; mkdir -p $obj build/ab/$name
 if [ $# -gt 0 ]; then
-  make -s -j10 -C paper_1908_01964_b200/csrc >/dev/null
-  cp build/csrc/*.o $obj/
+  cp build/csrc/*.o $obj/  # the main build's objects (build it first, from the main sources)
   for o in "$@"; do rm -f $obj/$o; done
 fi
 make -s -j10 -C paper_1908_01964_b200/csrc OUT=$PWD/build/ab/$name/librcscm_gpu.so OBJDIR=$obj \

@@ -213,8 +213,15 @@ __device__ __forceinline__ float tfma(float a, float b, float c) { return fmaf(a
 // registers) instead of one 256-thread CTA's worth (0).
 // PREM: fused precompute for M = PREM mics (0: read K1's sigma / tau arrays).
 // EPI (PREM > 0, complex128): the Wiener output (dry, image) as the epilogue.
+// WE > 0 (CL == 1): a ONE-WARP CTA per bin (32 threads, launch bounds 32 x MINB)
+// that holds the slots a CTA of WE warps x SPT/WE slots would, in the same
+// places: lane l's slot w * SPT/WE + k is frame k * 32 WE + 32 w + l, its
+// in-thread tree runs per group w, and the bin total is the WE warp totals in
+// block_total4's zero-padded order -- every result is bitwise that of the
+// WE-warp layout, with no barrier in the iteration loop and the per-iteration
+// lambda chain amortised over WE times the slots.
 template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
-          typename T = double, int PREM = 0, bool EPI = false>
+          typename T = double, int PREM = 0, bool EPI = false, int WE = 0>
 #ifndef RCSCM_K2_LB_THREADS
 #define RCSCM_K2_LB_THREADS 128  // MINB launch-bounds CTA size (tools may override)
 #endif
@@ -223,7 +230,7 @@ template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool D
 #endif
 // 256-thread CTAs: two per SM (<= 128 registers) with shared-memory constants
 // or, for clusters, with the scalar carried state (a slot in 12 registers)
-__global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
+__global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
                                   MINB ? MINB
                                        : ((SMEMC || (CL > 1 && DIRECT && !TRAJ && sizeof(T) == 8 && RCSCM_K2_SST)) ? 2 : 1))
     k_accel(AccelArgs P) {
@@ -238,6 +245,8 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
   __shared__ __align__(16) double cl_vals[2][16];
   __shared__ __align__(8) unsigned long long cl_bar[2];
   extern __shared__ __align__(16) unsigned char dyn_raw[];
+  static_assert(WE == 0 || (CL == 1 && !TRAJ && SPT % (WE ? WE : 1) == 0 && WE <= 4), "one-warp CTA layout");
+  constexpr int SPTH = WE ? SPT / WE : SPT;  // slots per emulated thread (WE > 0)
   const int NT = blockDim.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bin = blockIdx.x / CL;
@@ -249,6 +258,11 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
   const int64_t base = bin * J;
   const int64_t ldp = P.ld_p;
   auto pslot = [&](int64_t t) { return ldp ? bin + t * ldp : base + t; };  // r_h / r_u index
+  // frame of this thread's slot k
+  auto slot_t = [&](int k) -> int64_t {
+    if constexpr (WE > 0) return t0 + static_cast<int64_t>(k % SPTH) * (32 * WE) + (k / SPTH) * 32 + lane;
+    else return t0 + static_cast<int64_t>(k) * NT + tid;
+  };
   const double inv_M = P.inv_M;
   // shared planes ([k][tid], conflict-free): tax, (txx, dd) packed, and for
   // SMEMC 1 also cc
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
   if constexpr (XPRE) {
 #pragma unroll
     for (int k = 0; k < SPT; ++k) {
-      const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+      const int64_t t = slot_t(k);
       const int64_t tt = (FULL || t < t_end) ? t : t0;
       const int64_t s = base + tt;
 #pragma unroll
@@ -376,7 +390,7 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
   const T invMT = static_cast<T>(inv_M);
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
-    const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+    const int64_t t = slot_t(k);
     valid[k] = FULL || t < t_end;
     const int64_t s = base + (valid[k] ? t : t0);
     CT tk, sb;
@@ -488,10 +502,13 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
 #ifndef RCSCM_K2_UNROLL
 #define RCSCM_K2_UNROLL 2  // iteration-loop unroll (tools may override)
 #endif
-    constexpr int kUnroll = RCSCM_K2_UNROLL;
+#ifndef RCSCM_K2_W1_UNROLL
+#define RCSCM_K2_W1_UNROLL 1  // ... for the one-warp CTAs
+#endif
+    constexpr int kUnroll = WE ? RCSCM_K2_W1_UNROLL : RCSCM_K2_UNROLL;
 #pragma unroll kUnroll
     for (int it = 0; it < P.iters; ++it) {
-      const int buf = it & 1;
+      [[maybe_unused]] const int buf = it & 1;
       K2_PROBE(0, rh[0]);
       const T raaT = static_cast<T>(raa);
       // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
@@ -525,16 +542,22 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
         term[k] = (FULL || valid[k]) ? (SCL ? tfma(rr, iru, gk) : rr * iru) : T(0);
         g[k] = gk;
       }
-      // fixed pairwise tree over the thread's slots, then the warp total (FP64)
+      // fixed pairwise tree over the thread's slots (per emulated thread for
+      // WE > 0), then the warp total (FP64)
 #pragma unroll
-      for (int w = 1; w < SPT; w <<= 1) {
+      for (int h = 0; h < SPT; h += SPTH) {
 #pragma unroll
-        for (int k = 0; k + w < SPT; k += 2 * w) term[k] += term[k + w];
+        for (int w = 1; w < SPTH; w <<= 1) {
+#pragma unroll
+          for (int k = 0; k + w < SPTH; k += 2 * w) term[h + k] += term[h + k + w];
+        }
       }
       K2_PROBE(1, term[0]);
       const double part = warp_total(static_cast<double>(term[0]));
       K2_PROBE(2, part);
-      if (lane == 0) red[buf][warp] = part;
+      if constexpr (WE == 0) {
+        if (lane == 0) red[buf][warp] = part;
+      }
       // (2) everything that does not need the new lambda, overlapping the
       //     reduction: r_h (solver_accel.hpp:134-141) and (non-DIRECT) the two
       //     halves of the r_u update, which is affine in 1/lambda_new
@@ -565,10 +588,16 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
         p0[k] = tfma(m2g, re0, tfma(gq, taaM, xk));
         p1[k] = tfma(m2g * s2T, re1, tfma(gq, s2M, dk));          // s_ab s_bx = |s_ab|^2 c
       }
-      __syncthreads();
+      if constexpr (WE == 0) __syncthreads();
       K2_PROBE(3, 0.0);
       double total = 0.0;
-      if constexpr (CL == 1) {
+      if constexpr (WE > 0) {
+        // block_total4 of the WE emulated warps' totals, zero-padded
+        double pw[4] = {part, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int w = 1; w < WE; ++w) pw[w] = warp_total(static_cast<double>(term[w * SPTH]));
+        total = (pw[0] + pw[1]) + (pw[2] + pw[3]);
+      } else if constexpr (CL == 1) {
         total = NT <= 128 ? block_total4(red[buf]) : block_total8(red[buf]);
       } else {
         // CTA partial -> cluster: lane r < CL of warp 0 sends this CTA's partial
@@ -766,7 +795,7 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         if (valid[k]) {
-          const int64_t s = base + t0 + static_cast<int64_t>(k) * NT + tid;
+          const int64_t s = base + slot_t(k);
           const double g = rh[k] / fma(rh[k], raa, ru[k]);
           double2 r = rax[k];
           if constexpr (SST) {  // rho_ax at the final lambda
@@ -787,7 +816,7 @@ __global__ void __launch_bounds__(MINB ? RCSCM_K2_LB_THREADS : 256,
 #pragma unroll
   for (int k = 0; k < SPT; ++k) {
     if (valid[k]) {
-      const int64_t t = t0 + static_cast<int64_t>(k) * NT + tid;
+      const int64_t t = slot_t(k);
       if constexpr (F32) {
         P.r_h_f[base + t] = rh[k];
         P.r_u_f[base + t] = ru[k];

@@ -3,6 +3,10 @@
 
 #include "accel_launch.cuh"
 
+#ifndef RCSCM_K2_W1_MIN_BINS
+#define RCSCM_K2_W1_MIN_BINS 2048  // one-warp CTAs from this many bins on (0: never)
+#endif
+
 namespace rcscm {
 
 AccelCfg choose_accel_cfg(int64_t J, bool f32) {
@@ -76,6 +80,16 @@ bool accel_fusable(const AccelCfg& g, int M) {
   if (!(M == 2 || M == 4 || M == 8) || g.f32 || !g.direct) return false;
   // the tuned single-CTA shape, or a cluster with its constants in registers
   return (g.cl == 1 && g.full && g.smem == 0 && g.minb == RCSCM_K2_MINB1 && g.nt <= 128) || (g.cl >= 2 && g.smem == 0);
+}
+
+void accel_one_warp(AccelCfg& g, int64_t nb) {
+  const char* e = std::getenv("RCSCM_ACCEL_W1");
+  const int64_t min_nb = e ? std::atoll(e) : RCSCM_K2_W1_MIN_BINS;
+  if (min_nb <= 0 || nb < min_nb) return;
+  if (!g.prem || g.cl != 1 || !g.full || g.smem != 0 || g.nt != 64 || g.spt != 5 || g.we) return;
+  g.we = 2;
+  g.nt = 32;
+  g.spt = 10;
 }
 
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {

@@ -7,9 +7,9 @@
 namespace rcscm {
 
 template <int SPT, int CL, bool FULL, bool TRAJ, int SMEMC, int MINB = 0, bool DIRECT = false,
-          typename T = double, int PREM = 0, bool EPI = false>
+          typename T = double, int PREM = 0, bool EPI = false, int WE = 0>
 cudaError_t launch_accel_t(cudaStream_t s, const AccelArgs& A, int nt) {
-  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI>;
+  auto kern = k_accel<SPT, CL, FULL, TRAJ, SMEMC, MINB, DIRECT, T, PREM, EPI, WE>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(A.nb * CL));
   cfg.blockDim = dim3(nt);

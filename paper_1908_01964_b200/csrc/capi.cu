@@ -245,6 +245,7 @@ void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A, int prem = 0) {
   if (A.nb * A.J == 0) return;
   AccelCfg g = choose_accel_cfg(A.J, f32(c));
   g.prem = prem;
+  accel_one_warp(g, A.nb);
   if (!g.cl) {
     // longer than a 16-CTA cluster holds (32768 frames): stream the iterate
     // through HBM (two launches per iteration; complex128, sigma / tau from K1)
@@ -463,6 +464,7 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   AccelCfg g = choose_accel_cfg(J);
   if (!g.cl) return false;
   if (accel_fusable(g, M) && opt->iters > 0) g.prem = M;  // one kernel per chunk: precompute fused into K2
+  accel_one_warp(g, I / nch);
   for (int k = 0; k < 4; ++k)
     if (!c->aux[k]) CK(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
   for (int k = 0; k < kMaxChunks + 6; ++k)

@@ -42,6 +42,7 @@ struct AccelCfg {
   bool direct;  // r_u from rho(lambda_new) after the reduction (k_accel DIRECT), MINB path only
   bool f32;     // complex64 / FP32 per-slot arithmetic
   int prem = 0;  // fused precompute for M = prem mics (k_accel PREM; 0 = read K1's arrays)
+  int we = 0;    // one-warp CTAs emulating a CTA of `we` warps (k_accel WE; fused shapes only)
 };
 // Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL /
 // RCSCM_ACCEL_SMEM / RCSCM_ACCEL_MINB force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
@@ -51,6 +52,11 @@ cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& cfg
 // tuned single-CTA complex128 variant, M in {2, 4, 8}); env RCSCM_FUSE_PRE=0
 // disables it
 bool accel_fusable(const AccelCfg& cfg, int M);
+// For a fused configuration over nb bins: switch to one-warp CTAs (k_accel WE)
+// where that layout is instantiated and the batch fills the GPU with them;
+// every result stays bitwise the same (env RCSCM_ACCEL_W1 = the fewest bins
+// that take it, 0 disables it)
+void accel_one_warp(AccelCfg& cfg, int64_t nb);
 // Algorithm 2 streaming the iterate through HBM for bins longer than the on-chip
 // kernel holds (accel_stream.cuh; needs K1's sigma / tau arrays, complex128):
 // 2 launches per iteration; partial: [nb][accel_stream_chunks(J)], lam_buf: 4 nb.

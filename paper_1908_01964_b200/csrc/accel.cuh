@@ -290,6 +290,18 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
   // lambda on the BASELINE recipe (the one-iteration bars are 1e-9 of the
   // binary128 truth; tests).
   constexpr bool SST = DIRECT && !F32 && !TRAJ && RCSCM_K2_SST;
+#ifndef RCSCM_K2_SST2
+#define RCSCM_K2_SST2 1  // folded scalar-state arithmetic (tools may override)
+#endif
+  // SST2: the same scalar state with three operations per slot-iteration folded away.
+  //   lambda term: g + (g w + |c|^2) / r~_u with w = g |rho~|^2 + b2 equals
+  //     (g (q + b2) + |c|^2) / r~_u, q = r~_u + g |rho~|^2 (r_h's q): one add and one
+  //     FMA, and the thread's sum accumulates by FMA (two interleaved chains per
+  //     emulated thread, fixed order) instead of an add tree over finished terms;
+  //   the state advance reuses r_u's re = |rho~|^2 - (ds / 2) b2:
+  //     b2' = b2 - 2 ds |c|^2,  |rho~ + c ds|^2 = re - (ds / 2) b2'.
+  // 20 FP64 operations per slot-iteration + 1 per emulated thread instead of 22 + the tree.
+  constexpr bool SST2 = SST && RCSCM_K2_SST2;
   constexpr bool CARRY = DIRECT && !F32 && (CL > 1 || SMEMC >= 1) && !SST && RCSCM_K2_CARRY;
   CT* s_tax = reinterpret_cast<CT*>(dyn_raw);
   CT* s_xd = s_tax + SPT * NT;
@@ -514,12 +526,24 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
       // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
       //     (solver_accel.hpp:67-76, :143-158).
       T g[SPT], term[SPT];
+      [[maybe_unused]] T qv[SST2 ? SPT : 1], irv[SST2 ? SPT : 1];
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         const T D = tfma(rh[k], raaT, ru[k]);  // r~_u + r~_h rho~_aa
         const T inv = rcp_pos(D * ru[k]);
         const T gk = tfma(rh[k] * inv, ru[k], fault);  // gamma (+ gamma_fault)
         const T iru = D * inv;                          // 1 / r~_u
+        if constexpr (SST2) {
+          // term[k] holds the numerator g (q + b2) + |c|^2 (|s_bx|^2 when s_ab = 0)
+          const T ak = get_xd(k).y;
+          const T q = tfma(gk, rax[k].x, ru[k]);
+          qv[k] = q;
+          irv[k] = iru;
+          g[k] = gk;
+          if constexpr (SCL) term[k] = (FULL || valid[k]) ? tfma(gk, q + rax[k].y, ak) : T(0);
+          else term[k] = (FULL || valid[k]) ? ak : T(0);
+          continue;
+        }
         if constexpr (SST) {
           // |c - g rho~|^2 = |c|^2 + g (g |rho~|^2 + b2); |s_bx|^2 / r~_u when s_ab = 0
           const T ak = get_xd(k).y;
@@ -544,6 +568,21 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
       }
       // fixed pairwise tree over the thread's slots (per emulated thread for
       // WE > 0), then the warp total (FP64)
+      if constexpr (SST2) {
+        // sum_k term[k] / r~_u[k] per emulated thread: two interleaved FMA chains
+        // (even / odd k) and one add -- a fixed order, the same in both layouts
+#pragma unroll
+        for (int h = 0; h < SPT; h += SPTH) {
+          T ce = term[h] * irv[h];
+          [[maybe_unused]] T co = SPTH > 1 ? term[h + (SPTH > 1 ? 1 : 0)] * irv[h + (SPTH > 1 ? 1 : 0)] : T(0);
+#pragma unroll
+          for (int k = 2; k < SPTH; ++k) {
+            if (k & 1) co = tfma(term[h + k], irv[h + k], co);
+            else ce = tfma(term[h + k], irv[h + k], ce);
+          }
+          term[h] = SPTH > 1 ? ce + co : ce;
+        }
+      } else {
 #pragma unroll
       for (int h = 0; h < SPT; h += SPTH) {
 #pragma unroll
@@ -551,6 +590,7 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
 #pragma unroll
           for (int k = 0; k + w < SPTH; k += 2 * w) term[h + k] += term[h + k + w];
         }
+      }
       }
       K2_PROBE(1, term[0]);
       const double part = warp_total(static_cast<double>(term[0]));
@@ -570,7 +610,9 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
 #pragma unroll
       for (int k = 0; k < SPT; ++k) {
         if constexpr (DIRECT) {
-          const T q = tfma(g[k], SST ? rax[k].x : cnorm(rax[k]), ru[k]);
+          T q;
+          if constexpr (SST2) q = qv[k];
+          else q = tfma(g[k], SST ? rax[k].x : cnorm(rax[k]), ru[k]);
           const T gq = g[k] * q;
           rh[k] = floor_eps(tfma(gq, k1, k2), epsT);
           p0[k] = gq;          // gamma q
@@ -697,7 +739,10 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
           // Re(rho~ conj(rho~ + c ds)) = |rho~|^2 - (ds / 2) b2
           const T re = SCL ? tfma(hds, rax[k].y, rax[k].x) : rax[k].x;
           ru[k] = floor_eps(tfma(p1[k], re, tfma(p0[k], raaM, rxx)), epsT);
-          if constexpr (SCL) {
+          if constexpr (SCL && SST2) {
+            rax[k].y = tfma(m2ds, xd.y, rax[k].y);
+            rax[k].x = tfma(hds, rax[k].y, re);
+          } else if constexpr (SCL) {
             rax[k].x = tfma(dsT, tfma(dsT, xd.y, -rax[k].y), rax[k].x);
             rax[k].y = tfma(m2ds, xd.y, rax[k].y);
           }

@@ -447,7 +447,9 @@ def run_gpu(args):
     fp64_peak, probe_ms = fp_probe(ctx)
     k2_avg = sum(step_ms) / len(step_ms)
     roofline = accel_roofline(k2_avg, B * I * J, iters, M, fp64_peak,
-                              kernel="k_accel<5,1,FULL,-,0,3,DIRECT,double,PREM=4> (K2: sigma/tau precompute fused "
+                              kernel=("k_accel<10,1,FULL,-,0,8,DIRECT,double,PREM=4,-,WE=2> (one-warp CTAs)" if B * I >= 2048
+                                      else "k_accel<5,1,FULL,-,0,8,DIRECT,double,PREM=4> (64 x 5 CTAs)")
+                              + " (K2: sigma/tau precompute fused "
                                      "into the prologue, then the on-chip Algorithm 2 iterations), this rank's "
                                      f"{B} utterances x {I} bins", ncu_key="k_accel_c3")
     roofline["peak_probe"] = {"tflops": fp64_peak, "ms": probe_ms, "sm_mhz_during_bench": None}

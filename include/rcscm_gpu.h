@@ -136,11 +136,6 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* ctx);
 const char* rcscm_gpu_last_error(void);
 /* Number of CUDA kernels this context has launched so far. */
 int64_t rcscm_gpu_launch_count(const rcscm_gpu_ctx* ctx);
-/* Shape of the last Algorithm 2 on-chip launch (diagnostics / tests): CTAs per
-   cluster, threads per CTA, slots per thread and bin, bins in flight per cluster
-   (2 = the two-bin kernel k_accel_db). Each pointer may be NULL. */
-int rcscm_gpu_last_accel_shape(const rcscm_gpu_ctx* ctx, int* cluster, int* threads, int* slots,
-                               int* bins_in_flight);
 
 /* ---- reference entry points (host buffers) ------------------------------ */
 /* model.hpp:58-90 */

@@ -121,7 +121,6 @@ SIGNATURES = {
     "rcscm_gpu_destroy": (None, [_vp]),
     "rcscm_gpu_last_error": (ctypes.c_char_p, []),
     "rcscm_gpu_launch_count": (ctypes.c_int64, [_vp]),
-    "rcscm_gpu_last_accel_shape": (ctypes.c_int, [_vp] + [ctypes.POINTER(ctypes.c_int)] * 4),
     "rcscm_gpu_build_noise_scm": (ctypes.c_int, [_vp, _i64, _i64, ctypes.c_int, _dp, _dp, _dp, ctypes.c_int,
                                                  ctypes.c_double, _dp, _dp, _dp, _dp]),
     "rcscm_gpu_init_params": (ctypes.c_int, [_vp, ctypes.POINTER(CInputs), ctypes.c_int, _dp, _dp, _dp, _dp, _dp,

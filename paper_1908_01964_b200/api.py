@@ -202,18 +202,6 @@ class GpuContext:
         return int(self._lib.rcscm_gpu_launch_count(self._h))
 
     @property
-    def last_accel_shape(self):
-        """(CTAs per cluster, threads per CTA, slots per thread and bin, bins in
-        flight per cluster) of the last Algorithm 2 on-chip launch."""
-        v = [ctypes.c_int() for _ in range(4)]
-        self._lib.rcscm_gpu_last_accel_shape(self._h, *[ctypes.byref(x) for x in v])
-        return tuple(x.value for x in v)
-
-    @property
-    def last_accel_db(self) -> bool:
-        return self.last_accel_shape[3] == 2
-
-    @property
     def stream(self) -> int:
         return int(self._lib.rcscm_gpu_stream(self._h) or 0)
 

@@ -7,14 +7,7 @@
 #define RCSCM_K2_W1_MIN_BINS 2048  // one-warp CTAs from this many bins on (0: never)
 #endif
 
-#ifndef RCSCM_K2_DB
-#define RCSCM_K2_DB 0  // two bins in flight per cluster (env RCSCM_ACCEL_DB overrides)
-#endif
-
 namespace rcscm {
-
-cudaError_t launch_accel_db_full(cudaStream_t s, const AccelArgs& A, const AccelCfg& g);
-cudaError_t launch_accel_db_part(cudaStream_t s, const AccelArgs& A, const AccelCfg& g);
 
 AccelCfg choose_accel_cfg(int64_t J, bool f32) {
   AccelCfg best{0, 0, 0, false, 0, 0, false, f32};
@@ -99,30 +92,8 @@ void accel_one_warp(AccelCfg& g, int64_t nb) {
   g.spt = 10;
 }
 
-void accel_db(AccelCfg& g, int64_t J, int64_t nb) {
-  const char* e = std::getenv("RCSCM_ACCEL_DB");
-  const int on = e ? std::atoi(e) : RCSCM_K2_DB;
-  if (!on || !g.prem || g.cl < 2 || g.smem != 0 || g.f32 || g.we || nb < 2) return;
-  for (int cl : {2, 4, 8, 16}) {
-    const int64_t jc = (J + cl - 1) / cl;
-    if (jc > 256 * 4) continue;
-    int64_t nt = (jc + 3) / 4;
-    nt = (nt + 31) / 32 * 32;
-    g.db_cl = cl;
-    g.db_nt = static_cast<int>(nt);
-    g.db_full = nt * 4 == jc && jc * cl == J;
-    return;
-  }
-}
-
-bool accel_takes_db(const AccelArgs& A, const AccelCfg& g) {
-  return g.db_cl && !A.dry_w && !A.image_w && !A.traj_r_h && !A.obj_part;
-}
-
 cudaError_t launch_accel(cudaStream_t s, const AccelArgs& A, const AccelCfg& g) {
   if (A.nb * A.J == 0) return cudaSuccess;
-  if (accel_takes_db(A, g))
-    return g.db_full ? launch_accel_db_full(s, A, g) : launch_accel_db_part(s, A, g);
   if (g.prem && g.cl == 1) return launch_accel_fused(s, A, g);
   switch (g.cl) {
     case 1: return launch_accel_cl1(s, A, g);

@@ -246,7 +246,6 @@ void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A, int prem = 0) {
   AccelCfg g = choose_accel_cfg(A.J, f32(c));
   g.prem = prem;
   accel_one_warp(g, A.nb);
-  accel_db(g, A.J, A.nb);
   if (!g.cl) {
     // longer than a 16-CTA cluster holds (32768 frames): stream the iterate
     // through HBM (two launches per iteration; complex128, sigma / tau from K1)
@@ -261,7 +260,6 @@ void run_accel(rcscm_gpu_ctx* c, const AccelArgs& A, int prem = 0) {
     c->launched(e, n);
     return;
   }
-  c->note_k2(g, accel_takes_db(A, g));
   c->launched(launch_accel(c->stream, A, g));
 }
 
@@ -467,7 +465,6 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
   if (!g.cl) return false;
   if (accel_fusable(g, M) && opt->iters > 0) g.prem = M;  // one kernel per chunk: precompute fused into K2
   accel_one_warp(g, I / nch);
-  accel_db(g, J, I / nch);
   for (int k = 0; k < 4; ++k)
     if (!c->aux[k]) CK(cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking));
   for (int k = 0; k < kMaxChunks + 6; ++k)
@@ -582,10 +579,7 @@ bool run_accel_pipelined(rcscm_gpu_ctx* c, const rcscm_inputs* in, const rcscm_p
       A.r_u_in += off;
     }
     CK(cudaEventRecord(c->evt[2 * ch], cs));
-    if (opt->iters > 0) {
-      c->note_k2(g, accel_takes_db(A, g));
-      c->launched(launch_accel(cs, A, g));
-    }
+    if (opt->iters > 0) c->launched(launch_accel(cs, A, g));
     CK(cudaEventRecord(c->evt[2 * ch + 1], cs));
     if (!colmajor) {
       c->launched(launch_to_ij(cs, c->rh.as<double>() + off, t1 + i0, 1, Ic, J, I));
@@ -1036,15 +1030,6 @@ void rcscm_gpu_destroy(rcscm_gpu_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->own_stream) cudaStreamDestroy(c->stream);
   delete c;
-}
-
-int rcscm_gpu_last_accel_shape(const rcscm_gpu_ctx* c, int* cluster, int* threads, int* slots, int* bins_in_flight) {
-  if (!c) return RCSCM_INVALID_INPUT;
-  if (cluster) *cluster = c->last_k2[0];
-  if (threads) *threads = c->last_k2[1];
-  if (slots) *slots = c->last_k2[2];
-  if (bins_in_flight) *bins_in_flight = c->last_k2[3];
-  return RCSCM_OK;
 }
 
 int64_t rcscm_gpu_launch_count(const rcscm_gpu_ctx* c) {

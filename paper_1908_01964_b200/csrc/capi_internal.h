@@ -105,15 +105,6 @@ struct rcscm_gpu_ctx {
   cudaStream_t stream = nullptr;
   bool own_stream = false;
   int64_t launches = 0;
-  // shape of the last K2 launch: cluster size, threads per CTA, slots per thread
-  // and bin, bins in flight per cluster (rcscm_gpu_last_accel_shape)
-  int last_k2[4] = {0, 0, 0, 0};
-  void note_k2(const rcscm::AccelCfg& g, bool db) {
-    last_k2[0] = db ? g.db_cl : g.cl;
-    last_k2[1] = db ? g.db_nt : g.nt;
-    last_k2[2] = db ? 4 : g.spt;
-    last_k2[3] = db ? 2 : 1;
-  }
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // two copy streams (one DMA engine each: a single H2D stream reaches half the
   // PCIe rate on B200 hosts) and a compute stream for the pipelined entry points

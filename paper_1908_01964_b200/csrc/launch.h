@@ -43,9 +43,6 @@ struct AccelCfg {
   bool f32;     // complex64 / FP32 per-slot arithmetic
   int prem = 0;  // fused precompute for M = prem mics (k_accel PREM; 0 = read K1's arrays)
   int we = 0;    // one-warp CTAs emulating a CTA of `we` warps (k_accel WE; fused shapes only)
-  // two bins in flight per cluster (k_accel_db, accel_db.cuh): cluster size, CTA size, no masks
-  int db_cl = 0, db_nt = 0;
-  bool db_full = false;
 };
 // Chooses the configuration for J frames; env RCSCM_ACCEL_SPT / RCSCM_ACCEL_CL /
 // RCSCM_ACCEL_SMEM / RCSCM_ACCEL_MINB force a choice (tuning). Returns cl == 0 when J exceeds the on-chip capacity.
@@ -60,12 +57,6 @@ bool accel_fusable(const AccelCfg& cfg, int M);
 // every result stays bitwise the same (env RCSCM_ACCEL_W1 = the fewest bins
 // that take it, 0 disables it)
 void accel_one_warp(AccelCfg& cfg, int64_t nb);
-// For a fused cluster configuration over >= 2 bins: also set the two-bins-in-flight
-// shape (k_accel_db: 4 slots of each bin per thread, twice the CTAs per bin), which
-// launch_accel takes when no epilogue / recording is asked for (env RCSCM_ACCEL_DB)
-void accel_db(AccelCfg& cfg, int64_t J, int64_t nb);
-// true if launch_accel runs these arguments through k_accel_db
-bool accel_takes_db(const AccelArgs& A, const AccelCfg& cfg);
 // Algorithm 2 streaming the iterate through HBM for bins longer than the on-chip
 // kernel holds (accel_stream.cuh; needs K1's sigma / tau arrays, complex128):
 // 2 launches per iteration; partial: [nb][accel_stream_chunks(J)], lam_buf: 4 nb.

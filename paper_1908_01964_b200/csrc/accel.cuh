@@ -518,15 +518,6 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
 #define RCSCM_K2_W1_UNROLL 1  // ... for the one-warp CTAs
 #endif
     constexpr int kUnroll = WE ? RCSCM_K2_W1_UNROLL : RCSCM_K2_UNROLL;
-#ifndef RCSCM_K2_ROT
-#define RCSCM_K2_ROT 0  // rotated iteration loop (tools may override)
-#endif
-    // ROT: the loop is rotated so that its back edge sits where every slot's
-    // lambda term is complete anyway: phase (1) of iteration it + 1 shares a basic
-    // block with phase (3) of iteration it (the floors' integer tail then overlaps
-    // the next D / reciprocal work in ptxas's schedule). The same arithmetic in the
-    // same order; one unused phase (1) after the last iteration.
-    constexpr bool ROT = RCSCM_K2_ROT && WE > 0;
     T g[SPT], term[SPT];
     [[maybe_unused]] T qv[SST2 ? SPT : 1], irv[SST2 ? SPT : 1];
     // (1) lambda-critical values first: gamma, 1/r~_u and the residual norm
@@ -599,12 +590,11 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
       }
       }
     };
-    if constexpr (ROT) phase1();
 #pragma unroll kUnroll
     for (int it = 0; it < P.iters; ++it) {
       [[maybe_unused]] const int buf = it & 1;
       K2_PROBE(0, rh[0]);
-      if constexpr (!ROT) phase1();
+      phase1();
       K2_PROBE(1, term[0]);
       const double part = warp_total(static_cast<double>(term[0]));
       K2_PROBE(2, part);
@@ -792,7 +782,6 @@ __global__ void __launch_bounds__(WE ? 32 : (MINB ? RCSCM_K2_LB_THREADS : 256),
         }
       }
       K2_PROBE(5, ru[0]);
-      if constexpr (ROT) phase1();
       if constexpr (TRAJ) {
         if (P.traj_r_h) {
 #pragma unroll

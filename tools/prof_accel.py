@@ -16,8 +16,11 @@ ap.add_argument("--J", type=int, default=None)
 ap.add_argument("--B", type=int, default=1)
 ap.add_argument("--c64", action="store_true")
 ap.add_argument("--unfused", action="store_true", help="K2 alone (forms from K1's arrays)")
+ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
 a = ap.parse_args()
-c = synth.CONFIGS[a.cfg]
+c = dict(synth.CONFIGS[a.cfg])
+if a.iters is not None:
+    c["iters"] = a.iters
 utts = synth.make_config(a.cfg, utterances=a.B, I=a.I, J=a.J)
 X, W, A, T, V = synth.stack(utts)
 s = torch.cuda.Stream()

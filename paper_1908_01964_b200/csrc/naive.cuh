@@ -194,12 +194,20 @@ struct NaiveArgs {
 
 // One CTA per frequency bin runs every iteration (solver_naive.hpp:427-435
 // with the per-bin fusion of :319-386); threads stride over the bin's frames.
-template <int M, int NT>
+// EMU (NT = 64): the CTA holds the frames a 128-thread CTA would, thread tid those of
+// threads tid and tid + 64, keeps their two lambda accumulators apart (rounds of even
+// and odd parity) and leaves four warp partials in the 128-thread layout's order, so
+// every bit equals the 128-thread result: the CTA size may then follow the batch
+// size (J = 320 runs 5 exact rounds of 64 instead of 3 of 128 with half of the last
+// idle) without a sharded run differing from an unsharded one.
+template <int M, int NT, bool EMU = false>
 __global__ void __launch_bounds__(NT) k_naive(NaiveArgs P) {
+  static_assert(!EMU || NT == 64, "EMU emulates 128 threads with 64");
+  constexpr int NW = EMU ? 4 : NT / 32;  // warp partials of the (emulated) layout
   __shared__ double2 sa[M], sb[M], sw[M], su[M];
   __shared__ double2 sRp[M * M], sRut[M * M];
   __shared__ double sc[2];  // beta0 = Re b^H R~_u b, beta1 = Re b^H R~_u^{-1} b
-  __shared__ double red[2][NT / 32];
+  __shared__ double red[2][NW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bin = blockIdx.x;
   const int64_t J = P.J;
@@ -247,7 +255,9 @@ __global__ void __launch_bounds__(NT) k_naive(NaiveArgs P) {
     __syncthreads();
     const double beta0 = sc[0], beta1 = sc[1];
     double acc = 0.0;
-    for (int64_t t = tid; t < J; t += NT) {
+    [[maybe_unused]] double acc_hi = 0.0;  // EMU: the accumulator of emulated thread tid + 64
+    [[maybe_unused]] int round = 0;
+    for (int64_t t = tid; t < J; t += NT, ++round) {
       const int64_t slot = bin * J + t;
       const double rh = P.r_h[slot], ru = P.r_u[slot];
       double2 x[M];
@@ -320,14 +330,22 @@ __global__ void __launch_bounds__(NT) k_naive(NaiveArgs P) {
       const double Tb = ru * beta1 - ru2 * bzb + ru2 * cnorm(bz);
       P.r_h[slot] = std_max((hrh + P.beta) * inv_a2, P.eps);  // solver_naive.hpp:333-334
       P.scratch[slot] = make_double2(Ta, Tb);
-      acc += q / ru;
+      if (EMU && (round & 1)) acc_hi += q / ru; else acc += q / ru;
     }
     acc = warp_sum(acc);
     const int buf = it & 1;
-    if (lane == 0) red[buf][warp] = acc;
+    if constexpr (EMU) {
+      acc_hi = warp_sum(acc_hi);
+      if (lane == 0) {
+        red[buf][warp] = acc;
+        red[buf][warp + 2] = acc_hi;
+      }
+    } else {
+      if (lane == 0) red[buf][warp] = acc;
+    }
     __syncthreads();
     double total = 0.0;
-    for (int w = 0; w < NT / 32; ++w) total += red[buf][w];
+    for (int w = 0; w < NW; ++w) total += red[buf][w];
     const double lam_new = std_max(total / static_cast<double>(J), P.eps);
     const double d = lam_new - lam;
     const double den = fma(d, beta1, 1.0);

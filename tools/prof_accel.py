@@ -17,6 +17,7 @@ ap.add_argument("--B", type=int, default=1)
 ap.add_argument("--c64", action="store_true")
 ap.add_argument("--unfused", action="store_true", help="K2 alone (forms from K1's arrays)")
 ap.add_argument("--iters", type=int, default=None, help="override the config's iteration count")
+ap.add_argument("--epi", action="store_true", help="solve + extract in one call (K2 with the fused Wiener epilogue)")
 a = ap.parse_args()
 c = dict(synth.CONFIGS[a.cfg])
 if a.iters is not None:
@@ -40,7 +41,7 @@ for r in range(a.reps + 5):  # the first 5 are warm-up (clocks ramp after an idl
     elif a.unfused:
         ctx.session_run(C.STAGE_ACCEL, c["iters"], h)
     else:  # the bench step: precompute fused into K2
-        ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL, c["iters"], h)
+        ctx.session_run(C.STAGE_RESET | C.STAGE_PRECOMPUTE | C.STAGE_ACCEL | (C.STAGE_WIENER if a.epi else 0), c["iters"], h)
     e1.record(s)
     ev.append((e0, e1))
 torch.cuda.synchronize()

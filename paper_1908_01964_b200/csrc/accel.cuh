@@ -27,10 +27,11 @@
 // non-DIRECT variant forms r_u as P0 + P1/lambda_new with all but three FMAs
 // before the reduction).
 //
-// Instruction budget per slot-iteration (47 canonical flops): 22 FP64 ops
-// per slot with the scalar carried state (SST, below; 26 with the complex
-// rho~_ax) + the per-iteration lambda chain and trees amortised over the
-// thread's slots + 1 MUFU.RCP64H; floors run on the integer ALUs. The
+// Instruction budget per slot-iteration (47 canonical flops): 20 FP64 ops
+// per slot with the scalar carried state and its folded arithmetic (SST /
+// SST2, below; 22 unfolded, 26 with the complex rho~_ax) + the per-iteration
+// lambda chain and sums amortised over the thread's slots + 1 MUFU.RCP64H;
+// floors run on the integer ALUs. The
 // reference's two divisions share one reciprocal (inv = 1/(D r~_u) gives
 // gamma = r~_h r~_u inv and 1/r~_u = D inv); |s_ab|^2 leaves the per-slot
 // lambda term (scaled residual); gamma_fault rides in an FMA; 1/M is folded

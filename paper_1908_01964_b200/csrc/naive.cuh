@@ -200,10 +200,11 @@ struct NaiveArgs {
 // every bit equals the 128-thread result: the CTA size may then follow the batch
 // size (J = 320 runs 5 exact rounds of 64 instead of 3 of 128 with half of the last
 // idle) without a sharded run differing from an unsharded one.
-// (the 64-thread CTA of M <= 4 is held to 168 registers -- 16 bytes of spills at M = 4 --
-// so six of them, three warps per SM sub-partition, share an SM)
+// (for M <= 4 the kernel is held to 168 registers -- 8 bytes of spills at M = 4 -- so
+// twelve warps, three per SM sub-partition, share an SM: six 64-thread or three
+// 128-thread CTAs)
 template <int M, int NT, bool EMU = false>
-__global__ void __launch_bounds__(NT, (EMU && M <= 4) ? 6 : 1) k_naive(NaiveArgs P) {
+__global__ void __launch_bounds__(NT, M <= 4 ? 384 / NT : 1) k_naive(NaiveArgs P) {
   static_assert(!EMU || NT == 64, "EMU emulates 128 threads with 64");
   constexpr int NW = EMU ? 4 : NT / 32;  // warp partials of the (emulated) layout
   __shared__ double2 sa[M], sb[M], sw[M], su[M];
